@@ -1,0 +1,325 @@
+/*
+ * dcomp_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain-C restatement of the CPU reference's hot-path arithmetic
+ * (arXiv 2502.15443 reference package `dcomp`, /root/reference/pkg/src/dcomp).
+ * It exists to CHECK the CUDA product path: only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference leg may load it.  Nothing in
+ * paper_2502_15443_b200/ links or calls this file.
+ *
+ * Each function cites the reference file:line it restates.  Parity of this
+ * restatement is pinned against golden vectors produced by the reference
+ * itself (tests/golden/make_golden.py), see tests/test_oracle_golden.py.
+ *
+ * Build: oracle/Makefile -> oracle/liboracle.so (gcc, -O3, -ffp-contract=off).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define PROB_BITS 12
+#define PROB_SCALE (1u << PROB_BITS)
+#define STATE_LOWER (1ull << 20)
+#define STATE_UPPER (1ull << 28)
+#define BLOCK 4096 /* ans.py:39 _BLOCK */
+
+/* ------------------------------------------------------------------ */
+/* Frequency normalization: ans.py:213-243 (_normalize).              */
+/* hist[256] byte counts -> freq[256] summing to 4096.                 */
+/* ------------------------------------------------------------------ */
+void or_normalize(const uint64_t *hist, uint32_t *freq) {
+    uint64_t n = 0;
+    int present = 0, last = -1;
+    for (int s = 0; s < 256; s++) {
+        n += hist[s];
+        if (hist[s]) { present++; last = s; }
+        freq[s] = 0;
+    }
+    if (present == 0) return;
+    if (present == 1) { /* ans.py:222-224 */
+        freq[last] = PROB_SCALE;
+        return;
+    }
+    int64_t alloc[256];
+    int64_t rem[256];
+    int64_t total = 0;
+    for (int s = 0; s < 256; s++) {
+        int64_t scaled = (int64_t)hist[s] * PROB_SCALE; /* ans.py:225 */
+        rem[s] = scaled % (int64_t)n;
+        if (hist[s]) {
+            int64_t a = scaled / (int64_t)n; /* ans.py:226 max(scaled//n, 1) */
+            alloc[s] = a < 1 ? 1 : a;
+        } else {
+            alloc[s] = 0;
+        }
+        total += alloc[s];
+    }
+    int64_t deficit = (int64_t)PROB_SCALE - total; /* ans.py:227 */
+    if (deficit > 0) {
+        /* ans.py:229: lexsort((arange, -(scaled % n))): remainder descending,
+         * ties on the lower symbol.  Stable insertion sort over 256 entries. */
+        int order[256];
+        for (int s = 0; s < 256; s++) order[s] = s;
+        for (int i = 1; i < 256; i++) {
+            int v = order[i], j = i - 1;
+            while (j >= 0 && rem[order[j]] < rem[v]) { order[j + 1] = order[j]; j--; }
+            order[j + 1] = v;
+        }
+        for (int i = 0; i < 256 && deficit > 0; i++) { /* ans.py:230-235 */
+            int s = order[i];
+            if (hist[s] > 0) { alloc[s] += 1; deficit -= 1; }
+        }
+    }
+    while (deficit < 0) { /* ans.py:236-240: repay from the first argmax */
+        int best = 0;
+        for (int s = 1; s < 256; s++)
+            if (alloc[s] > alloc[best]) best = s;
+        alloc[best] -= 1;
+        deficit += 1;
+    }
+    for (int s = 0; s < 256; s++) freq[s] = (uint32_t)alloc[s];
+}
+
+/* ans.py:246-253 (_pack_u12): 256 x u12 (clamped to 4095) -> 384 bytes. */
+void or_pack_u12(const uint32_t *freq, uint8_t *out) {
+    for (int i = 0; i < 128; i++) {
+        uint32_t a = freq[2 * i] > 4095 ? 4095 : freq[2 * i];
+        uint32_t b = freq[2 * i + 1] > 4095 ? 4095 : freq[2 * i + 1];
+        out[3 * i + 0] = (uint8_t)(a & 0xFF);
+        out[3 * i + 1] = (uint8_t)(((a >> 8) & 0x0F) | ((b & 0x0F) << 4));
+        out[3 * i + 2] = (uint8_t)((b >> 4) & 0xFF);
+    }
+}
+
+/* ans.py:256-262 (_unpack_u12) + ans.py:284-299 (AnsTable.from_bytes).
+ * Returns 0 ok, 2 = "invalid frequency table" (CorruptStreamError). */
+int or_unpack_table(const uint8_t *buf, uint32_t *freq) {
+    uint32_t total = 0;
+    int nz = 0, last = 0;
+    for (int i = 0; i < 128; i++) {
+        uint32_t b0 = buf[3 * i], b1 = buf[3 * i + 1], b2 = buf[3 * i + 2];
+        freq[2 * i] = b0 | ((b1 & 0x0F) << 8);
+        freq[2 * i + 1] = (b1 >> 4) | (b2 << 4);
+    }
+    for (int s = 0; s < 256; s++) {
+        total += freq[s];
+        if (freq[s]) { nz++; last = s; }
+    }
+    if (total == PROB_SCALE - 1 && nz == 1) { freq[last] = PROB_SCALE; return 0; }
+    return total == PROB_SCALE ? 0 : 2;
+}
+
+/* ------------------------------------------------------------------ */
+/* Reverse rANS encode: ans.py:55-68 (_enc_kernel).                    */
+/* Emits bytes into out[0..pos) in encoder order; the caller reverses.  */
+/* ------------------------------------------------------------------ */
+void or_encode(const uint8_t *data, uint64_t n, const uint32_t *freq, uint8_t *out,
+               uint64_t *pos_out, uint32_t *state_out) {
+    uint32_t cum[256];
+    uint32_t c = 0;
+    for (int s = 0; s < 256; s++) { cum[s] = c; c += freq[s]; } /* ans.py:301-304 */
+    uint64_t x = STATE_LOWER, pos = 0;
+    for (int64_t i = (int64_t)n - 1; i >= 0; i--) {
+        uint32_t s = data[i];
+        uint64_t f = freq[s];
+        uint64_t x_max = f << 16;
+        while (x >= x_max) { out[pos++] = (uint8_t)(x & 0xFF); x >>= 8; }
+        x = (x / f) * PROB_SCALE + cum[s] + (x % f);
+    }
+    *pos_out = pos;
+    *state_out = (uint32_t)x;
+}
+
+/* Full blob: table(384) | u32 LE final state | stream.  ans.py:316-330.
+ * out must hold 388 + 2n + 8 bytes.  Returns blob length. */
+uint64_t or_compress_blob(const uint8_t *data, uint64_t n, uint8_t *out, uint8_t *scratch) {
+    uint64_t hist[256] = {0};
+    uint32_t freq[256];
+    for (uint64_t i = 0; i < n; i++) hist[data[i]]++; /* ans.py:282 bincount */
+    or_normalize(hist, freq);
+    or_pack_u12(freq, out);
+    uint64_t pos;
+    uint32_t x;
+    or_encode(data, n, freq, scratch, &pos, &x);
+    out[384] = (uint8_t)(x & 0xFF);
+    out[385] = (uint8_t)((x >> 8) & 0xFF);
+    out[386] = (uint8_t)((x >> 16) & 0xFF);
+    out[387] = (uint8_t)((x >> 24) & 0xFF);
+    for (uint64_t i = 0; i < pos; i++) out[388 + i] = scratch[pos - 1 - i]; /* ans.py:324 reverse */
+    return 388 + pos;
+}
+
+/* ------------------------------------------------------------------ */
+/* Forward decode: ans.py:71-94 (_dec1) with the padded-payload         */
+/* semantics of ans.py:333-343 (bytes past plen read as zero).          */
+/* Returns 0 ok, 1 corrupt.                                             */
+/* ------------------------------------------------------------------ */
+static inline uint32_t rd(const uint8_t *p, uint64_t i, uint64_t plen) { return i < plen ? p[i] : 0u; }
+
+static void build_slots(const uint32_t *freq, uint64_t *tab) { /* ans.py:306-313 decode_table */
+    uint32_t cum = 0;
+    for (int s = 0; s < 256; s++) {
+        for (uint32_t k = 0; k < freq[s]; k++)
+            tab[cum + k] = (uint64_t)freq[s] | ((uint64_t)k << 16) | ((uint64_t)s << 32);
+        cum += freq[s];
+    }
+}
+
+int or_decode(const uint8_t *stream, uint64_t plen, uint32_t x0, const uint32_t *freq,
+              uint8_t *out, uint64_t n) {
+    uint64_t tab[PROB_SCALE];
+    build_slots(freq, tab);
+    uint64_t x = x0, p = 0;
+    for (uint64_t i = 0; i < n;) {
+        uint64_t end = i + BLOCK < n ? i + BLOCK : n;
+        for (uint64_t j = i; j < end; j++) {
+            uint64_t e = tab[x & (PROB_SCALE - 1)];
+            out[j] = (uint8_t)(e >> 32);
+            x = (e & 0xFFFF) * (x >> 12) + ((e >> 16) & 0xFFFF);
+            if (x < STATE_LOWER) {
+                x = (x << 8) | rd(stream, p++, plen);
+                if (x < STATE_LOWER) x = (x << 8) | rd(stream, p++, plen);
+            }
+        }
+        if (p > plen) return 1; /* ans.py:89-90 */
+        i = end;
+    }
+    return (x != STATE_LOWER || p != plen) ? 1 : 0; /* ans.py:92-94 */
+}
+
+/* 4-lane interleaved decode of four equal-length streams: ans.py:137-200
+ * (_dec4).  Same verdict rule per lane; returns a bad-lane bitmask, or 15
+ * when any lane over-read (caller re-runs lanes singly, ans.py:405-412).
+ * Used only to make the CPU baseline as fast as the reference. */
+int or_decode4(const uint8_t *const *streams, const uint64_t *plens, const uint32_t *x0s,
+               const uint32_t *const *freqs, uint8_t *const *outs, uint64_t n) {
+    static __thread uint64_t tabs[4][PROB_SCALE];
+    uint64_t x[4], p[4] = {0, 0, 0, 0};
+    for (int l = 0; l < 4; l++) { build_slots(freqs[l], tabs[l]); x[l] = x0s[l]; }
+    for (uint64_t i = 0; i < n;) {
+        uint64_t end = i + BLOCK < n ? i + BLOCK : n;
+        for (uint64_t j = i; j < end; j++) {
+            for (int l = 0; l < 4; l++) {
+                uint64_t e = tabs[l][x[l] & (PROB_SCALE - 1)];
+                outs[l][j] = (uint8_t)(e >> 32);
+                x[l] = (e & 0xFFFF) * (x[l] >> 12) + ((e >> 16) & 0xFFFF);
+                if (x[l] < STATE_LOWER) {
+                    x[l] = (x[l] << 8) | rd(streams[l], p[l]++, plens[l]);
+                    if (x[l] < STATE_LOWER) x[l] = (x[l] << 8) | rd(streams[l], p[l]++, plens[l]);
+                }
+            }
+        }
+        for (int l = 0; l < 4; l++)
+            if (p[l] > plens[l]) return 15;
+        i = end;
+    }
+    int bad = 0;
+    for (int l = 0; l < 4; l++)
+        if (x[l] != STATE_LOWER || p[l] != plens[l]) bad |= 1 << l;
+    return bad;
+}
+
+/* ------------------------------------------------------------------ */
+/* CRC-32/ISO-HDLC as zlib.crc32 (container.py:117,169,205,329).       */
+/* ------------------------------------------------------------------ */
+static uint32_t crc_tab[8][256];
+static int crc_ready = 0;
+static void crc_init(void) {
+    for (uint32_t i = 0; i < 256; i++) {
+        uint32_t c = i;
+        for (int k = 0; k < 8; k++) c = (c & 1) ? (c >> 1) ^ 0xEDB88320u : c >> 1;
+        crc_tab[0][i] = c;
+    }
+    for (uint32_t i = 0; i < 256; i++)
+        for (int t = 1; t < 8; t++) crc_tab[t][i] = (crc_tab[t - 1][i] >> 8) ^ crc_tab[0][crc_tab[t - 1][i] & 0xFF];
+    crc_ready = 1;
+}
+uint32_t or_crc32(const uint8_t *p, uint64_t n, uint32_t crc) {
+    if (!crc_ready) crc_init();
+    crc = ~crc;
+    while (n >= 8) {
+        uint32_t lo = crc ^ ((uint32_t)p[0] | (uint32_t)p[1] << 8 | (uint32_t)p[2] << 16 | (uint32_t)p[3] << 24);
+        uint32_t hi = (uint32_t)p[4] | (uint32_t)p[5] << 8 | (uint32_t)p[6] << 16 | (uint32_t)p[7] << 24;
+        crc = crc_tab[7][lo & 0xFF] ^ crc_tab[6][(lo >> 8) & 0xFF] ^ crc_tab[5][(lo >> 16) & 0xFF] ^
+              crc_tab[4][lo >> 24] ^ crc_tab[3][hi & 0xFF] ^ crc_tab[2][(hi >> 8) & 0xFF] ^
+              crc_tab[1][(hi >> 16) & 0xFF] ^ crc_tab[0][hi >> 24];
+        p += 8;
+        n -= 8;
+    }
+    while (n--) crc = (crc >> 8) ^ crc_tab[0][(crc ^ *p++) & 0xFF];
+    return ~crc;
+}
+
+/* ------------------------------------------------------------------ */
+/* Quantization: scaling.py:78-105 (scale_weights + quantize with       */
+/* _round_half_away).  w (rows*cols f64, row-major), s (cols f64).      */
+/* Returns 0 ok, 1 empty, 2 zero dynamic range.                         */
+/* ------------------------------------------------------------------ */
+int or_quantize(const double *w, const double *s, uint64_t rows, uint64_t cols, int8_t *q,
+                double *w_scale_out) {
+    uint64_t n = rows * cols;
+    if (n == 0) return 1;
+    double m = 0.0;
+    for (uint64_t r = 0; r < rows; r++)
+        for (uint64_t c = 0; c < cols; c++) {
+            double v = fabs(w[r * cols + c] * s[c]); /* scaling.py:81, :99 */
+            if (v > m) m = v;
+        }
+    if (m == 0.0) return 2;
+    double ws = m / 127.0; /* scaling.py:102 */
+    for (uint64_t r = 0; r < rows; r++)
+        for (uint64_t c = 0; c < cols; c++) {
+            double x = (w[r * cols + c] * s[c]) / ws;      /* scaling.py:103 */
+            double a = floor(fabs(x) + 0.5);               /* scaling.py:84-86 */
+            double v = x < 0 ? -a : (x > 0 ? a : 0.0);
+            if (v > 127.0) v = 127.0;
+            if (v < -127.0) v = -127.0;
+            q[r * cols + c] = (int8_t)v;
+        }
+    *w_scale_out = ws;
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Pruning: pruning.py:37-64.  Zero the k lowest scores cm[c]*|q|       */
+/* (stable flat-index tie-break, pruning.py:43-45).                     */
+/* ------------------------------------------------------------------ */
+typedef struct { double key; uint64_t idx; } kv_t;
+static int kv_cmp(const void *a, const void *b) {
+    const kv_t *x = (const kv_t *)a, *y = (const kv_t *)b;
+    if (x->key < y->key) return -1;
+    if (x->key > y->key) return 1;
+    return x->idx < y->idx ? -1 : (x->idx > y->idx ? 1 : 0);
+}
+static void lowest_k(const int8_t *q, const double *cm, uint64_t cols, uint64_t base, uint64_t n,
+                     uint64_t k, int8_t *out, kv_t *buf) {
+    for (uint64_t i = 0; i < n; i++) {
+        uint64_t flat = base + i;
+        int a = q[flat] < 0 ? -(int)q[flat] : (int)q[flat];
+        buf[i].key = cm[flat % cols] * (double)a; /* pruning.py:40 */
+        buf[i].idx = i;
+    }
+    qsort(buf, n, sizeof(kv_t), kv_cmp);
+    for (uint64_t i = 0; i < k; i++) out[base + buf[i].idx] = 0;
+}
+/* per_row = 0: k = floor(sparsity*n) over the tensor; 1: k per row. */
+int or_prune(const int8_t *q, const double *cm, uint64_t rows, uint64_t cols, double sparsity,
+             int per_row, int8_t *out) {
+    uint64_t n = rows * cols;
+    memcpy(out, q, n);
+    if (!per_row) {
+        uint64_t k = (uint64_t)floor(sparsity * (double)n); /* pruning.py:58 */
+        kv_t *buf = (kv_t *)malloc(sizeof(kv_t) * (n ? n : 1));
+        if (!buf) return -1;
+        lowest_k(q, cm, cols, 0, n, k, out, buf);
+        free(buf);
+    } else {
+        uint64_t k = (uint64_t)floor(sparsity * (double)cols); /* pruning.py:61 */
+        kv_t *buf = (kv_t *)malloc(sizeof(kv_t) * (cols ? cols : 1));
+        if (!buf) return -1;
+        for (uint64_t r = 0; r < rows; r++) lowest_k(q, cm, cols, r * cols, cols, k, out, buf);
+        free(buf);
+    }
+    return 0;
+}
