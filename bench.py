@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark driver (contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): OPT-1.3B-shaped W8A8 weights, random
+init on the GPU, compression-aware quantized (alpha 0.5), packed FULLY
+compressed into DCC1 at the reference's default 16 MiB chunks by the GPU
+encoder.  One step = decompress every chunk of the resident container to
+its int8 weights (split-point parallel rANS decode + raw copy of stored
+chunks), i.e. the work a compressed-weight inference pass repeats.
+
+  value     decompressed GB/s with the container resident in HBM
+  e2e       same metric through the public API ``container.unpack`` from
+            HOST bytes (H2D copy, decode, CRC verification, D2H weights)
+  roofline  dominant kernel (k_decode_segments): algorithmic bytes
+            N * (1 + 1/CR) per launch / its CUDA-event time vs measured HBM
+  cpu_baseline  the C oracle (a restatement of the reference's numba
+            kernels) decoding a bounded sample on this box's host cores
+
+``--impl reference`` times the CPU reference path (the oracle port, all host
+threads) on the same metric; under torchrun only rank 0 runs it.
+Multi-GPU: one process per GPU, each decodes its own model copy (weak
+scaling, no collective on the data path); time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode GB/s (decompressed INT8) vs HBM peak; tokens/s compressed vs INT8; CR"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--model", default="opt-1.3b")
+    p.add_argument("--chunk-size", type=int, default=16 * 2**20)
+    p.add_argument("--alpha", type=float, default=0.5)
+    p.add_argument("--seg-shift", type=int, default=9)
+    p.add_argument("--layers", type=int, default=None, help="limit layers (debug only)")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample_decode(image_bytes: bytes, entries, budget_s: float, threads: int):
+    """C oracle decoding a bounded sample of the container's chunks on host
+    cores (the reference's algorithm, restated in C; oracle/)."""
+    from oracle import oracle as O
+    O.lib()
+    import numpy as np
+    jobs, labels, total = [], [], 0
+    sample = []
+    for i, e in enumerate(entries):
+        if e["codec"] == 1:
+            sample.append(i)
+        if len(sample) >= max(threads * 4, 16):
+            break
+    blobs = [image_bytes[int(entries[i]["file_offset"]): int(entries[i]["file_offset"] + entries[i]["comp_len"])]
+             for i in sample]
+    outs = [np.empty(int(entries[i]["uncomp_len"]), np.uint8) for i in sample]
+    nbytes = sum(o.size for o in outs)
+
+    def run():
+        from concurrent.futures import ThreadPoolExecutor
+        per = max(1, -(-len(blobs) // threads))
+        parts = [(list(zip(blobs[k:k + per], outs[k:k + per])), sample[k:k + per]) for k in range(0, len(blobs), per)]
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            list(ex.map(lambda p: O.decode_blobs_into(p[0], p[1]), parts))
+
+    run()  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        run()
+        reps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    del jobs, labels, total
+    return nbytes * reps / dt / 1e9, f"{len(sample)} ANS chunks x {reps} reps ({nbytes / 1e6:.1f} MB each rep)", threads
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on host cores (C oracle port,
+    all threads), on a bounded sample of the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import oracle as O
+    O.lib()
+    sys.path.insert(0, ROOT)
+    from paper_2502_15443_b200.tensors import SynthSpec, model_layout, synth_ensemble
+    threads = os.cpu_count() or 1
+    layout = model_layout(args.model)[:6]  # one transformer layer of the model shape
+    entries = []
+    for i, (name, r, c) in enumerate(layout):
+        w, st = synth_ensemble(SynthSpec(rows=r, cols=c, name=name), 1000 + i)
+        q, ws = O.quantize(w.values, O.compute_scale(st.channel_max, args.alpha))
+        entries.append((name, q, ws, args.alpha, O.compute_scale(st.channel_max, args.alpha), st.channel_max))
+    chunk = min(args.chunk_size, 16 * 2**20)
+    data = O.pack(entries, chunk, threads=threads)
+    raw = sum(e[1].size for e in entries)
+    for _ in range(args.warmup):
+        O.unpack(data, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.unpack(data, threads=threads)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times)
+    v = raw * args.steps / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"{args.model} one layer (6 linears), alpha {args.alpha}, DCC1 unpack, "
+                               f"{chunk} B chunks, CR {raw / len(data):.4f}", "chunk_size": chunk},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{raw / 1e6:.1f} MB decompressed per step (one {args.model} layer)"},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    from paper_2502_15443_b200 import container, engine, native, synth
+    native.require_cuda()
+
+    t_build = time.perf_counter()
+    m = synth.build_model(args.model, alpha=args.alpha, seed=1234 + rank, device=dev, layers=args.layers)
+    pm = synth.pack_model(m, args.chunk_size, seg_shift=args.seg_shift)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
+    raw = pm.raw_bytes
+    comp = pm.comp_bytes
+    cr_file = raw / pm.file_bytes
+    out = native.device_bytes(raw, dev)
+    status = torch.zeros(pm.jobs.n, dtype=torch.int32, device=dev)
+    has_store = bool((pm.entries["codec"] == 0).any())
+
+    def step():
+        engine.decode_segments(pm.image, pm.jobs, pm.index, pm.tasks, out, status)
+        if has_store:
+            engine.store_copy(pm.image, pm.jobs, out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if int(status.abs().sum().item()) != 0 or not torch.equal(out, m.payload):
+        raise SystemExit("decode mismatch: GPU output != encoder input")
+
+    # kernel-only timing of the dominant kernel (per launch, its stream)
+    kstart, kend = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        for _ in range(args.steps):
+            step()
+        end.record()
+        torch.cuda.synchronize()
+        # kernel alone (same stream, back to back)
+        kstart.record()
+        for _ in range(args.steps):
+            engine.decode_segments(pm.image, pm.jobs, pm.index, pm.tasks, out, status)
+        kend.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    kms = kstart.elapsed_time(kend) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = raw * world * args.steps / (ms / 1e3) / 1e9
+    hbm, peak_kind = peaks()
+    ans_raw = int(pm.entries["uncomp_len"][pm.entries["codec"] == 1].sum())
+    ans_comp = int(pm.entries["comp_len"][pm.entries["codec"] == 1].sum())
+    alg_bytes = ans_raw + ans_comp  # decompressed bytes written + compressed bytes read
+    achieved = alg_bytes / (kms / 1e3) / 1e9
+
+    # e2e through the public API from host bytes (rank 0 reports its own)
+    host_file = pm.image.cpu().numpy().tobytes()
+    side = pm.index.to_bytes(container.binding_of(host_file))
+    e2e_times = []
+    for i in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bundle = container.unpack(host_file, index=side)
+        torch.cuda.synchronize()
+        if i:
+            e2e_times.append(time.perf_counter() - t0)
+    ok = bundle.tensors[0].qvalues.tobytes() == m.payload[: m.shapes[0][0] * m.shapes[0][1]].cpu().numpy().tobytes()
+    if not ok:
+        raise SystemExit("e2e mismatch")
+    e2e_s = statistics.median(e2e_times)
+    e2e = {"value": raw / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": len(host_file) + len(side),
+           "d2h_bytes_per_step": raw + 8 * pm.jobs.n, "api": "container.unpack(host bytes, index=sidecar)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            v, sample, cores = cpu_sample_decode(host_file, pm.entries, args.cpu_seconds, os.cpu_count() or 1)
+            cpu = {"value": v, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample}
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"{args.model}-shaped W8A8 fully compressed (alpha {args.alpha}), decompress all "
+                                   f"chunks of the resident DCC1 container", "model": args.model,
+                       "chunk_size": args.chunk_size, "seg_len": 1 << args.seg_shift, "n_chunks": int(pm.jobs.n),
+                       "raw_bytes": raw, "file_bytes": pm.file_bytes, "cr": cr_file,
+                       "cr_resident": raw / (pm.file_bytes + pm.index.nbytes), "index_bytes": pm.index.nbytes,
+                       "l2": "inputs (compressed) and outputs exceed the 126 MB L2", "parallelism": f"dp{world} (replicas)",
+                       "build_s": t_build},
+            "roofline": {"bound": "hbm", "kernel": "k_decode_segments", "achieved": achieved, "peak": hbm,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                         "alg_bytes_per_launch": alg_bytes, "launch_ms": kms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * (1 + int(has_store)),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

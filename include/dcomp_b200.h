@@ -1,0 +1,190 @@
+/*
+ * dcomp_b200.h -- C ABI of the B200-native hot path of arXiv 2502.15443
+ * ("LLM double compression": compression-aware INT8 quantization, pruning,
+ * chunked static-table rANS in the DCC1 container, fused decode->W8A8 GEMM).
+ *
+ * The reference (`dcomp`, /root/reference/pkg/src/dcomp) is a CPU Python
+ * package whose only natively compiled code is four numba kernels; every
+ * entry point below replaces one of those kernels or a numpy hot loop, cited
+ * as "replaces <file>:<line>".  The reference has no FFI of its own: the
+ * Python host layer (paper_2502_15443_b200/) binds these symbols with ctypes
+ * exactly as a maintainer would bind them from the reference.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Every pointer argument is a DEVICE
+ *    pointer unless its name ends in `_host`.  `stream` is a cudaStream_t
+ *    passed as void*.  Calls are asynchronous on `stream` unless noted.
+ *  - Return value: 0 = ok, negative = argument / CUDA error (message via
+ *    dc_last_error()).  Data errors never become return codes: they are
+ *    written per chunk into a device `status` array (DC_CHUNK_* below), and
+ *    the host maps them to the reference's exception classes and messages.
+ *  - The library never allocates long-lived device memory; callers own all
+ *    buffers (the Python layer uses the torch caching allocator).
+ *  - Buffers that stream bytes are read from must have DC_READ_SLACK readable
+ *    bytes past their end (corrupt streams may over-read; verdicts stay exact).
+ */
+#ifndef DCOMP_B200_H
+#define DCOMP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DC_OK 0
+#define DC_ERR_ARG (-1)
+#define DC_ERR_CUDA (-2)
+#define DC_ERR_UNSUPPORTED (-3)
+
+#define DC_READ_SLACK 16384
+
+/* Per-chunk status codes (device int32 arrays).  Map 1:1 onto the reference
+ * exceptions raised by ans.split_blob / _prepare_payload / decode_blobs_into
+ * (ans.py:333-343, 364-367, 375-430) and container.unpack (container.py:327-331). */
+#define DC_CHUNK_OK 0
+#define DC_CHUNK_TRUNC_TABLE 1 /* TruncatedError "truncated stream: missing table header" */
+#define DC_CHUNK_BAD_TABLE 2   /* CorruptStreamError "corrupt stream: invalid frequency table" */
+#define DC_CHUNK_STATE_RANGE 3 /* CorruptStreamError "corrupt stream: final state out of range" */
+#define DC_CHUNK_EMPTY_BAD 4   /* CorruptStreamError "corrupt stream" (zero-length output) */
+#define DC_CHUNK_CORRUPT 5     /* CorruptStreamError "corrupt stream" (decode verdict) */
+#define DC_CHUNK_CHAIN 6       /* internal: split-point chain mismatch -> exact serial re-decode */
+
+/* ---------------------------------------------------------------- info */
+int dc_version(void);
+const char *dc_last_error(void);
+int dc_device_sm_count(int device);
+
+/* ------------------------------------------------------- rANS decoding
+ * A decode "job list" describes n chunks inside one device byte buffer:
+ *   blob_off[i]  u64  offset of chunk i's bytes in `base` (ANS blob: u12 table | u32 state | stream)
+ *   blob_len[i]  u64  comp_len of chunk i
+ *   out_off[i]   u64  where its decoded bytes go in `out`
+ *   out_len[i]   u64  uncomp_len
+ *   codec[i]     u8   0 = store (raw copy), 1 = ANS
+ * Split-point ("segment") index: for ANS chunk i, segments of 2^seg_shift
+ * symbols start at seg_base[i]; seg_state[j] / seg_off[j] hold the decoder
+ * state and stream byte offset (relative to blob+388) at each segment start.
+ */
+
+/* Prologue checks of every ANS chunk: blob length, u12 table validity,
+ * start-state range, zero-length outputs.  replaces ans.py:284-299 (from_bytes),
+ * ans.py:333-343 (_prepare_payload), ans.py:364-367 (split_blob), ans.py:382-392. */
+int dc_ans_validate(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
+                    const uint64_t *out_len, const uint8_t *codec, int64_t n_chunks,
+                    int32_t *status, void *stream);
+
+/* Exact serial decode of the listed chunks, one CTA per chunk: the
+ * reference verdict rule (final state == 2^20 and every stream byte
+ * consumed; bytes past the stream read as zero) and, when seg_state is
+ * non-null, the split points of every segment.  Skips chunks whose status
+ * is a prologue error.  replaces ans.py:71-94 (_dec1) and ans.py:413-430
+ * (the lone re-run of flagged lanes). */
+int dc_ans_decode_serial(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
+                         const uint64_t *out_off, const uint64_t *out_len, const int32_t *chunk_ids,
+                         int64_t n_ids, uint8_t *out, uint32_t seg_shift, const int64_t *seg_base,
+                         uint32_t *seg_state, uint32_t *seg_off, int32_t *status, void *stream);
+
+/* Segment-parallel decode (the hot kernel): each lane decodes one segment
+ * from its split point; every segment's end state/offset must meet the next
+ * split point (or 2^20 / stream end), else the chunk is flagged
+ * DC_CHUNK_CHAIN for an exact serial re-decode.  tasks: int32 quads
+ * (chunk, first segment (relative), segment count, 0), at most
+ * dc_decode_task_segments() segments each, sorted by chunk.
+ * replaces ans.py:97-200 (_dec2/_dec4 multi-lane interleave) with
+ * thousands of lanes per chunk. */
+int dc_decode_task_segments(void);
+int dc_ans_decode_segments(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
+                           const uint64_t *out_off, const uint64_t *out_len, uint32_t seg_shift,
+                           const int64_t *seg_base, const uint32_t *seg_state, const uint32_t *seg_off,
+                           const int32_t *tasks, int64_t n_tasks, uint8_t *out, int32_t *status,
+                           void *stream);
+
+/* Raw copy of store chunks (codec 0).  replaces container.py:309-310. */
+int dc_store_copy(const uint8_t *base, const uint64_t *blob_off, const uint64_t *out_off,
+                  const uint64_t *out_len, const uint8_t *codec, int64_t n_chunks, uint8_t *out,
+                  void *stream);
+
+/* --------------------------------------------------------------- CRC32
+ * CRC-32/ISO-HDLC (zlib.crc32) of n byte ranges data[off[i] .. off[i]+len[i]);
+ * max_len >= every len[i] (sizes the grid).
+ * replaces container.py:169 and :327-331 (zlib.crc32 per chunk). */
+int dc_crc32_ranges(const uint8_t *data, const uint64_t *off, const uint64_t *len, int64_t n,
+                    uint64_t max_len, uint32_t *crc_out, void *stream);
+
+/* ------------------------------------------------------- rANS encoding
+ * Payload = `total` bytes split every `chunk_size` bytes (last may be short).
+ */
+
+/* Per-chunk 256-bin byte histograms (hist: n_chunks*256 u32, zeroed by the
+ * call).  replaces ans.py:282 (np.bincount in AnsTable.for_data). */
+int dc_hist_chunks(const uint8_t *data, uint64_t total, uint64_t chunk_size, int64_t n_chunks,
+                   uint32_t *hist, void *stream);
+
+/* Largest-remainder normalization to 4096 with the reference's exact
+ * tie-breaks, plus the packed 384-byte u12 wire table of every chunk.
+ * replaces ans.py:213-243 (_normalize) and ans.py:246-253 (_pack_u12). */
+int dc_normalize_tables(const uint32_t *hist, int64_t n_chunks, uint32_t *freq, uint8_t *table_bytes,
+                        void *stream);
+
+/* Reverse rANS encode of every chunk with todo[i] != 0, one lane per chunk.
+ * Emitted bytes are written BACKWARDS from the end of the chunk's slot in
+ * `scratch` (slot i = [i*chunk_size, i*chunk_size + len_i)), so the decoder-
+ * order stream is scratch[slot_end - stream_len[i] .. slot_end).  Encoding
+ * stops early once the blob could not beat raw storage (388 + emitted >=
+ * len_i; stream_len = UINT64_MAX then), since container.pack stores such
+ * chunks.  flags bit 0 = standalone blob: never stop early (the caller
+ * leaves 2*len_i + 8 writable bytes below the slot end).  When seg_state is
+ * non-null, records the encoder state and emitted byte count at every
+ * 2^seg_shift-th symbol (the decoder split points).
+ * replaces ans.py:55-68 (_enc_kernel) and ans.py:316-325 (ans_compress). */
+int dc_ans_encode_chunks(const uint8_t *data, uint64_t total, uint64_t chunk_size, int64_t n_chunks,
+                         const uint8_t *todo, const uint32_t *freq, uint8_t *scratch,
+                         uint32_t *final_state, uint64_t *stream_len, uint32_t seg_shift,
+                         const int64_t *seg_base, uint32_t *seg_state, uint32_t *seg_emitted,
+                         uint32_t flags, void *stream);
+
+/* Assemble chunk payloads into the container byte image: chunk i goes to
+ * dst[file_off[i]]: ANS = table_bytes[i] | u32 LE final_state | stream;
+ * store = raw bytes.  replaces container.py:160-177 (payload join). */
+int dc_assemble_payloads(const uint8_t *data, uint64_t total, uint64_t chunk_size, int64_t n_chunks,
+                         const uint8_t *codec, const uint8_t *table_bytes, const uint32_t *final_state,
+                         const uint64_t *stream_len, const uint8_t *scratch, const uint64_t *file_off,
+                         uint8_t *dst, void *stream);
+
+/* ------------------------------------------------ quantization (kernel 1)
+ * dtype: 0 = f64 (the reference's type), 1 = f32, 2 = bf16, 3 = f16; widened
+ * to f64 exactly.  s (f64 [cols]) may be NULL (identity scale).
+ */
+
+/* max |W[r,c] * s[c]| as the bits of a non-negative f64 (exact: max is
+ * order-free), plus a non-finite flag.  replaces scaling.py:78-81 (W*s) and
+ * :99 (np.abs(v).max()); WeightTensor's isfinite check (tensors.py:33-34). */
+int dc_quant_absmax(const void *w, int dtype, const double *s, int64_t rows, int64_t cols,
+                    unsigned long long *absmax_bits, int *nonfinite, void *stream);
+
+/* q = clip(sign(x) * floor(|x| + 0.5), -127, 127), x = (W*s) / w_scale in IEEE
+ * f64.  replaces scaling.py:84-105 (_round_half_away, quantize). */
+int dc_quantize(const void *w, int dtype, const double *s, int64_t rows, int64_t cols, double w_scale,
+                int8_t *q, void *stream);
+
+/* out = q * w_scale / s[c].  replaces scaling.py:114-117 (dequantize). */
+int dc_dequantize(const int8_t *q, double w_scale, const double *s, int64_t rows, int64_t cols, double *out,
+                  void *stream);
+
+/* out = W * s[c].  replaces scaling.py:78-81 (scale_weights). */
+int dc_scale_weights(const double *w, const double *s, int64_t rows, int64_t cols, double *out, void *stream);
+
+/* ------------------------------------------------------ pruning (kernel 1)
+ * Zero the k lowest scores cm[c]*|q| (f64), ties by row-major index.
+ * replaces pruning.py:37-64 (prune_scores, _lowest_k, prune). */
+int dc_prune_scratch_bytes(int64_t rows, int64_t cols, uint64_t *out_host);
+int dc_prune_tensor(const int8_t *q, const double *cm, int64_t rows, int64_t cols, int64_t k, int8_t *out,
+                    uint8_t *scratch, void *stream);
+int dc_prune_rows(const int8_t *q, const double *cm, int64_t rows, int64_t cols, int64_t k_per_row, int8_t *out,
+                  void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCOMP_B200_H */

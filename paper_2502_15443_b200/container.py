@@ -1,0 +1,455 @@
+"""DCC1 container -- the reference's container.py API over B200 kernels.
+
+Byte layout (normative, reference container.py:1-18, little-endian):
+
+    "DCC1" | u16 version | u32 header_len | header (body | u32 crc32(body))
+    | u32 chunk_count | chunk_count x <B Q Q Q I> | chunk payloads
+
+    body  = u32 chunk_size, u32 tensor_count, then per tensor
+            u16 name_len | name | u32 rows | u32 cols | f64 w_scale | f64 alpha
+            | f32[cols] scale vector | f32[cols] channel maxima
+    entry = codec (0 store / 1 ans) | file_offset | comp_len | uncomp_len
+            | crc32 of the uncompressed chunk
+
+Tensors are concatenated row-major and cut every ``chunk_size`` bytes.
+
+What runs where:
+  * GPU: per-chunk histograms, normalization, rANS encode, payload assembly,
+    rANS decode (split-point parallel when an index is available, else the
+    exact per-chunk walk), CRC32 of every chunk.
+  * host: the header / chunk-table bytes (format code, O(tensors + chunks)).
+
+``pack``/``unpack`` return exactly what the reference returns (bytes /
+ModelBundle); ``pack_indexed``, ``unpack(..., index=)``, the ``.dcidx``
+sidecar and ``DeviceContainer`` (device.py) are B200 extensions.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import math
+import os
+import struct
+import zlib
+
+import numpy as np
+import torch
+
+from . import engine
+from . import native as nv
+from .errors import (
+    BadMagicError,
+    ChecksumError,
+    CorruptStreamError,
+    DataFormatError,
+    DcompError,
+    TruncatedError,
+    UnsupportedVersionError,
+)
+from .scaling import QuantizedTensor, ScaleVector
+from .tensors import ActivationStats
+
+MAGIC = b"DCC1"
+VERSION = 1
+MIN_CHUNK_SIZE = 4096
+DEFAULT_CHUNK_SIZE = 16 * 2**20
+CODEC_STORE = 0
+CODEC_ANS = 1
+
+_ENTRY = struct.Struct("<BQQQI")
+ENTRY_DTYPE = np.dtype([("codec", "u1"), ("file_offset", "<u8"), ("comp_len", "<u8"),
+                        ("uncomp_len", "<u8"), ("crc32", "<u4")])
+assert ENTRY_DTYPE.itemsize == _ENTRY.size == 29
+SIDECAR_SUFFIX = ".dcidx"
+
+
+def thread_count() -> int:
+    """DCOMP_THREADS semantics of the reference (container.py:58-65); the
+    GPU path does not use host threads, the CPU baseline does."""
+    env = os.environ.get("DCOMP_THREADS")
+    if env is not None:
+        try:
+            return max(1, int(env))
+        except ValueError:
+            raise DcompError(f"DCOMP_THREADS must be an integer, got {env!r}") from None
+    return os.cpu_count() or 1
+
+
+@dataclasses.dataclass(frozen=True)
+class ModelBundle:
+    tensors: list[QuantizedTensor]
+    stats: dict[str, ActivationStats]
+    chunk_size: int = DEFAULT_CHUNK_SIZE
+
+
+@dataclasses.dataclass(frozen=True)
+class ChunkEntry:
+    codec: int
+    file_offset: int
+    comp_len: int
+    uncomp_len: int
+    crc32: int
+
+
+@dataclasses.dataclass(frozen=True)
+class ContainerInfo:
+    chunk_size: int
+    directory: list[tuple[str, int, int, float, float]]  # name, rows, cols, w_scale, alpha
+    chunks: list[ChunkEntry]
+    file_size: int
+
+    @property
+    def total_uncompressed(self) -> int:
+        return sum(c.uncomp_len for c in self.chunks)
+
+
+# ------------------------------------------------------------------ writer
+def _stats_map(stats) -> dict[str, ActivationStats]:
+    return stats if isinstance(stats, dict) else {s.name: s for s in stats}
+
+
+def _header(tensors, stats: dict, chunk_size: int) -> bytes:
+    parts = [struct.pack("<II", chunk_size, len(tensors))]
+    for t in tensors:
+        st = stats.get(t.name)
+        if st is None:
+            raise DcompError(f"missing activation stats for tensor {t.name!r}")
+        if len(st.channel_max) != t.cols:
+            raise DcompError(f"stats length {len(st.channel_max)} != cols {t.cols} for tensor {t.name!r}")
+        raw_name = t.name.encode("utf-8")
+        parts += [struct.pack("<H", len(raw_name)), raw_name,
+                  struct.pack("<IIdd", t.rows, t.cols, t.w_scale, t.scale_vec.alpha),
+                  t.scale_vec.s.astype("<f4").tobytes(), st.channel_max.astype("<f4").tobytes()]
+    body = b"".join(parts)
+    return body + struct.pack("<I", zlib.crc32(body))
+
+
+def _mask_of(plan, n_chunks: int) -> np.ndarray:
+    if plan is None:
+        return np.ones(n_chunks, dtype=bool)
+    mask = np.asarray(getattr(plan, "compressed_mask", plan), dtype=bool)
+    if mask.shape != (n_chunks,):
+        raise DcompError(f"plan covers {mask.size} chunks, container has {n_chunks}")
+    return mask
+
+
+def _device_payload(tensors) -> torch.Tensor:
+    dev = nv.require_cuda()
+    total = sum(t.qvalues.size for t in tensors)
+    out = nv.device_bytes(total, dev)
+    pos = 0
+    for t in tensors:
+        n = t.qvalues.size
+        if n:
+            out[pos:pos + n].copy_(torch.from_numpy(np.ascontiguousarray(t.qvalues).reshape(-1).view(np.uint8)))
+        pos += n
+    return out
+
+
+def pack_device(payload: torch.Tensor, header: bytes, chunk_size: int, plan=None,
+                seg_shift: int | None = engine.DEFAULT_SEG_SHIFT):
+    """Encode a device-resident payload into a DCC1 image.
+
+    Returns (device file image uint8, EncodeResult, entries ndarray).  The
+    image holds the whole file; its payload region is assembled on the GPU.
+    """
+    total = int(payload.numel())
+    n = math.ceil(total / chunk_size) if total else 0
+    mask = _mask_of(plan, n)
+    enc = engine.encode_payload(payload, chunk_size, mask, seg_shift)
+    first = len(MAGIC) + 2 + 4 + len(header) + 4 + n * _ENTRY.size
+    offs = np.zeros(n, dtype=np.uint64)
+    if n:
+        offs[1:] = np.cumsum(enc.comp_len)[:-1]
+    file_off = offs + np.uint64(first)
+    entries = np.zeros(n, dtype=ENTRY_DTYPE)
+    entries["codec"] = enc.codec
+    entries["file_offset"] = file_off
+    entries["comp_len"] = enc.comp_len
+    entries["uncomp_len"] = np.minimum(chunk_size, total - np.arange(n, dtype=np.uint64) * np.uint64(chunk_size))
+    entries["crc32"] = enc.crc
+    size = first + int(enc.comp_len.sum())
+    image = nv.device_bytes(size, payload.device)
+    prefix = MAGIC + struct.pack("<HI", VERSION, len(header)) + header + struct.pack("<I", n) + entries.tobytes()
+    image[:first].copy_(torch.frombuffer(bytearray(prefix), dtype=torch.uint8))
+    engine.assemble(payload, enc, file_off, image)
+    return image, enc, entries
+
+
+def _pack_impl(tensors, stats, chunk_size, plan, seg_shift):
+    if chunk_size < MIN_CHUNK_SIZE:
+        raise DcompError(f"chunk_size must be >= {MIN_CHUNK_SIZE}, got {chunk_size}")
+    names = [t.name for t in tensors]
+    if len(set(names)) != len(names):
+        raise DcompError("duplicate tensor names")
+    header = _header(tensors, _stats_map(stats), chunk_size)
+    total = sum(t.qvalues.size for t in tensors)
+    _mask_of(plan, math.ceil(total / chunk_size))  # reference checks the plan before encoding
+    if total == 0:
+        data = MAGIC + struct.pack("<HI", VERSION, len(header)) + header + struct.pack("<I", 0)
+        return data, None
+    payload = _device_payload(tensors)
+    image, enc, _ = pack_device(payload, header, chunk_size, plan, seg_shift)
+    return image.cpu().numpy().tobytes(), enc.index
+
+
+def pack(tensors, stats, chunk_size: int = DEFAULT_CHUNK_SIZE, plan=None) -> bytes:
+    """Serialize quantized tensors into DCC1 bytes (bit-identical to the
+    reference's pack).  ``plan`` selects per-chunk codecs (None = all ANS);
+    chunks whose blob would not shrink are stored raw."""
+    return _pack_impl(tensors, stats, chunk_size, plan, None)[0]
+
+
+def pack_indexed(tensors, stats, chunk_size: int = DEFAULT_CHUNK_SIZE, plan=None,
+                 seg_shift: int = engine.DEFAULT_SEG_SHIFT):
+    """``pack`` plus the split-point index the GPU encoder records for free."""
+    return _pack_impl(tensors, stats, chunk_size, plan, seg_shift)
+
+
+def write_container(path, tensors, stats, chunk_size: int = DEFAULT_CHUNK_SIZE, plan=None,
+                    sidecar: bool = False) -> None:
+    data, index = _pack_impl(tensors, stats, chunk_size, plan, engine.DEFAULT_SEG_SHIFT if sidecar else None)
+    with open(path, "wb") as f:
+        f.write(data)
+    if sidecar and index is not None:
+        with open(str(path) + SIDECAR_SUFFIX, "wb") as f:
+            f.write(index.to_bytes(binding_of(data)))
+
+
+# ------------------------------------------------------------------ reader
+class _Cursor:
+    def __init__(self, buf: bytes, pos: int = 0):
+        self.buf = buf
+        self.pos = pos
+
+    def take(self, n: int) -> bytes:
+        if self.pos + n > len(self.buf):
+            raise TruncatedError(f"truncated file at offset {self.pos}")
+        out = self.buf[self.pos:self.pos + n]
+        self.pos += n
+        return out
+
+    def fmt(self, f: str):
+        return struct.unpack(f, self.take(struct.calcsize(f)))
+
+
+def _parse_header(header: bytes):
+    if len(header) < 4:
+        raise DataFormatError("header too small to hold its checksum")
+    body = header[:-4]
+    if zlib.crc32(body) != struct.unpack("<I", header[-4:])[0]:
+        raise ChecksumError(-1, "header checksum mismatch")
+    cur = _Cursor(body)
+    chunk_size, count = cur.fmt("<II")
+    if chunk_size < 1:
+        raise DataFormatError("invalid chunk size 0")
+    directory = []
+    for _ in range(count):
+        (nl,) = cur.fmt("<H")
+        try:
+            name = cur.take(nl).decode("utf-8")
+        except UnicodeDecodeError as e:
+            raise DataFormatError(f"tensor name is not valid UTF-8: {e}") from None
+        rows, cols, w_scale, alpha = cur.fmt("<IIdd")
+        if rows < 1 or cols < 1:
+            raise DataFormatError(f"{name}: invalid dims {rows}x{cols}")
+        if not (np.isfinite(w_scale) and w_scale > 0):
+            raise DataFormatError(f"{name}: invalid w_scale {w_scale}")
+        s = np.frombuffer(cur.take(4 * cols), dtype="<f4").astype(np.float64)
+        cm = np.frombuffer(cur.take(4 * cols), dtype="<f4").astype(np.float64)
+        if (s <= 0).any() or not np.isfinite(s).all():
+            raise DataFormatError(f"{name}: scale vector not positive finite")
+        if (cm < 0).any() or not np.isfinite(cm).all():
+            raise DataFormatError(f"{name}: channel maxima not finite non-negative")
+        directory.append((name, rows, cols, w_scale, alpha, s, cm))
+    if cur.pos != len(body):
+        raise DataFormatError(f"{len(body) - cur.pos} stray bytes in header")
+    names = [d[0] for d in directory]
+    if len(set(names)) != len(names):
+        raise DataFormatError("duplicate tensor names in header")
+    return chunk_size, directory
+
+
+def _parse(data: bytes):
+    """Structure + chunk table validation (reference container.py:238-274),
+    vectorized over chunks with the reference's first-error order."""
+    cur = _Cursor(data)
+    if cur.take(4) != MAGIC:
+        raise BadMagicError("not a DCC1 container")
+    (version,) = cur.fmt("<H")
+    if version != VERSION:
+        raise UnsupportedVersionError(f"unsupported container version {version}")
+    (hlen,) = cur.fmt("<I")
+    chunk_size, directory = _parse_header(cur.take(hlen))
+    (count,) = cur.fmt("<I")
+    avail = (len(data) - cur.pos) // _ENTRY.size
+    if avail < count:
+        raise TruncatedError(f"truncated file at offset {cur.pos + avail * _ENTRY.size}")
+    ent = np.frombuffer(data, dtype=ENTRY_DTYPE, count=count, offset=cur.pos)
+    cur.pos += count * _ENTRY.size
+    start = cur.pos
+    if count:
+        codec = ent["codec"]
+        off = ent["file_offset"]
+        clen = ent["comp_len"]
+        ulen = ent["uncomp_len"]
+        huge = bool((clen > np.uint64(1 << 50)).any())
+        if huge:  # exact big-int accumulation, as the reference does
+            exp = [start]
+            for c in clen[:-1]:
+                exp.append(exp[-1] + int(c))
+            expected = np.array(exp, dtype=object)
+            off_cmp = np.array([int(o) for o in off], dtype=object) != expected
+        else:
+            expected = np.empty(count, dtype=np.uint64)
+            expected[0] = start
+            expected[1:] = np.uint64(start) + np.cumsum(clen[:-1], dtype=np.uint64)
+            off_cmp = off != expected
+        last = np.zeros(count, bool)
+        last[-1] = True
+        conds = [
+            ((codec != CODEC_STORE) & (codec != CODEC_ANS), lambda i: f"chunk {i}: unknown codec {ent['codec'][i]}"),
+            (off_cmp, lambda i: f"chunk {i}: offset {int(off[i])}, expected {int(expected[i])}"),
+            ((codec == CODEC_STORE) & (clen != ulen), lambda i: f"chunk {i}: store codec with comp_len != uncomp_len"),
+            (ulen == 0, lambda i: f"chunk {i}: empty chunk"),
+            ((~last & (ulen != np.uint64(chunk_size))) | (ulen > np.uint64(chunk_size)),
+             lambda i: f"chunk {i}: uncompressed length {int(ulen[i])} breaks chunking"),
+        ]
+        first_bad = [int(np.argmax(c)) if c.any() else count for c, _ in conds]
+        i = min(first_bad)
+        if i < count:
+            k = first_bad.index(i)
+            raise DataFormatError(conds[k][1](i))
+        end = int(expected[-1]) + int(clen[-1])
+    else:
+        end = start
+    if end > len(data):
+        raise TruncatedError(f"chunk payloads extend past end of file ({end} > {len(data)})")
+    if end < len(data):
+        raise DataFormatError(f"{len(data) - end} trailing bytes after last chunk")
+    total = int(ent["uncomp_len"].sum(dtype=np.uint64)) if count else 0
+    want = sum(r * c for _, r, c, *_ in directory)
+    if total != want:
+        raise DataFormatError(f"chunks carry {total} bytes, directory declares {want}")
+    return chunk_size, directory, ent, start
+
+
+def binding_of(data: bytes) -> int:
+    """Ties a sidecar index to its container: CRC32 of the header + chunk table."""
+    (hlen,) = struct.unpack_from("<I", data, 6)
+    (count,) = struct.unpack_from("<I", data, 10 + hlen)
+    return zlib.crc32(memoryview(data)[: 14 + hlen + count * _ENTRY.size])
+
+
+def _file_bytes(data) -> bytes:
+    if isinstance(data, (bytes, bytearray, memoryview)):
+        return bytes(data)
+    with open(data, "rb") as f:
+        return f.read()
+
+
+def inspect(data) -> ContainerInfo:
+    """Validate the structure (no payload decode) and describe the container."""
+    data = _file_bytes(data)
+    chunk_size, directory, ent, _ = _parse(data)
+    chunks = [ChunkEntry(int(e["codec"]), int(e["file_offset"]), int(e["comp_len"]), int(e["uncomp_len"]),
+                         int(e["crc32"])) for e in ent]
+    return ContainerInfo(chunk_size, [(n, r, c, ws, a) for n, r, c, ws, a, _, _ in directory], chunks, len(data))
+
+
+def jobs_for(ent: np.ndarray, device=None) -> engine.JobTable:
+    n = len(ent)
+    ulen = ent["uncomp_len"].astype(np.uint64)
+    ooff = np.zeros(n, dtype=np.uint64)
+    if n:
+        ooff[1:] = np.cumsum(ulen)[:-1]
+    return engine.JobTable.build(ent["file_offset"], ent["comp_len"], ooff, ulen, ent["codec"], device)
+
+
+def raise_decode_errors(status: np.ndarray) -> None:
+    """First prologue error (chunk order), then the first corrupt chunk --
+    the order the reference's decode_blobs_into reports them in."""
+    pro = np.nonzero((status >= nv.CHUNK_TRUNC_TABLE) & (status <= nv.CHUNK_EMPTY_BAD))[0]
+    if len(pro):
+        i = int(pro[0])
+        s = int(status[i])
+        if s == nv.CHUNK_TRUNC_TABLE:
+            raise TruncatedError(f"truncated stream: missing table header (chunk {i})")
+        if s == nv.CHUNK_BAD_TABLE:
+            raise CorruptStreamError(f"corrupt stream: invalid frequency table (chunk {i})")
+        if s == nv.CHUNK_STATE_RANGE:
+            raise CorruptStreamError(f"corrupt stream: final state out of range (chunk {i})")
+        raise CorruptStreamError(f"corrupt stream (chunk {i})")
+    bad = np.nonzero(status != nv.CHUNK_OK)[0]
+    if len(bad):
+        raise CorruptStreamError(f"corrupt stream (chunk {int(bad[0])})")
+
+
+def decode_and_verify(base: torch.Tensor, ent: np.ndarray, index=None, build_index: bool = False,
+                      tasks=None) -> engine.DecodeResult:
+    """GPU decode of every chunk + reference error semantics + CRC check."""
+    jobs = jobs_for(ent, base.device)
+    res = engine.decode_jobs(base, jobs, index=index, build_index=build_index, tasks=tasks)
+    raise_decode_errors(res.status)
+    if jobs.n:
+        crc = engine.crc32_ranges(res.out, jobs.d_out_off, jobs.d_out_len, int(jobs.out_len.max()))
+        got = crc.cpu().numpy().view(np.uint32)
+        bad = np.nonzero(got != ent["crc32"])[0]
+        if len(bad):
+            raise ChecksumError(int(bad[0]))
+    return res
+
+
+def _bundle(directory, host: np.ndarray, chunk_size: int) -> ModelBundle:
+    tensors, stats = [], {}
+    pos = 0
+    for name, rows, cols, w_scale, alpha, s, cm in directory:
+        n = rows * cols
+        q = host[pos:pos + n].view(np.int8).reshape(rows, cols)
+        pos += n
+        tensors.append(QuantizedTensor(name, q, w_scale, ScaleVector(alpha, s)))
+        stats[name] = ActivationStats(name, cm)
+    return ModelBundle(tensors=tensors, stats=stats, chunk_size=chunk_size)
+
+
+def unpack(data, index=None) -> ModelBundle:
+    """Decode and verify a container (inverse of pack).  ``index`` (a
+    SegmentIndex or sidecar bytes) enables the split-point parallel decoder;
+    without it each ANS chunk is decoded by one exact sequential walk."""
+    data = _file_bytes(data)
+    chunk_size, directory, ent, _ = _parse(data)
+    if len(ent) == 0:
+        return _bundle(directory, np.empty(0, np.uint8), chunk_size)
+    base = nv.to_device_bytes(data)
+    if isinstance(index, (bytes, bytearray)):
+        index = engine.SegmentIndex.from_bytes(bytes(index), jobs_for(ent, base.device), binding_of(data))
+    res = decode_and_verify(base, ent, index=index)
+    return _bundle(directory, res.out.cpu().numpy(), chunk_size)
+
+
+def read_container(path) -> ModelBundle:
+    side = str(path) + SIDECAR_SUFFIX
+    index = None
+    if os.path.exists(side):
+        with open(side, "rb") as f:
+            index = f.read()
+    return unpack(path, index=index)
+
+
+# --------------------------------------------------------- benchmark helpers
+def chunked_compress(data, chunk_size: int = DEFAULT_CHUNK_SIZE) -> list[bytes]:
+    """Split raw bytes into chunk-sized ANS blobs (every chunk encoded, no store fallback)."""
+    from .ans import compress_blob
+    u8 = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data.reshape(-1).view(np.uint8)
+    return [compress_blob(u8[i:i + chunk_size]) for i in range(0, u8.size, chunk_size)]
+
+
+def chunked_decompress(blobs: list[bytes], lengths: list[int]) -> np.ndarray:
+    from .ans import decode_blobs_into
+    out = np.empty(int(sum(lengths)), dtype=np.uint8)
+    jobs, pos = [], 0
+    for blob, n in zip(blobs, lengths):
+        jobs.append((blob, out[pos:pos + n]))
+        pos += n
+    decode_blobs_into(jobs)
+    return out

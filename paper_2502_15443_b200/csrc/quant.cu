@@ -1,0 +1,187 @@
+// Compression-aware INT8 quantization on B200, bit-exact with the reference
+// (scaling.py:78-117):
+//   v = W[r,c] * s[c]                      (f64 multiply, scale_weights)
+//   m = max |v|; w_scale = m / 127         (host, f64)
+//   q = clip(sign(x) * floor(|x| + 0.5), -127, 127),  x = v / w_scale
+//       (IEEE f64 division, half-away-from-zero rounding, _round_half_away)
+// Inputs may be f64 (the reference type) or f32 / bf16 / f16 device tensors,
+// widened to f64 exactly in registers.  Everything is HBM-bound: each kernel
+// streams its input once with 16-byte loads.  No FMA contraction: the
+// multiply, divide and add use explicit _rn intrinsics.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace dc {
+
+enum : int { kF64 = 0, kF32 = 1, kBF16 = 2, kF16 = 3 };
+
+template <int T>
+struct In;
+template <>
+struct In<kF64> {
+    using type = double;
+    __device__ static double f64(double v) { return v; }
+};
+template <>
+struct In<kF32> {
+    using type = float;
+    __device__ static double f64(float v) { return (double)v; }
+};
+template <>
+struct In<kBF16> {
+    using type = __nv_bfloat16;
+    __device__ static double f64(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
+};
+template <>
+struct In<kF16> {
+    using type = __half;
+    __device__ static double f64(__half v) { return (double)__half2float(v); }
+};
+
+constexpr int kQThreads = 256;
+
+// rows are processed whole by a CTA slab; threads stride the columns.
+template <int T>
+__global__ void __launch_bounds__(kQThreads) k_absmax(const typename In<T>::type* __restrict__ w,
+                                                       const double* __restrict__ s, int64_t rows, int64_t cols,
+                                                       int64_t rows_per_cta, unsigned long long* __restrict__ out,
+                                                       int* __restrict__ nonfinite) {
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+    const int64_t r1 = min(rows, r0 + rows_per_cta);
+    double m = 0.0;
+    bool bad = false;
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+        const double sc = s ? s[c] : 1.0;
+        for (int64_t r = r0; r < r1; ++r) {
+            const double raw = In<T>::f64(w[r * cols + c]);
+            bad |= !isfinite(raw);
+            const double v = fabs(__dmul_rn(raw, sc));
+            m = v > m ? v : m;
+        }
+    }
+    __shared__ double red[kQThreads / 32];
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, m, d);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    const int anybad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int i = 0; i < kQThreads / 32; ++i) b = red[i] > b ? red[i] : b;
+        // non-negative doubles order like their bit patterns
+        atomicMax(out, (unsigned long long)__double_as_longlong(b));
+        if (anybad) atomicExch(nonfinite, 1);
+    }
+}
+
+__device__ __forceinline__ int8_t q_of(double v, double w_scale) {
+    const double x = __ddiv_rn(v, w_scale);
+    double a = floor(__dadd_rn(fabs(x), 0.5));
+    a = a > 127.0 ? 127.0 : a;
+    const double sg = x < 0.0 ? -a : (x > 0.0 ? a : 0.0);
+    return (int8_t)(int)sg;
+}
+
+// q[r, c] plus, optionally, the per-(column, |q|) histogram used by pruning
+// (counts[c * 129 + |q|], u32, must be zeroed).
+template <int T>
+__global__ void __launch_bounds__(kQThreads) k_quantize(const typename In<T>::type* __restrict__ w,
+                                                         const double* __restrict__ s, int64_t rows, int64_t cols,
+                                                         int64_t rows_per_cta, double w_scale,
+                                                         int8_t* __restrict__ q) {
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+    const int64_t r1 = min(rows, r0 + rows_per_cta);
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+        const double sc = s ? s[c] : 1.0;
+        for (int64_t r = r0; r < r1; ++r) {
+            const double v = __dmul_rn(In<T>::f64(w[r * cols + c]), sc);
+            q[r * cols + c] = q_of(v, w_scale);
+        }
+    }
+}
+
+// v = q * w_scale / s[c]   (scaling.py:114-117, dequantize)
+__global__ void k_dequantize(const int8_t* __restrict__ q, double w_scale, const double* __restrict__ s,
+                             int64_t rows, int64_t cols, double* __restrict__ out) {
+    const int64_t n = rows * cols;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i % cols;
+        out[i] = __ddiv_rn(__dmul_rn((double)q[i], w_scale), s[c]);
+    }
+}
+
+// W' = W * s[c]  (scaling.py:78-81, scale_weights)
+__global__ void k_scale(const double* __restrict__ w, const double* __restrict__ s, int64_t rows, int64_t cols,
+                        double* __restrict__ out) {
+    const int64_t n = rows * cols;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __dmul_rn(w[i], s[i % cols]);
+}
+
+static int64_t rows_per(int64_t rows, int64_t cols) {
+    // ~64K elements per CTA, at least one row
+    int64_t r = (65536 + cols - 1) / cols;
+    return r < 1 ? 1 : r;
+}
+
+}  // namespace dc
+
+using namespace dc;
+
+extern "C" int dc_quant_absmax(const void* w, int dtype, const double* s, int64_t rows, int64_t cols,
+                               unsigned long long* absmax_bits, int* nonfinite, void* stream) {
+    if (rows < 0 || cols < 0 || dtype < 0 || dtype > 3) return DC_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(absmax_bits, 0, sizeof(unsigned long long), st);
+    cudaMemsetAsync(nonfinite, 0, sizeof(int), st);
+    if (rows == 0 || cols == 0) return DC_OK;
+    const int64_t rp = rows_per(rows, cols);
+    const unsigned grid = (unsigned)((rows + rp - 1) / rp);
+    switch (dtype) {
+        case kF64: k_absmax<kF64><<<grid, kQThreads, 0, st>>>((const double*)w, s, rows, cols, rp, absmax_bits, nonfinite); break;
+        case kF32: k_absmax<kF32><<<grid, kQThreads, 0, st>>>((const float*)w, s, rows, cols, rp, absmax_bits, nonfinite); break;
+        case kBF16: k_absmax<kBF16><<<grid, kQThreads, 0, st>>>((const __nv_bfloat16*)w, s, rows, cols, rp, absmax_bits, nonfinite); break;
+        default: k_absmax<kF16><<<grid, kQThreads, 0, st>>>((const __half*)w, s, rows, cols, rp, absmax_bits, nonfinite); break;
+    }
+    DC_CHECK_LAUNCH("k_absmax");
+    return DC_OK;
+}
+
+extern "C" int dc_quantize(const void* w, int dtype, const double* s, int64_t rows, int64_t cols, double w_scale,
+                           int8_t* q, void* stream) {
+    if (rows < 0 || cols < 0 || dtype < 0 || dtype > 3 || !(w_scale > 0.0)) return DC_ERR_ARG;
+    if (rows == 0 || cols == 0) return DC_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t rp = rows_per(rows, cols);
+    const unsigned grid = (unsigned)((rows + rp - 1) / rp);
+    switch (dtype) {
+        case kF64: k_quantize<kF64><<<grid, kQThreads, 0, st>>>((const double*)w, s, rows, cols, rp, w_scale, q); break;
+        case kF32: k_quantize<kF32><<<grid, kQThreads, 0, st>>>((const float*)w, s, rows, cols, rp, w_scale, q); break;
+        case kBF16: k_quantize<kBF16><<<grid, kQThreads, 0, st>>>((const __nv_bfloat16*)w, s, rows, cols, rp, w_scale, q); break;
+        default: k_quantize<kF16><<<grid, kQThreads, 0, st>>>((const __half*)w, s, rows, cols, rp, w_scale, q); break;
+    }
+    DC_CHECK_LAUNCH("k_quantize");
+    return DC_OK;
+}
+
+extern "C" int dc_dequantize(const int8_t* q, double w_scale, const double* s, int64_t rows, int64_t cols,
+                             double* out, void* stream) {
+    if (rows < 0 || cols < 0) return DC_ERR_ARG;
+    if (rows == 0 || cols == 0) return DC_OK;
+    k_dequantize<<<1184, 256, 0, (cudaStream_t)stream>>>(q, w_scale, s, rows, cols, out);
+    DC_CHECK_LAUNCH("k_dequantize");
+    return DC_OK;
+}
+
+extern "C" int dc_scale_weights(const double* w, const double* s, int64_t rows, int64_t cols, double* out,
+                                void* stream) {
+    if (rows < 0 || cols < 0) return DC_ERR_ARG;
+    if (rows == 0 || cols == 0) return DC_OK;
+    k_scale<<<1184, 256, 0, (cudaStream_t)stream>>>(w, s, rows, cols, out);
+    DC_CHECK_LAUNCH("k_scale");
+    return DC_OK;
+}

@@ -1,0 +1,538 @@
+// rANS decoding of the DCC1 chunk payloads on B200 (sm_100a).
+//
+// Reference semantics (/root/reference/pkg/src/dcomp/ans.py):
+//   blob   = u12 table (384 B) | u32 LE start state | stream        (:1-12)
+//   decode = e = tab[x & 4095]; sym = e.sym;
+//            x = f * (x >> 12) + (slot - cum); refill bytes while x < 2^20   (:71-94)
+//   verdict: ok iff final x == 2^20 and all stream bytes consumed; bytes
+//            past the stream read as zero (padding, :333-343).
+//
+// Three kernels:
+//   k_validate        warp per chunk: the prologue checks (:284-299, :333-343, :364-367)
+//   k_decode_segments the hot path: a task = up to 256 split-point segments of
+//                     one chunk; the task's stream bytes are staged into shared
+//                     memory with one TMA bulk copy, every lane decodes two
+//                     segments interleaved (ILP 2) from its split point and
+//                     writes output through a per-warp staging buffer as
+//                     coalesced 16-byte stores.  Chain checks flag chunks whose
+//                     segments do not meet (corrupt data) for an exact re-run.
+//   k_decode_serial   CTA per chunk, one lane walks the whole stream exactly as
+//                     the reference does (the verdict of record) and records
+//                     the split points every 2^seg_shift symbols.
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace dc {
+
+// ------------------------------------------------------------------ tables
+struct alignas(128) TableSmem {
+    uint32_t tab[kProbScale];  // slot -> sym | (slot - cum) << 8 | f << 20
+    uint32_t freq[256];
+    uint32_t cum[256];
+    int32_t present[256];
+    int32_t npresent;
+    int32_t single;  // symbol of a single-symbol table, else -1
+    uint32_t warp_tot[4];
+};
+
+// 128 threads: unpack the u12 wire table (ans.py:256-262), fix up the
+// single-symbol case (ans.py:292-295), exclusive cumulative sums
+// (ans.py:301-304), and the slot table (ans.py:306-313) with a compact u32
+// entry.  Tables are validated beforehand by k_validate.
+__device__ void build_decode_table(const uint8_t* __restrict__ tb, TableSmem& T) {
+    const int t = threadIdx.x;
+    uint32_t a, b;
+    unpack_pair(tb, t, a, b);
+    // pack (frequency sum, present count) and scan both at once
+    uint32_t v = (a + b) | (((a != 0) + (b != 0)) << 16);
+    uint32_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if ((t & 31) >= d) inc += o;
+    }
+    if ((t & 31) == 31) T.warp_tot[t >> 5] = inc;
+    __syncthreads();
+    uint32_t carry = 0;
+    for (int w = 0; w < (t >> 5); ++w) carry += T.warp_tot[w];
+    const uint32_t total = T.warp_tot[0] + T.warp_tot[1] + T.warp_tot[2] + T.warp_tot[3];
+    uint32_t ex = carry + inc - v;
+    uint32_t c0 = ex & 0xFFFF, k0 = ex >> 16;
+    T.freq[2 * t] = a;
+    T.freq[2 * t + 1] = b;
+    T.cum[2 * t] = c0;
+    T.cum[2 * t + 1] = c0 + a;
+    if (a) T.present[k0++] = 2 * t;
+    if (b) T.present[k0] = 2 * t + 1;
+    if (t == 0) {
+        T.npresent = total >> 16;
+        T.single = -1;
+    }
+    __syncthreads();
+    if ((total & 0xFFFF) == kProbScale - 1) {  // validated: exactly one nonzero entry
+        if (t == 0) {
+            int s = T.present[0];
+            T.single = s;
+            T.freq[s] = kProbScale;
+        }
+        __syncthreads();
+        return;
+    }
+    // fill: warps take present symbols round-robin, lanes stride the slots
+    const int np = T.npresent;
+    const int lane = t & 31;
+    for (int i = t >> 5; i < np; i += 4) {
+        const uint32_t s = T.present[i];
+        const uint32_t f = T.freq[s], c = T.cum[s];
+        for (uint32_t k = lane; k < f; k += 32) T.tab[c + k] = s | (k << 8) | (f << 20);
+    }
+    __syncthreads();
+}
+
+// --------------------------------------------------------------- validate
+__global__ void k_validate(const uint8_t* __restrict__ base, const uint64_t* __restrict__ blob_off,
+                           const uint64_t* __restrict__ blob_len, const uint64_t* __restrict__ out_len,
+                           const uint8_t* __restrict__ codec, int64_t n, int32_t* __restrict__ status) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= n) return;
+    int st = DC_CHUNK_OK;
+    if (codec[w] == 1) {
+        const uint64_t len = blob_len[w];
+        if (len < kHeaderBytes) {
+            st = DC_CHUNK_TRUNC_TABLE;  // ans.py:365-366
+        } else {
+            const uint8_t* b = base + blob_off[w];
+            uint32_t sum = 0, nz = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t fa, fb;
+                unpack_pair(b, lane * 4 + k, fa, fb);
+                sum += fa + fb;
+                nz += (fa != 0) + (fb != 0);
+            }
+#pragma unroll
+            for (int d = 16; d; d >>= 1) {
+                sum += __shfl_xor_sync(0xffffffffu, sum, d);
+                nz += __shfl_xor_sync(0xffffffffu, nz, d);
+            }
+            const bool single = (sum == kProbScale - 1 && nz == 1);
+            if (!single && sum != kProbScale) {
+                st = DC_CHUNK_BAD_TABLE;  // ans.py:296-297
+            } else {
+                const uint32_t x0 = ld_u32_le_unaligned(b + kTableBytes);
+                if (x0 < kStateLower || x0 >= kStateUpper)
+                    st = DC_CHUNK_STATE_RANGE;  // ans.py:338-339
+                else if (out_len[w] == 0 && (len != kHeaderBytes || x0 != kStateLower))
+                    st = DC_CHUNK_EMPTY_BAD;  // ans.py:388-390
+            }
+        }
+    }
+    if (lane == 0) status[w] = st;
+}
+
+// ------------------------------------------------------------- serial decode
+constexpr int kSerialThreads = 128;
+
+__global__ void __launch_bounds__(kSerialThreads) k_decode_serial(
+    const uint8_t* __restrict__ base, const uint64_t* __restrict__ blob_off, const uint64_t* __restrict__ blob_len,
+    const uint64_t* __restrict__ out_off, const uint64_t* __restrict__ out_len, const int32_t* __restrict__ ids,
+    int64_t n_ids, uint8_t* __restrict__ out, uint32_t seg_shift, const int64_t* __restrict__ seg_base,
+    uint32_t* __restrict__ seg_state, uint32_t* __restrict__ seg_off, int32_t* __restrict__ status) {
+    __shared__ TableSmem T;
+    for (int64_t id = blockIdx.x; id < n_ids; id += gridDim.x) {
+        const int c = ids[id];
+        const int32_t st0 = status[c];
+        if (st0 != DC_CHUNK_OK && st0 != DC_CHUNK_CHAIN) continue;  // prologue error: never decoded
+        const uint8_t* blob = base + blob_off[c];
+        const uint64_t n = out_len[c];
+        if (n == 0) continue;
+        const uint8_t* s = blob + kHeaderBytes;
+        const uint64_t plen = blob_len[c] - kHeaderBytes;
+        const uint32_t x0 = ld_u32_le_unaligned(blob + kTableBytes);
+        uint8_t* o = out + out_off[c];
+        __syncthreads();
+        build_decode_table(blob, T);
+        const uint32_t K = 1u << seg_shift;
+        const int64_t sb = seg_state ? seg_base[c] : 0;
+        if (T.single >= 0) {
+            // f = 4096: the state never changes and no byte is ever read.
+            const uint8_t sym = (uint8_t)T.single;
+            for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) o[i] = sym;
+            if (seg_state)
+                for (uint64_t j = threadIdx.x; j < ((n + K - 1) >> seg_shift); j += blockDim.x) {
+                    seg_state[sb + j] = x0;
+                    seg_off[sb + j] = 0;
+                }
+            if (threadIdx.x == 0) status[c] = (x0 == kStateLower && plen == 0) ? DC_CHUNK_OK : DC_CHUNK_CORRUPT;
+            continue;
+        }
+        if (threadIdx.x == 0) {
+            uint32_t x = x0;
+            uint64_t p = 0;
+            bool bad = false;
+            for (uint64_t i = 0; i < n;) {
+                const uint64_t end = (i + kCheckBlock < n) ? i + kCheckBlock : n;
+                for (uint64_t j = i; j < end; ++j) {
+                    if (seg_state && (j & (K - 1)) == 0) {
+                        seg_state[sb + (j >> seg_shift)] = x;
+                        seg_off[sb + (j >> seg_shift)] = (uint32_t)p;
+                    }
+                    const uint32_t e = T.tab[x & (kProbScale - 1)];
+                    o[j] = (uint8_t)e;
+                    x = (e >> 20) * (x >> 12) + ((e >> 8) & 0xFFF);
+                    if (x < kStateLower) {
+                        x = (x << 8) | (p < plen ? s[p] : 0u);
+                        ++p;
+                        if (x < kStateLower) {
+                            x = (x << 8) | (p < plen ? s[p] : 0u);
+                            ++p;
+                        }
+                    }
+                }
+                if (p > plen) {  // ans.py:89-90
+                    bad = true;
+                    break;
+                }
+                i = end;
+            }
+            if (x != kStateLower || p != plen) bad = true;  // ans.py:92-93
+            status[c] = bad ? DC_CHUNK_CORRUPT : DC_CHUNK_OK;
+        }
+    }
+}
+
+// ---------------------------------------------------------- segment decode
+constexpr int kDecThreads = 128;
+constexpr int kDecWarps = kDecThreads / 32;
+constexpr int kDecIlp = 2;
+constexpr int kTaskSegs = kDecThreads * kDecIlp;  // segments per task
+constexpr uint32_t kStageCap = 64 * 1024;         // staged stream bytes per task
+constexpr uint32_t kStageSlack = 2 * 1024 + 128;  // over-read room (>= 2 * max segment)
+constexpr int kOutLine = 64;                      // bytes per lane-segment per flush
+constexpr int kOutStride = 80;                    // padded: conflict-free 16-B stores
+constexpr int kOutWarpBytes = kDecIlp * 32 * kOutStride;
+constexpr size_t kDecSmem = sizeof(TableSmem) + kStageCap + kStageSlack + kDecWarps * kOutWarpBytes + 128;
+static_assert(sizeof(TableSmem) % 128 == 0 && (kStageCap + kStageSlack) % 128 == 0, "16-B aligned smem carve-up");
+
+__device__ __forceinline__ uint32_t dec_step(uint32_t& x, uint32_t& p, const uint32_t* __restrict__ tab,
+                                             const uint8_t* __restrict__ stg) {
+    const uint32_t e = tab[x & (kProbScale - 1)];
+    x = (e >> 20) * (x >> 12) + ((e >> 8) & 0xFFF);
+    if (x < kStateLower) {
+        x = (x << 8) | stg[p];
+        ++p;
+        if (x < kStateLower) {
+            x = (x << 8) | stg[p];
+            ++p;
+        }
+    }
+    return e & 0xFF;
+}
+
+// One warp decodes NU segments per lane (segment r = warp*32 + lane + u*128
+// of the task) and writes them out through its staging buffer `ob`.
+template <int NU>
+__device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, int64_t sb, uint32_t lo,
+                                            uint32_t delta, uint32_t plen, uint64_t olen, uint32_t nseg_chunk,
+                                            const uint32_t* __restrict__ seg_state,
+                                            const uint32_t* __restrict__ seg_off, const uint32_t* __restrict__ tab,
+                                            const uint8_t* __restrict__ stage, uint8_t* __restrict__ ob,
+                                            uint8_t* __restrict__ obase, bool out_aligned, int32_t* st) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t K = 1u << seg_shift;
+    const int G = (int)(K >> 4);
+    uint32_t x[NU], p[NU], n[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const int r = warp * 32 + lane + u * kDecThreads;
+        const uint32_t rel = (uint32_t)(s0 + r);
+        if (r < ns) {
+            x[u] = seg_state[sb + rel];
+            p[u] = seg_off[sb + rel] - lo + delta;
+            const uint64_t rem = olen - ((uint64_t)rel << seg_shift);
+            n[u] = rem < K ? (uint32_t)rem : K;
+        } else {  // decodes harmless garbage from stage[0..2K), never written
+            x[u] = kStateLower;
+            p[u] = 0;
+            n[u] = 0;
+        }
+    }
+    for (int g = 0; g < G; ++g) {
+        const uint32_t g0 = (uint32_t)g << 4;
+        uint32_t w[NU][4];
+        bool full = true;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+            w[u][0] = w[u][1] = w[u][2] = w[u][3] = 0;
+            full = full && (n[u] == 0 || g0 + 16 <= n[u]);
+        }
+        if (full) {
+#pragma unroll
+            for (int v = 0; v < 16; ++v) {
+#pragma unroll
+                for (int u = 0; u < NU; ++u) {
+                    const uint32_t sym = dec_step(x[u], p[u], tab, stage);
+                    w[u][v >> 2] |= sym << (8 * (v & 3));
+                }
+            }
+        } else {
+#pragma unroll 1
+            for (int v = 0; v < 16; ++v) {
+#pragma unroll
+                for (int u = 0; u < NU; ++u) {
+                    if (g0 + v < n[u]) {
+                        const uint32_t sym = dec_step(x[u], p[u], tab, stage);
+                        w[u][v >> 2] |= sym << (8 * (v & 3));
+                    }
+                }
+            }
+        }
+        const int slot = g & 3;
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+            *reinterpret_cast<uint4*>(ob + (u * 32 + lane) * kOutStride + slot * 16) =
+                make_uint4(w[u][0], w[u][1], w[u][2], w[u][3]);
+        if (slot == 3) {  // G is a multiple of 4 (K >= 64)
+            __syncwarp();
+            const uint32_t line0 = (uint32_t)(g >> 2) * kOutLine;
+#pragma unroll
+            for (int k = 0; k < NU * 4; ++k) {
+                const int pc = k * 32 + lane;
+                const int u = pc >> 7, ln = (pc >> 2) & 31, part = pc & 3;
+                const int r = warp * 32 + ln + u * kDecThreads;
+                if (r >= ns) continue;
+                const uint64_t seg_start = (uint64_t)(s0 + r) << seg_shift;
+                const uint64_t rem = olen - seg_start;
+                const uint32_t slen = rem < K ? (uint32_t)rem : K;
+                const uint32_t boff = line0 + part * 16;
+                if (boff >= slen) continue;
+                const uint8_t* src = ob + (u * 32 + ln) * kOutStride + part * 16;
+                uint8_t* dst = obase + seg_start + boff;
+                const uint32_t nbytes = min(16u, slen - boff);
+                if (nbytes == 16 && out_aligned) {
+                    st_na_v4(dst, *reinterpret_cast<const uint4*>(src));
+                } else {
+                    for (uint32_t i = 0; i < nbytes; ++i) dst[i] = src[i];
+                }
+            }
+            __syncwarp();
+        }
+    }
+    // chain checks: every segment must end exactly where the next one starts
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const int r = warp * 32 + lane + u * kDecThreads;
+        if (r >= ns) continue;
+        const uint32_t rel = (uint32_t)(s0 + r);
+        uint32_t xe, pe;
+        if (rel + 1 < nseg_chunk) {
+            xe = seg_state[sb + rel + 1];
+            pe = seg_off[sb + rel + 1];
+        } else {
+            xe = kStateLower;
+            pe = plen;
+        }
+        if (x[u] != xe || p[u] - delta + lo != pe) atomicExch(st, DC_CHUNK_CHAIN);
+    }
+}
+
+__global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
+    const uint8_t* __restrict__ base, const uint64_t* __restrict__ blob_off, const uint64_t* __restrict__ blob_len,
+    const uint64_t* __restrict__ out_off, const uint64_t* __restrict__ out_len, uint32_t seg_shift,
+    const int64_t* __restrict__ seg_base, const uint32_t* __restrict__ seg_state,
+    const uint32_t* __restrict__ seg_off, const int4* __restrict__ tasks, int64_t n_tasks,
+    uint8_t* __restrict__ out, int32_t* __restrict__ status) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+    TableSmem& T = *reinterpret_cast<TableSmem*>(smem);
+    uint8_t* stage = smem + sizeof(TableSmem);
+    uint8_t* outbuf = stage + kStageCap + kStageSlack;
+    __shared__ uint64_t bar;
+
+    const int warp = threadIdx.x >> 5;
+    uint8_t* ob = outbuf + warp * kOutWarpBytes;
+    const uint32_t K = 1u << seg_shift;
+
+    const int64_t t_begin = (int64_t)blockIdx.x * n_tasks / gridDim.x;
+    const int64_t t_end = (int64_t)(blockIdx.x + 1) * n_tasks / gridDim.x;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    int cur_chunk = -1;
+    uint32_t phase = 0;
+
+    for (int64_t ti = t_begin; ti < t_end; ++ti) {
+        const int4 task = tasks[ti];
+        const int c = task.x, s0 = task.y, ns = task.z;
+        const uint8_t* blob = base + blob_off[c];
+        const uint8_t* gstream = blob + kHeaderBytes;
+        const uint32_t plen = (uint32_t)(blob_len[c] - kHeaderBytes);
+        const uint64_t olen = out_len[c];
+        const uint32_t nseg_chunk = (uint32_t)((olen + K - 1) >> seg_shift);
+        const int64_t sb = seg_base[c];
+        const uint32_t lo = seg_off[sb + s0];
+        const uint32_t hi = ((uint32_t)(s0 + ns) < nseg_chunk) ? seg_off[sb + s0 + ns] : plen;
+        const uintptr_t gsrc = reinterpret_cast<uintptr_t>(gstream) + lo;
+        const uintptr_t a16 = gsrc & ~(uintptr_t)15;
+        const uint32_t delta = (uint32_t)(gsrc - a16);
+        const uint32_t bytes = (hi >= lo) ? ((hi - lo + delta + 15u) & ~15u) : 0xFFFFFFFFu;
+        const bool stage_ok = bytes <= kStageCap;
+
+        __syncthreads();  // previous task done with stage[] and T
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            const uint32_t nb = stage_ok ? bytes : 0u;
+            mbar_arrive_expect_tx(&bar, nb);
+            for (uint32_t off = 0; off < nb; off += 16384u)
+                bulk_g2s(stage + off, reinterpret_cast<const void*>(a16 + off), min(16384u, nb - off), &bar);
+        }
+        if (c != cur_chunk) {
+            build_decode_table(blob, T);  // overlaps the bulk copy
+            cur_chunk = c;
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        if (!stage_ok) {  // index/host invariant broken: let the exact path decide
+            if (threadIdx.x == 0) atomicExch(&status[c], DC_CHUNK_CHAIN);
+            continue;
+        }
+
+        uint8_t* obase = out + out_off[c];
+        const bool out_aligned = ((reinterpret_cast<uintptr_t>(obase) | (uintptr_t)K) & 15) == 0;
+
+        if (T.single >= 0) {  // f = 4096: output is one repeated byte
+            const uint64_t from = (uint64_t)s0 << seg_shift;
+            uint64_t to = (uint64_t)(s0 + ns) << seg_shift;
+            if (to > olen) to = olen;
+            const uint8_t sym = (uint8_t)T.single;
+            for (uint64_t i = from + threadIdx.x; i < to; i += blockDim.x) obase[i] = sym;
+            if (threadIdx.x == 0 && s0 == 0) {
+                const uint32_t x0 = ld_u32_le_unaligned(blob + kTableBytes);
+                if (x0 != kStateLower || plen != 0) atomicExch(&status[c], DC_CHUNK_CORRUPT);
+            }
+            continue;
+        }
+
+        if (warp * 32 >= ns) continue;  // idle warp in a short task
+        if (warp * 32 + kDecThreads < ns)
+            decode_warp<2>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state, seg_off, T.tab,
+                           stage, ob, obase, out_aligned, &status[c]);
+        else
+            decode_warp<1>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state, seg_off, T.tab,
+                           stage, ob, obase, out_aligned, &status[c]);
+    }
+}
+
+// -------------------------------------------------------------- store copy
+__global__ void k_store_copy(const uint8_t* __restrict__ base, const uint64_t* __restrict__ blob_off,
+                             const uint64_t* __restrict__ out_off, const uint64_t* __restrict__ out_len,
+                             const uint8_t* __restrict__ codec, int64_t n, uint8_t* __restrict__ out) {
+    for (int64_t c = blockIdx.y; c < n; c += gridDim.y) {
+        if (codec[c] != 0) continue;
+        const uint8_t* s = base + blob_off[c];
+        uint8_t* d = out + out_off[c];
+        const uint64_t len = out_len[c];
+        // align the destination, then 16-byte stores fed by funnel-shifted loads
+        const uint32_t head = (uint32_t)((16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15);
+        const uint64_t h = head < len ? head : len;
+        for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < h; i += gridDim.x * blockDim.x) d[i] = s[i];
+        const uint64_t body = (len - h) & ~(uint64_t)15;
+        const uint8_t* s2 = s + h;
+        uint8_t* d2 = d + h;
+        const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(s2) & 3);
+        const uint32_t* sw = reinterpret_cast<const uint32_t*>(s2 - mis);
+        for (uint64_t v = (uint64_t)(blockIdx.x * blockDim.x + threadIdx.x) * 16; v < body;
+             v += (uint64_t)gridDim.x * blockDim.x * 16) {
+            uint32_t wv[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) wv[k] = (k < 4 || mis) ? __ldg(sw + v / 4 + k) : 0u;
+            uint4 r;
+            r.x = __funnelshift_r(wv[0], wv[1], 8 * mis);
+            r.y = __funnelshift_r(wv[1], wv[2], 8 * mis);
+            r.z = __funnelshift_r(wv[2], wv[3], 8 * mis);
+            r.w = __funnelshift_r(wv[3], wv[4], 8 * mis);
+            *reinterpret_cast<uint4*>(d2 + v) = r;
+        }
+        for (uint64_t i = h + body + blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
+            d[i] = s[i];
+    }
+}
+
+static int g_sm_count = 0;
+int sm_count() {
+    if (!g_sm_count) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sm_count <= 0) g_sm_count = 148;
+    }
+    return g_sm_count;
+}
+
+}  // namespace dc
+
+using namespace dc;
+
+extern "C" int dc_ans_validate(const uint8_t* base, const uint64_t* blob_off, const uint64_t* blob_len,
+                               const uint64_t* out_len, const uint8_t* codec, int64_t n_chunks, int32_t* status,
+                               void* stream) {
+    if (n_chunks < 0) return DC_ERR_ARG;
+    if (n_chunks == 0) return DC_OK;
+    const int threads = 256;
+    const int64_t blocks = (n_chunks * 32 + threads - 1) / threads;
+    k_validate<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(base, blob_off, blob_len, out_len, codec,
+                                                                      n_chunks, status);
+    DC_CHECK_LAUNCH("k_validate");
+    return DC_OK;
+}
+
+extern "C" int dc_ans_decode_serial(const uint8_t* base, const uint64_t* blob_off, const uint64_t* blob_len,
+                                    const uint64_t* out_off, const uint64_t* out_len, const int32_t* chunk_ids,
+                                    int64_t n_ids, uint8_t* out, uint32_t seg_shift, const int64_t* seg_base,
+                                    uint32_t* seg_state, uint32_t* seg_off, int32_t* status, void* stream) {
+    if (n_ids < 0 || (seg_state && (seg_shift < 4 || seg_shift > 20))) return DC_ERR_ARG;
+    if (n_ids == 0) return DC_OK;
+    const int64_t grid = n_ids < (int64_t)sm_count() * 12 ? n_ids : (int64_t)sm_count() * 12;
+    k_decode_serial<<<(unsigned)grid, kSerialThreads, 0, (cudaStream_t)stream>>>(
+        base, blob_off, blob_len, out_off, out_len, chunk_ids, n_ids, out, seg_shift, seg_base, seg_state, seg_off,
+        status);
+    DC_CHECK_LAUNCH("k_decode_serial");
+    return DC_OK;
+}
+
+extern "C" int dc_decode_task_segments(void) { return kTaskSegs; }
+
+extern "C" int dc_ans_decode_segments(const uint8_t* base, const uint64_t* blob_off, const uint64_t* blob_len,
+                                      const uint64_t* out_off, const uint64_t* out_len, uint32_t seg_shift,
+                                      const int64_t* seg_base, const uint32_t* seg_state, const uint32_t* seg_off,
+                                      const int32_t* tasks, int64_t n_tasks, uint8_t* out, int32_t* status,
+                                      void* stream) {
+    if (n_tasks < 0 || seg_shift < 6 || seg_shift > 10) return DC_ERR_ARG;
+    if (n_tasks == 0) return DC_OK;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_decode_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem);
+        attr = true;
+    }
+    const int64_t cap = (int64_t)sm_count() * 2;
+    const int64_t grid = n_tasks < cap ? n_tasks : cap;
+    k_decode_segments<<<(unsigned)grid, kDecThreads, kDecSmem, (cudaStream_t)stream>>>(
+        base, blob_off, blob_len, out_off, out_len, seg_shift, seg_base, seg_state, seg_off,
+        reinterpret_cast<const int4*>(tasks), n_tasks, out, status);
+    DC_CHECK_LAUNCH("k_decode_segments");
+    return DC_OK;
+}
+
+extern "C" int dc_store_copy(const uint8_t* base, const uint64_t* blob_off, const uint64_t* out_off,
+                             const uint64_t* out_len, const uint8_t* codec, int64_t n_chunks, uint8_t* out,
+                             void* stream) {
+    if (n_chunks < 0) return DC_ERR_ARG;
+    if (n_chunks == 0) return DC_OK;
+    dim3 grid(8, (unsigned)(n_chunks < 65535 ? n_chunks : 65535));
+    k_store_copy<<<grid, 256, 0, (cudaStream_t)stream>>>(base, blob_off, out_off, out_len, codec, n_chunks, out);
+    DC_CHECK_LAUNCH("k_store_copy");
+    return DC_OK;
+}

@@ -1,0 +1,349 @@
+"""Device-side engine: chunk job tables, the split-point index, and the
+decode / encode pipelines over the C-ABI kernels.
+
+Data layout in HBM:
+  * ``base``      uint8: the chunk payloads exactly as in the DCC1 file
+                  (the whole file image, or any buffer holding blobs), with
+                  READ_SLACK readable bytes past the end.
+  * job table     five device arrays (blob_off, blob_len, out_off, out_len,
+                  codec), one entry per chunk.
+  * SegmentIndex  per ANS chunk ceil(len / 2^shift) split points
+                  (state u32, stream offset u32): 8 bytes per segment.  It
+                  lives OUTSIDE the DCC1 bytes (which stay bit-exact) and is
+                  only an accelerator: a wrong index is detected by the chain
+                  checks and the chunk is re-decoded exactly.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import math
+import struct
+import zlib
+
+import numpy as np
+import torch
+
+from . import native as nv
+
+HEADER_BYTES = 388
+DEFAULT_SEG_SHIFT = 9          # 512-symbol segments: 8 B of index per 512 B of weights
+STAGE_CAP = 64 * 1024 - 16     # kStageCap in rans_decode.cu minus alignment slop
+
+
+def _dev():
+    return nv.require_cuda()
+
+
+def _t(a: np.ndarray, dtype, device) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dtype)
+
+
+@dataclasses.dataclass
+class JobTable:
+    """Chunk jobs inside one device byte buffer."""
+
+    n: int
+    blob_off: np.ndarray   # u64 host copies
+    blob_len: np.ndarray
+    out_off: np.ndarray
+    out_len: np.ndarray
+    codec: np.ndarray      # u8
+    d_blob_off: torch.Tensor
+    d_blob_len: torch.Tensor
+    d_out_off: torch.Tensor
+    d_out_len: torch.Tensor
+    d_codec: torch.Tensor
+
+    @classmethod
+    def build(cls, blob_off, blob_len, out_off, out_len, codec, device=None) -> "JobTable":
+        dev = device or _dev()
+        arrs = [np.ascontiguousarray(a, dtype=np.uint64) for a in (blob_off, blob_len, out_off, out_len)]
+        cod = np.ascontiguousarray(codec, dtype=np.uint8)
+        d = [_t(a.view(np.int64), torch.int64, dev) for a in arrs]
+        return cls(len(cod), *arrs, cod, *d, _t(cod, torch.uint8, dev))
+
+    @property
+    def total_out(self) -> int:
+        return int(self.out_off[-1] + self.out_len[-1]) if self.n else 0
+
+
+@dataclasses.dataclass
+class SegmentIndex:
+    """Split points of every ANS chunk (device arrays + host copies)."""
+
+    seg_shift: int
+    seg_base: np.ndarray       # i64 per chunk (first segment), host
+    n_segs: int
+    d_seg_base: torch.Tensor   # int64 [n_chunks]
+    d_state: torch.Tensor      # int32 storage of u32 [n_segs]
+    d_off: torch.Tensor        # int32 storage of u32 [n_segs]
+
+    @staticmethod
+    def layout(out_len: np.ndarray, codec: np.ndarray, seg_shift: int) -> tuple[np.ndarray, int]:
+        K = 1 << seg_shift
+        nseg = np.where(codec == 1, (out_len.astype(np.int64) + K - 1) // K, 0)
+        base = np.zeros(len(nseg), dtype=np.int64)
+        if len(nseg):
+            base[1:] = np.cumsum(nseg)[:-1]
+        return base, int(nseg.sum())
+
+    @classmethod
+    def empty(cls, jobs: JobTable, seg_shift: int = DEFAULT_SEG_SHIFT, device=None) -> "SegmentIndex":
+        dev = device or _dev()
+        base, n = cls.layout(jobs.out_len, jobs.codec, seg_shift)
+        return cls(seg_shift, base, n, _t(base, torch.int64, dev),
+                   torch.zeros(max(n, 1), dtype=torch.int32, device=dev),
+                   torch.zeros(max(n, 1), dtype=torch.int32, device=dev))
+
+    @property
+    def nbytes(self) -> int:
+        return 8 * self.n_segs
+
+    def host_arrays(self) -> tuple[np.ndarray, np.ndarray]:
+        return (self.d_state[: self.n_segs].cpu().numpy().view(np.uint32),
+                self.d_off[: self.n_segs].cpu().numpy().view(np.uint32))
+
+    # ---- sidecar (".dcidx") -------------------------------------------------
+    MAGIC = b"DCIX"
+
+    def to_bytes(self, binding: int) -> bytes:
+        st, off = self.host_arrays()
+        head = self.MAGIC + struct.pack("<HIIQ", 1, self.seg_shift, binding, self.n_segs)
+        body = st.tobytes() + off.tobytes()
+        return head + body + struct.pack("<I", zlib.crc32(body))
+
+    @classmethod
+    def from_bytes(cls, buf: bytes, jobs: JobTable, binding: int, device=None) -> "SegmentIndex | None":
+        """Load a sidecar; None if it does not belong to this container."""
+        if len(buf) < 26 or buf[:4] != cls.MAGIC:
+            return None
+        ver, shift, bind, n = struct.unpack_from("<HIIQ", buf, 4)
+        if ver != 1 or bind != binding or not 6 <= shift <= 10:
+            return None
+        base, want = cls.layout(jobs.out_len, jobs.codec, shift)
+        body = buf[22:22 + 8 * n]
+        if n != want or len(buf) != 22 + 8 * n + 4 or zlib.crc32(body) != struct.unpack_from("<I", buf, 22 + 8 * n)[0]:
+            return None
+        st = np.frombuffer(body, np.uint32, n, 0)
+        off = np.frombuffer(body, np.uint32, n, 4 * n)
+        dev = device or _dev()
+        return cls(shift, base, n, _t(base, torch.int64, dev), _t(st.view(np.int32), torch.int32, dev),
+                   _t(off.view(np.int32), torch.int32, dev))
+
+    # ---- work decomposition -------------------------------------------------
+    def tasks(self, jobs: JobTable, ok: np.ndarray, max_segs: int | None = None) -> torch.Tensor:
+        """int32 [n_tasks, 4] = (chunk, first segment, count, 0): at most
+        ``max_segs`` segments and at most STAGE_CAP staged stream bytes each."""
+        max_segs = max_segs or nv.call("dc_decode_task_segments")
+        K = 1 << self.seg_shift
+        sel = np.nonzero((jobs.codec == 1) & ok & (jobs.out_len > 0))[0]
+        nseg = (jobs.out_len[sel].astype(np.int64) + K - 1) // K
+        ntask = (nseg + max_segs - 1) // max_segs
+        chunk = np.repeat(sel, ntask)
+        first_task = np.repeat(np.cumsum(ntask) - ntask, ntask)
+        s0 = (np.arange(int(ntask.sum())) - first_task) * max_segs
+        nsg = np.repeat(nseg, ntask)
+        cnt = np.minimum(max_segs, nsg - s0)
+        # stream byte span per task: split the (rare) ones that overflow staging
+        _, off = self.host_arrays()
+        base = self.seg_base[chunk]
+        plen = jobs.blob_len[chunk].astype(np.int64) - HEADER_BYTES
+        lo = off[base + s0].astype(np.int64)
+        end = s0 + cnt
+        hi = np.where(end < nsg, off[np.minimum(base + end, max(self.n_segs - 1, 0))].astype(np.int64), plen)
+        big = np.nonzero(hi - lo + 15 > STAGE_CAP)[0]
+        out = np.stack([chunk, s0, cnt, np.zeros_like(cnt)], axis=1).astype(np.int32)
+        if len(big):
+            extra = []
+            for t in big:
+                c, a, m = int(chunk[t]), int(s0[t]), int(cnt[t])
+                b0 = int(self.seg_base[c])
+                n_c = int(nsg[t])
+                pl = int(plen[t])
+                i = a
+                while i < a + m:
+                    j = i + 1
+                    while j < a + m:
+                        hij = int(off[b0 + j + 1]) if j + 1 < n_c else pl
+                        if hij - int(off[b0 + i]) + 15 > STAGE_CAP:
+                            break
+                        j += 1
+                    extra.append((c, i, j - i, 0))
+                    i = j
+            keep = np.ones(len(out), bool)
+            keep[big] = False
+            out = np.concatenate([out[keep], np.array(extra, dtype=np.int32).reshape(-1, 4)])
+            out = out[np.lexsort((out[:, 1], out[:, 0]))]
+        return torch.from_numpy(np.ascontiguousarray(out)).to(_dev())
+
+
+# ------------------------------------------------------------------ decode
+def validate(base: torch.Tensor, jobs: JobTable, status: torch.Tensor) -> None:
+    nv.call("dc_ans_validate", base.data_ptr(), jobs.d_blob_off.data_ptr(), jobs.d_blob_len.data_ptr(),
+            jobs.d_out_len.data_ptr(), jobs.d_codec.data_ptr(), jobs.n, status.data_ptr(), nv.stream_ptr())
+
+
+def decode_serial(base, jobs: JobTable, ids: np.ndarray, out: torch.Tensor, status: torch.Tensor,
+                  index: SegmentIndex | None = None) -> None:
+    if len(ids) == 0:
+        return
+    d_ids = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)).to(out.device)
+    nv.call("dc_ans_decode_serial", base.data_ptr(), jobs.d_blob_off.data_ptr(), jobs.d_blob_len.data_ptr(),
+            jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(), d_ids.data_ptr(), len(ids), out.data_ptr(),
+            index.seg_shift if index else 0, index.d_seg_base.data_ptr() if index else None,
+            index.d_state.data_ptr() if index else None, index.d_off.data_ptr() if index else None,
+            status.data_ptr(), nv.stream_ptr())
+
+
+def decode_segments(base, jobs: JobTable, index: SegmentIndex, tasks: torch.Tensor, out: torch.Tensor,
+                    status: torch.Tensor) -> None:
+    if tasks.shape[0] == 0:
+        return
+    nv.call("dc_ans_decode_segments", base.data_ptr(), jobs.d_blob_off.data_ptr(), jobs.d_blob_len.data_ptr(),
+            jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(), index.seg_shift, index.d_seg_base.data_ptr(),
+            index.d_state.data_ptr(), index.d_off.data_ptr(), tasks.data_ptr(), tasks.shape[0], out.data_ptr(),
+            status.data_ptr(), nv.stream_ptr())
+
+
+def store_copy(base, jobs: JobTable, out: torch.Tensor) -> None:
+    if not (jobs.codec == 0).any():
+        return
+    nv.call("dc_store_copy", base.data_ptr(), jobs.d_blob_off.data_ptr(), jobs.d_out_off.data_ptr(),
+            jobs.d_out_len.data_ptr(), jobs.d_codec.data_ptr(), jobs.n, out.data_ptr(), nv.stream_ptr())
+
+
+def crc32_ranges(data: torch.Tensor, d_off: torch.Tensor, d_len: torch.Tensor, max_len: int) -> torch.Tensor:
+    n = d_off.shape[0]
+    out = torch.empty(max(n, 1), dtype=torch.int32, device=data.device)
+    if n:
+        nv.call("dc_crc32_ranges", data.data_ptr(), d_off.data_ptr(), d_len.data_ptr(), n, int(max_len),
+                out.data_ptr(), nv.stream_ptr())
+    return out[:n]
+
+
+@dataclasses.dataclass
+class DecodeResult:
+    out: torch.Tensor          # uint8 [total]
+    status: np.ndarray         # int32 per chunk (DC_CHUNK_*)
+    index: SegmentIndex | None
+
+
+def decode_jobs(base: torch.Tensor, jobs: JobTable, index: SegmentIndex | None = None,
+                build_index: bool = False, seg_shift: int = DEFAULT_SEG_SHIFT,
+                tasks: torch.Tensor | None = None, out: torch.Tensor | None = None) -> DecodeResult:
+    """Decode every job into one device buffer.  With an index: segment-
+    parallel kernel (+ exact serial re-run of chunks whose chain breaks).
+    Without: exact serial kernel per chunk (optionally recording an index)."""
+    dev = base.device
+    if out is None:
+        out = nv.device_bytes(jobs.total_out, dev)
+    status = torch.zeros(max(jobs.n, 1), dtype=torch.int32, device=dev)
+    validate(base, jobs, status)
+    st = status[: jobs.n].cpu().numpy()
+    ok = st == nv.CHUNK_OK
+    ans_ids = np.nonzero((jobs.codec == 1) & ok & (jobs.out_len > 0))[0]
+    if index is None and build_index:
+        index = SegmentIndex.empty(jobs, seg_shift, dev)
+        decode_serial(base, jobs, ans_ids, out, status, index)
+    elif index is None:
+        decode_serial(base, jobs, ans_ids, out, status, None)
+    else:
+        if tasks is None:
+            tasks = index.tasks(jobs, ok)
+        decode_segments(base, jobs, index, tasks, out, status)
+        st = status[: jobs.n].cpu().numpy()
+        redo = np.nonzero(st == nv.CHUNK_CHAIN)[0]
+        if len(redo):
+            decode_serial(base, jobs, redo, out, status, None)
+    store_copy(base, jobs, out)
+    return DecodeResult(out, status[: jobs.n].cpu().numpy(), index)
+
+
+# ------------------------------------------------------------------ encode
+@dataclasses.dataclass
+class EncodeResult:
+    n: int
+    chunk_size: int
+    total: int
+    codec: np.ndarray          # u8: 1 = ANS blob, 0 = stored
+    comp_len: np.ndarray       # u64 per chunk
+    crc: np.ndarray            # u32 per chunk (uncompressed bytes)
+    freq: torch.Tensor         # int32 [n, 256]
+    d_tables: torch.Tensor     # uint8 [n, 384]
+    d_state: torch.Tensor      # int32 [n] (u32)
+    d_stream_len: torch.Tensor  # int64 [n]
+    scratch: torch.Tensor      # uint8 [total] encoder output slots
+    index: SegmentIndex | None
+
+
+def encode_payload(payload: torch.Tensor, chunk_size: int, mask: np.ndarray | None,
+                   seg_shift: int | None = DEFAULT_SEG_SHIFT) -> EncodeResult:
+    """Histogram -> normalize -> reverse encode every chunk selected by
+    ``mask`` (None = all); decide codec per chunk like container.pack."""
+    dev = payload.device
+    total = int(payload.numel())
+    n = math.ceil(total / chunk_size) if total else 0
+    sp = nv.stream_ptr()
+    mask = np.ones(n, bool) if mask is None else np.asarray(mask, bool)
+    lens = np.minimum(chunk_size, total - np.arange(n, dtype=np.int64) * chunk_size).astype(np.uint64)
+    hist = torch.empty((max(n, 1), 256), dtype=torch.int32, device=dev)
+    freq = torch.empty((max(n, 1), 256), dtype=torch.int32, device=dev)
+    tables = torch.empty((max(n, 1), 384), dtype=torch.uint8, device=dev)
+    state = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    slen = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    scratch = nv.device_bytes(total, dev)
+    index = None
+    if n:
+        nv.call("dc_hist_chunks", payload.data_ptr(), total, chunk_size, n, hist.data_ptr(), sp)
+        nv.call("dc_normalize_tables", hist.data_ptr(), n, freq.data_ptr(), tables.data_ptr(), sp)
+        todo = torch.from_numpy(mask.astype(np.uint8)).to(dev)
+        if seg_shift is not None:
+            base_np, nseg = SegmentIndex.layout(lens, np.where(mask, 1, 0).astype(np.uint8), seg_shift)
+            index = SegmentIndex(seg_shift, base_np, nseg, _t(base_np, torch.int64, dev),
+                                 torch.zeros(max(nseg, 1), dtype=torch.int32, device=dev),
+                                 torch.zeros(max(nseg, 1), dtype=torch.int32, device=dev))
+        nv.call("dc_ans_encode_chunks", payload.data_ptr(), total, chunk_size, n, todo.data_ptr(),
+                freq.data_ptr(), scratch.data_ptr(), state.data_ptr(), slen.data_ptr(),
+                seg_shift if index else 0, index.d_seg_base.data_ptr() if index else None,
+                index.d_state.data_ptr() if index else None, index.d_off.data_ptr() if index else None, 0, sp)
+    d_off = torch.from_numpy((np.arange(n, dtype=np.int64) * chunk_size)).to(dev)
+    d_len = torch.from_numpy(lens.view(np.int64)).to(dev)
+    crc = crc32_ranges(payload, d_off, d_len, min(chunk_size, total)).cpu().numpy().view(np.uint32)
+    sl = slen[:n].cpu().numpy().view(np.uint64)
+    is_ans = mask & (sl != np.uint64(0xFFFFFFFFFFFFFFFF))
+    comp = np.where(is_ans, sl + HEADER_BYTES, lens).astype(np.uint64)
+    codec = is_ans.astype(np.uint8)
+    if index is not None:
+        # encoder recorded (state, bytes emitted so far); decoder offset = total - emitted
+        d_codec = torch.from_numpy(codec).to(dev)
+        seg_chunk = torch.repeat_interleave(
+            torch.arange(n, device=dev),
+            torch.from_numpy(np.where(mask, (lens.astype(np.int64) + (1 << seg_shift) - 1) >> seg_shift, 0)).to(dev))
+        if index.n_segs:
+            sl_t = slen[:n]
+            emitted = index.d_off[: index.n_segs].to(torch.int64) & 0xFFFFFFFF
+            offs = sl_t[seg_chunk] - emitted
+            index.d_off[: index.n_segs] = offs.to(torch.int32)
+        # chunks that ended up stored carry no segments: rebuild a compact index
+        if not is_ans.all() and index.n_segs:
+            keep_seg = d_codec[seg_chunk].bool()
+            base_np, nseg = SegmentIndex.layout(lens, codec, seg_shift)
+            index = SegmentIndex(seg_shift, base_np, nseg, _t(base_np, torch.int64, dev),
+                                 index.d_state[: index.n_segs][keep_seg].contiguous(),
+                                 index.d_off[: index.n_segs][keep_seg].contiguous())
+            if nseg == 0:
+                index.d_state = torch.zeros(1, dtype=torch.int32, device=dev)
+                index.d_off = torch.zeros(1, dtype=torch.int32, device=dev)
+    return EncodeResult(n, chunk_size, total, codec, comp, crc, freq, tables, state, slen, scratch, index)
+
+
+def assemble(payload: torch.Tensor, enc: EncodeResult, file_off: np.ndarray, dst: torch.Tensor) -> None:
+    if enc.n == 0:
+        return
+    dev = payload.device
+    d_codec = torch.from_numpy(enc.codec).to(dev)
+    d_foff = torch.from_numpy(np.ascontiguousarray(file_off, dtype=np.uint64).view(np.int64)).to(dev)
+    nv.call("dc_assemble_payloads", payload.data_ptr(), enc.total, enc.chunk_size, enc.n, d_codec.data_ptr(),
+            enc.d_tables.data_ptr(), enc.d_state.data_ptr(), enc.d_stream_len.data_ptr(), enc.scratch.data_ptr(),
+            d_foff.data_ptr(), dst.data_ptr(), nv.stream_ptr())

@@ -1,0 +1,136 @@
+"""ctypes binding of the C-ABI library (include/dcomp_b200.h).
+
+The library is built in-tree (``python -m paper_2502_15443_b200._build``) as
+``libdcomp_b200.so``.  There is no CPU fallback: if the library or a CUDA
+device is missing, every GPU entry point raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdcomp_b200.so")
+
+READ_SLACK = 16384  # DC_READ_SLACK
+
+# per-chunk status codes (DC_CHUNK_*)
+CHUNK_OK = 0
+CHUNK_TRUNC_TABLE = 1
+CHUNK_BAD_TABLE = 2
+CHUNK_STATE_RANGE = 3
+CHUNK_EMPTY_BAD = 4
+CHUNK_CORRUPT = 5
+CHUNK_CHAIN = 6
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library or device is not available (no CPU fallback exists)."""
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned an argument or CUDA error."""
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_U64 = ctypes.c_uint64
+_U32 = ctypes.c_uint32
+_I32 = ctypes.c_int32
+
+# name -> argtypes (restype int unless listed in _RESTYPES)
+SIGNATURES: dict[str, list] = {
+    "dc_version": [],
+    "dc_last_error": [],
+    "dc_device_sm_count": [ctypes.c_int],
+    "dc_ans_validate": [_P, _P, _P, _P, _P, _I64, _P, _P],
+    "dc_ans_decode_serial": [_P, _P, _P, _P, _P, _P, _I64, _P, _U32, _P, _P, _P, _P, _P],
+    "dc_decode_task_segments": [],
+    "dc_ans_decode_segments": [_P, _P, _P, _P, _P, _U32, _P, _P, _P, _P, _I64, _P, _P, _P],
+    "dc_store_copy": [_P, _P, _P, _P, _P, _I64, _P, _P],
+    "dc_crc32_ranges": [_P, _P, _P, _I64, _U64, _P, _P],
+    "dc_hist_chunks": [_P, _U64, _U64, _I64, _P, _P],
+    "dc_normalize_tables": [_P, _I64, _P, _P, _P],
+    "dc_ans_encode_chunks": [_P, _U64, _U64, _I64, _P, _P, _P, _P, _P, _U32, _P, _P, _P, _U32, _P],
+    "dc_assemble_payloads": [_P, _U64, _U64, _I64, _P, _P, _P, _P, _P, _P, _P, _P],
+    "dc_quant_absmax": [_P, ctypes.c_int, _P, _I64, _I64, _P, _P, _P],
+    "dc_quantize": [_P, ctypes.c_int, _P, _I64, _I64, ctypes.c_double, _P, _P],
+    "dc_dequantize": [_P, ctypes.c_double, _P, _I64, _I64, _P, _P],
+    "dc_scale_weights": [_P, _P, _I64, _I64, _P, _P],
+    "dc_prune_scratch_bytes": [_I64, _I64, _P],
+    "dc_prune_tensor": [_P, _P, _I64, _I64, _I64, _P, _P, _P],
+    "dc_prune_rows": [_P, _P, _I64, _I64, _I64, _P, _P],
+}
+_RESTYPES = {"dc_last_error": ctypes.c_char_p}
+
+_lib = None
+
+
+def lib():
+    """Load the library (fails loudly: there is no CPU path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeUnavailable(
+            f"{LIB_PATH} is missing; build it with `python -m paper_2502_15443_b200._build`")
+    L = ctypes.CDLL(LIB_PATH)
+    for name, args in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
+    _lib = L
+    return L
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device: the dcomp B200 path has no CPU fallback")
+    lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def call(name: str, *args) -> int:
+    rc = getattr(lib(), name)(*args)
+    if rc < 0:
+        msg = lib().dc_last_error().decode(errors="replace")
+        raise NativeError(f"{name} failed ({rc}): {msg}")
+    return rc
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def device_bytes(nbytes: int, device=None) -> torch.Tensor:
+    """uint8 device buffer of ``nbytes`` with READ_SLACK readable bytes past
+    its end (returned view excludes the slack)."""
+    dev = device if device is not None else require_cuda()
+    raw = torch.empty(int(nbytes) + READ_SLACK, dtype=torch.uint8, device=dev)
+    return raw[: int(nbytes)]
+
+
+def to_device_bytes(data, device=None, pinned: bool = True) -> torch.Tensor:
+    """Host bytes-like / uint8 ndarray -> device buffer with read slack."""
+    import numpy as np
+
+    arr = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data.reshape(-1).view(np.uint8)
+    out = device_bytes(arr.size, device)
+    if arr.size:
+        use_pin = pinned and arr.size >= (1 << 20)
+        host = torch.empty(arr.size, dtype=torch.uint8, pin_memory=use_pin)
+        host.numpy()[:] = arr
+        out.copy_(host, non_blocking=use_pin)
+    return out
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)

@@ -1,0 +1,125 @@
+"""Device-side synthetic model builder for the benchmarks.
+
+Large configs (OPT-1.3B .. LLaMA-13B) are far too big for the host numpy
+generator in f64 (10-100 GB), so the bench draws the same distribution as
+``SynthSpec`` (N(0, 0.2) clipped to +-1 weights, log-normal(-1, 1) channel
+maxima with 2% outlier channels x20) with torch's CUDA generator, then
+quantizes with the compression-aware scale (kernel 1) and packs with the
+GPU encoder (kernel 2).  Parity of those kernels is established on the
+reference's own generator in the tests; here only the shapes matter.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+import torch
+
+from . import container, engine
+from .scaling import quantize_device
+from .tensors import model_layout
+
+
+@dataclasses.dataclass
+class DeviceModel:
+    model: str
+    names: list[str]
+    shapes: list[tuple[int, int]]
+    payload: torch.Tensor       # uint8, concatenated int8 weights (row-major, exporter order)
+    w_scales: list[float]
+    s: list[torch.Tensor]       # f64 per-column scale vectors (device)
+    cm: list[torch.Tensor]      # f64 channel maxima (device)
+    alpha: float
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.payload.numel())
+
+    def offsets(self) -> np.ndarray:
+        sizes = np.array([r * c for r, c in self.shapes], dtype=np.int64)
+        return np.concatenate([[0], np.cumsum(sizes)])
+
+
+def build_model(model: str, alpha: float = 0.5, seed: int = 0, device=None, layers: int | None = None) -> DeviceModel:
+    dev = device or torch.device("cuda")
+    layout = model_layout(model)
+    if layers is not None:
+        per = sum(1 for n, _, _ in layout if n.startswith("layers.0."))
+        layout = layout[: per * layers]
+    total = sum(r * c for _, r, c in layout)
+    from .native import device_bytes
+    payload = device_bytes(total, dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    names, shapes, scales, svec, cms = [], [], [], [], []
+    pos = 0
+    for name, r, c in layout:
+        w = torch.randn((r, c), generator=g, device=dev, dtype=torch.float32).mul_(0.2).clamp_(-1.0, 1.0)
+        cm = torch.exp(torch.randn(c, generator=g, device=dev, dtype=torch.float64) * 1.0 - 1.0)
+        k = int(round(0.02 * c))
+        if k:
+            idx = torch.randperm(c, generator=g, device=dev)[:k]
+            cm[idx] *= 20.0
+        s = torch.clamp(cm, min=1e-8) ** alpha if alpha else torch.ones(c, dtype=torch.float64, device=dev)
+        q = payload[pos:pos + r * c].view(torch.int8).view(r, c)
+        _, ws = quantize_device(w, s, name, out=q)
+        names.append(name)
+        shapes.append((r, c))
+        scales.append(ws)
+        svec.append(s)
+        cms.append(cm)
+        pos += r * c
+        del w
+    return DeviceModel(model, names, shapes, payload, scales, svec, cms, alpha)
+
+
+def header_for(m: DeviceModel, chunk_size: int) -> bytes:
+    """DCC1 header body for a device model (f32 s / cm as the format stores)."""
+    import struct
+    import zlib
+    parts = [struct.pack("<II", chunk_size, len(m.names))]
+    for name, (r, c), ws, s, cm in zip(m.names, m.shapes, m.w_scales, m.s, m.cm):
+        nb = name.encode()
+        parts += [struct.pack("<H", len(nb)), nb, struct.pack("<IIdd", r, c, ws, m.alpha),
+                  s.cpu().numpy().astype("<f4").tobytes(), cm.cpu().numpy().astype("<f4").tobytes()]
+    body = b"".join(parts)
+    return body + struct.pack("<I", zlib.crc32(body))
+
+
+@dataclasses.dataclass
+class PackedModel:
+    image: torch.Tensor          # device DCC1 file image
+    entries: np.ndarray
+    jobs: engine.JobTable
+    index: engine.SegmentIndex | None
+    tasks: torch.Tensor | None
+    chunk_size: int
+
+    @property
+    def file_bytes(self) -> int:
+        return int(self.image.numel())
+
+    @property
+    def comp_bytes(self) -> int:
+        return int(self.entries["comp_len"].sum())
+
+    @property
+    def raw_bytes(self) -> int:
+        return int(self.entries["uncomp_len"].sum())
+
+
+def pack_model(m: DeviceModel, chunk_size: int, plan=None, seg_shift: int = engine.DEFAULT_SEG_SHIFT) -> PackedModel:
+    header = header_for(m, chunk_size)
+    image, enc, entries = container.pack_device(m.payload, header, chunk_size, plan, seg_shift)
+    jobs = container.jobs_for(entries, image.device)
+    tasks = None
+    if enc.index is not None:
+        ok = np.ones(jobs.n, bool)
+        tasks = enc.index.tasks(jobs, ok)
+    return PackedModel(image, entries, jobs, enc.index, tasks, chunk_size)
+
+
+def n_chunks(total: int, chunk_size: int) -> int:
+    return math.ceil(total / chunk_size)

@@ -1,0 +1,89 @@
+"""GPU parity of the rANS codec against the reference's golden blobs and the
+C oracle: bit-exact blobs, tables, decoded bytes and error verdicts."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import split_concat
+
+pytestmark = pytest.mark.gpu
+
+
+def test_for_data_and_blobs_bit_exact(cuda, codec_golden):
+    datas = split_concat(codec_golden["data"], codec_golden["data_len"])
+    blobs = split_concat(codec_golden["blob"], codec_golden["blob_len"])
+    for d, b, f in zip(datas, blobs, codec_golden["freq"]):
+        assert np.array_equal(cuda.AnsTable.for_data(d).frequencies, f)
+        assert cuda.compress_blob(d) == b.tobytes()
+        assert cuda.decompress_blob(b.tobytes(), d.size) == d.tobytes()
+
+
+def test_corrupt_verdicts_match_reference(cuda, golden):
+    for case in golden["corrupt"]["cases"]:
+        blob = bytes.fromhex(case["blob_hex"])
+        want = case["verdict"]
+        try:
+            out = cuda.decompress_blob(blob, case["out_len"])
+            got = {"ok": True, "sha": hashlib.sha256(out).hexdigest()}
+        except cuda.DcompError as e:
+            got = {"ok": False, "cls": type(e).__name__, "msg": str(e)}
+        assert got == want, (case["kind"], case["arg"])
+
+
+def test_random_roundtrips_match_oracle(cuda, oracle):
+    rng = np.random.default_rng(11)
+    for _ in range(60):
+        n = int(rng.integers(1, 40_000))
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            d = rng.integers(0, int(rng.integers(2, 257)), n).astype(np.uint8)
+        elif kind == 1:
+            d = np.clip(np.abs(rng.laplace(0, float(rng.uniform(0.3, 40)), n)), 0, 255).astype(np.uint8)
+        else:
+            d = np.clip(np.round(rng.normal(0, float(rng.uniform(1, 30)), n)), -127, 127).astype(np.int8).view(np.uint8)
+        blob = cuda.compress_blob(d)
+        assert blob == oracle.compress_blob(d)
+        assert cuda.decompress_blob(blob, n) == d.tobytes()
+
+
+def test_decode_blobs_into_grouping_and_isolation(cuda):
+    rng = np.random.default_rng(12)
+    datas = [rng.integers(0, int(rng.integers(2, 200)), 4096).astype(np.uint8) for _ in range(11)]
+    outs = [np.empty(4096, np.uint8) for _ in datas]
+    cuda.ans.decode_blobs_into([(cuda.compress_blob(d), o) for d, o in zip(datas, outs)])
+    for d, o in zip(datas, outs):
+        assert np.array_equal(d, o)
+    # corrupt one lane of four: the error names it
+    datas = [rng.integers(0, 30, 4096).astype(np.uint8) for _ in range(4)]
+    blobs = [bytearray(cuda.compress_blob(d)) for d in datas]
+    blobs[2][cuda.ans.HEADER_BYTES + 5] ^= 0x55
+    outs = [np.empty(4096, np.uint8) for _ in range(4)]
+    with pytest.raises(cuda.CorruptStreamError, match="chunk c2"):
+        cuda.ans.decode_blobs_into([(bytes(b), o) for b, o in zip(blobs, outs)], labels=["c0", "c1", "c2", "c3"])
+    # mixed lengths
+    datas = [rng.integers(0, 50, n).astype(np.uint8) for n in (100, 100, 100, 100, 7, 7, 9)]
+    outs = [np.empty(d.size, np.uint8) for d in datas]
+    cuda.ans.decode_blobs_into([(cuda.compress_blob(d), o) for d, o in zip(datas, outs)])
+    assert all(np.array_equal(d, o) for d, o in zip(datas, outs))
+
+
+def test_edge_cases(cuda):
+    with pytest.raises(cuda.DcompError, match="empty input"):
+        cuda.ans_compress(np.empty(0, np.uint8))
+    for b in (0, 7, 255):
+        d = np.array([b], np.uint8)
+        assert cuda.decompress_blob(cuda.compress_blob(d), 1) == d.tobytes()
+    big = np.full(10_000, 9, np.uint8)
+    blob = cuda.compress_blob(big)
+    assert len(blob) <= 420
+    q = np.random.default_rng(6).integers(-128, 128, 1000).astype(np.int8)
+    assert np.array_equal(np.frombuffer(cuda.decompress_blob(cuda.compress_blob(q), 1000), np.int8), q)
+    t = cuda.AnsTable.for_data(np.array([3, 9] * 51 + [3], np.uint8))
+    assert t.frequencies[3] > t.frequencies[9]
+
+
+def test_long_stream(cuda):
+    d = np.abs(np.random.default_rng(7).laplace(0, 6, 2**20)).astype(np.uint8)
+    assert cuda.decompress_blob(cuda.compress_blob(d), d.size) == d.tobytes()

@@ -1,0 +1,158 @@
+"""GPU parity of DCC1 pack/unpack: bit-exact container bytes against the
+reference's golden files / digests, split-point decode == exact decode,
+reference error classes and chunk indices on corrupted inputs."""
+
+import hashlib
+import struct
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def small_model(dc, seed=0, rows=64, cols=96):
+    rng = np.random.default_rng(seed)
+    tensors, stats = [], {}
+    for i, name in enumerate(("alpha", "beta", "gamma")):
+        q = rng.integers(-30, 31, (rows + i, cols)).astype(np.int8)
+        sv = dc.ScaleVector(0.5, np.exp(rng.normal(0, 0.2, cols)))
+        tensors.append(dc.QuantizedTensor(name, q, float(rng.uniform(0.001, 0.1)), sv))
+        stats[name] = dc.ActivationStats(name, np.abs(rng.normal(0, 1, cols)))
+    return tensors, stats
+
+
+@pytest.mark.parametrize("bs", [0, 1, 2, 5])
+def test_pack_bit_exact_vs_reference(cuda, golden, bs):
+    tensors, stats = small_model(cuda)
+    n = -(-sum(t.qvalues.size for t in tensors) // 4096)
+    plan = cuda.CompressionPlan.block_plan(4096, n, bs)
+    blob = cuda.pack(tensors, stats, chunk_size=4096, plan=plan)
+    assert hashlib.sha256(blob).hexdigest() == golden["containers"][f"small_bs{bs}"]["sha"]
+    bundle = cuda.unpack(blob)
+    for a, b in zip(tensors, bundle.tensors):
+        assert np.array_equal(a.qvalues, b.qvalues) and a.w_scale == b.w_scale
+
+
+def test_short_last_chunk_and_empty(cuda, golden):
+    tensors, stats = small_model(cuda, rows=100, cols=41)
+    blob = cuda.pack(tensors, stats, chunk_size=4096)
+    assert hashlib.sha256(blob).hexdigest() == golden["containers"]["small_short"]["sha"]
+    empty = cuda.pack([], {})
+    assert empty.hex() == golden["containers"]["empty"]["hex"]
+    assert cuda.unpack(empty).tensors == []
+
+
+@pytest.mark.parametrize("name", ["small_bs0", "small_bs1", "small_bs2", "small_bs5", "small_short"])
+def test_unpack_reference_files(cuda, oracle, name):
+    data = open(f"{GOLDEN}/{name}.dcc", "rb").read()
+    want = oracle.unpack(data)
+    got = cuda.unpack(data)
+    for (n, q, ws, a, s, cm), t in zip(want, got.tensors):
+        assert t.name == n and np.array_equal(t.qvalues, q) and t.w_scale == ws
+        assert np.array_equal(t.scale_vec.s, s) and np.array_equal(got.stats[n].channel_max, cm)
+
+
+def test_split_point_decode_equals_exact(cuda):
+    from paper_2502_15443_b200 import container, engine
+    rng = np.random.default_rng(3)
+    for cs, shift in ((4096, 6), (65536, 9), (1 << 20, 9), (300_000, 10), (123_457, 7)):
+        q = np.clip(np.round(rng.normal(0, 9, (700, 1500))), -127, 127).astype(np.int8)
+        q[:, :40] = 0  # a run of zeros
+        t = cuda.QuantizedTensor("w", q, 0.01, cuda.ScaleVector.identity(1500))
+        st = {"w": cuda.ActivationStats("w", np.ones(1500))}
+        data, index = container.pack_indexed([t], st, chunk_size=cs, seg_shift=shift)
+        assert data == cuda.pack([t], st, chunk_size=cs)
+        ent = container._parse(data)[2]
+        base = cuda.native.to_device_bytes(data)
+        jobs = container.jobs_for(ent)
+        exact = engine.decode_jobs(base, jobs, build_index=True, seg_shift=shift)
+        fast = engine.decode_jobs(base, jobs, index=index)
+        assert (exact.status == 0).all() and (fast.status == 0).all()
+        assert torch.equal(exact.out, fast.out)
+        assert np.array_equal(exact.out.cpu().numpy().view(np.int8).reshape(q.shape), q)
+        # the serially built index equals the encoder's
+        a1, b1 = index.host_arrays()
+        a2, b2 = exact.index.host_arrays()
+        assert np.array_equal(a1, a2) and np.array_equal(b1, b2)
+        assert np.array_equal(cuda.unpack(data, index=index).tensors[0].qvalues, q)
+
+
+def test_broken_index_falls_back_exactly(cuda):
+    from paper_2502_15443_b200 import container, engine
+    rng = np.random.default_rng(4)
+    q = np.clip(np.round(rng.normal(0, 9, (300, 1000))), -127, 127).astype(np.int8)
+    t = cuda.QuantizedTensor("w", q, 0.01, cuda.ScaleVector.identity(1000))
+    st = {"w": cuda.ActivationStats("w", np.ones(1000))}
+    data, index = container.pack_indexed([t], st, chunk_size=65536, seg_shift=8)
+    index.d_state[5] += 1  # corrupt one split point
+    index.d_off[17] += 3
+    assert np.array_equal(cuda.unpack(data, index=index).tensors[0].qvalues, q)
+
+
+def test_sidecar_roundtrip(cuda, tmp_path):
+    rng = np.random.default_rng(5)
+    q = np.clip(np.round(rng.normal(0, 9, (200, 1000))), -127, 127).astype(np.int8)
+    t = cuda.QuantizedTensor("w", q, 0.01, cuda.ScaleVector.identity(1000))
+    st = {"w": cuda.ActivationStats("w", np.ones(1000))}
+    p = tmp_path / "m.dcc"
+    cuda.write_container(p, [t], st, chunk_size=65536, sidecar=True)
+    assert (tmp_path / "m.dcc.dcidx").exists()
+    assert np.array_equal(cuda.container.read_container(p).tensors[0].qvalues, q)
+
+
+def test_corruption_errors_match_oracle(cuda, oracle):
+    tensors, stats = small_model(cuda, rows=200)
+    data = cuda.pack(tensors, stats, chunk_size=4096)
+    info = cuda.inspect(data)
+    rng = np.random.default_rng(9)
+    checked = 0
+    for _ in range(300):
+        c = info.chunks[int(rng.integers(0, len(info.chunks)))]
+        pos = c.file_offset + int(rng.integers(0, c.comp_len))
+        b = bytearray(data)
+        b[pos] ^= 1 << int(rng.integers(0, 8))
+        b = bytes(b)
+        try:
+            oracle.unpack(b)
+            want = None
+        except oracle.OracleError as e:
+            want = (e.kind, e.msg)
+        try:
+            cuda.unpack(b)
+            got = None
+        except cuda.DcompError as e:
+            got = (type(e).__name__, str(e))
+        assert got == want
+        checked += want is not None
+    assert checked > 250
+
+
+def test_c1_opt125m_digests(cuda, model_digests):
+    """C1 parity config: OPT-125M-shaped synthetic weights, alpha 0.5, per-tensor
+    prune 0.2: GPU quantize+prune+pack bytes == the reference's (SHA-256)."""
+    import importlib
+    tens = importlib.import_module("paper_2502_15443_b200.tensors")
+    for key, alpha, sp in (("opt125m_a0.5_p0.2", 0.5, 0.2), ("opt125m_a0.0_p0.0", 0.0, 0.0)):
+        want = model_digests[key]
+        qts, stats = [], {}
+        h = hashlib.sha256()
+        for i, (name, r, c) in enumerate(tens.model_layout("opt-125m")):
+            w, s = cuda.synth_ensemble(cuda.SynthSpec(rows=r, cols=c, name=name), 1000 + i)
+            qt = cuda.quantize_scaled(w, s, alpha)
+            assert struct.pack("<d", qt.w_scale).hex() == want["w_scales"][i]
+            if sp:
+                qt = cuda.prune(qt, s, cuda.PruneConfig(sp))
+            h.update(qt.qvalues.tobytes())
+            qts.append(qt)
+            stats[name] = s
+        assert h.hexdigest() == want["q_sha"]
+        for cs, meta in want["containers"].items():
+            blob = cuda.pack(qts, stats, chunk_size=int(cs))
+            assert len(blob) == meta["size"]
+            assert hashlib.sha256(blob).hexdigest() == meta["sha"]
+            back = cuda.unpack(blob)
+            assert all(np.array_equal(a.qvalues, b.qvalues) for a, b in zip(qts, back.tensors))

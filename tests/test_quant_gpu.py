@@ -1,0 +1,107 @@
+"""GPU parity of quantization and pruning against reference golden vectors
+and the C oracle (bit-exact q, bit-exact f64 w_scale, identical zero sets)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_quantize_golden(cuda, golden):
+    for c in golden["transforms"]["quantize"]:
+        w = cuda.WeightTensor("g", np.array(c["w"], dtype=np.float64))
+        if "cm" in c:
+            qt = cuda.quantize_scaled(w, cuda.ActivationStats("g", np.array(c["cm"])), c["alpha"])
+            assert np.array_equal(qt.scale_vec.s, np.array(c["s"]))
+        else:
+            qt = cuda.quantize(w)
+        assert np.array_equal(qt.qvalues, np.array(c["q"], dtype=np.int8))
+        assert qt.w_scale.hex() == c["w_scale"]
+
+
+def test_quantize_matches_oracle_random(cuda, oracle):
+    rng = np.random.default_rng(21)
+    for _ in range(12):
+        r, c = int(rng.integers(1, 300)), int(rng.integers(1, 3000))
+        w, st = cuda.synth_ensemble(cuda.SynthSpec(rows=r, cols=c), int(rng.integers(0, 1 << 30)))
+        alpha = float(rng.choice([0.0, 0.25, 0.5, 0.9, 1.0]))
+        qt = cuda.quantize_scaled(w, st, alpha)
+        q, ws = oracle.quantize(w.values, oracle.compute_scale(st.channel_max, alpha))
+        assert np.array_equal(qt.qvalues, q) and qt.w_scale == ws
+        assert qt.qvalues.min() >= -127
+
+
+def test_quantize_errors(cuda):
+    with pytest.raises(cuda.DcompError, match="zero dynamic range"):
+        cuda.quantize(cuda.WeightTensor("z", np.zeros((3, 3))))
+    with pytest.raises(cuda.DcompError, match="empty input"):
+        cuda.quantize(cuda.WeightTensor("e", np.zeros((0, 3))))
+    # max element maps to +-127 exactly; half-away rounding
+    qt = cuda.quantize(cuda.WeightTensor("h", np.array([[1.0, -1.0, 0.0]])))
+    assert qt.qvalues.tolist() == [[127, -127, 0]] and qt.w_scale == 1 / 127
+
+
+def test_device_dtypes_match_f64(cuda):
+    from paper_2502_15443_b200.scaling import quantize_device
+    rng = np.random.default_rng(2)
+    w32 = torch.from_numpy(rng.normal(0, 0.2, (257, 1031)).astype(np.float32)).cuda()
+    for dt in (torch.float32, torch.bfloat16, torch.float16):
+        wd = w32.to(dt)
+        q1, s1 = quantize_device(wd)
+        q2, s2 = quantize_device(wd.to(torch.float64))
+        assert torch.equal(q1, q2) and s1 == s2
+
+
+def test_dequantize_and_scale(cuda):
+    rng = np.random.default_rng(8)
+    w, st = cuda.synth_ensemble(cuda.SynthSpec(rows=64, cols=96), 3)
+    qt = cuda.quantize_scaled(w, st, 0.5)
+    dq = cuda.dequantize(qt)
+    want = qt.qvalues.astype(np.float64) * qt.w_scale / qt.scale_vec.s[None, :]
+    assert np.array_equal(dq.values, want)
+    sw = cuda.scale_weights(w, qt.scale_vec)
+    assert np.array_equal(sw.values, w.values * qt.scale_vec.s[None, :])
+    del rng
+
+
+def test_prune_golden(cuda, golden):
+    for c in golden["transforms"]["prune"]:
+        q = np.array(c["q"], dtype=np.int8)
+        qt = cuda.QuantizedTensor("p", q, 0.1, cuda.ScaleVector.identity(q.shape[1]))
+        st = cuda.ActivationStats("p", np.array(c["cm"]))
+        scope = cuda.PruneScope.PER_ROW if c["per_row"] else cuda.PruneScope.PER_TENSOR
+        out = cuda.prune(qt, st, cuda.PruneConfig(c["sparsity"], scope)).qvalues
+        assert np.array_equal(out, np.array(c["out"], dtype=np.int8))
+
+
+def test_prune_matches_oracle_random(cuda, oracle):
+    rng = np.random.default_rng(33)
+    for _ in range(16):
+        r, c = int(rng.integers(1, 400)), int(rng.integers(1, 900))
+        q = np.clip(np.round(rng.normal(0, float(rng.uniform(1, 40)), (r, c))), -127, 127).astype(np.int8)
+        if rng.random() < 0.3:
+            q[0, 0] = -128
+        cm = rng.choice([0.0, 0.5, 1.0, 2.0, 3.0], c) if rng.random() < 0.5 else rng.lognormal(-1, 1, c)
+        sp = float(rng.choice([0.0, 0.05, 0.2, 0.5, 0.999, 1.0]))
+        per_row = bool(rng.random() < 0.4)
+        qt = cuda.QuantizedTensor("p", q, 0.1, cuda.ScaleVector.identity(c))
+        st = cuda.ActivationStats("p", cm)
+        scope = cuda.PruneScope.PER_ROW if per_row else cuda.PruneScope.PER_TENSOR
+        got = cuda.prune(qt, st, cuda.PruneConfig(sp, scope)).qvalues
+        assert np.array_equal(got, oracle.prune(q, cm, sp, per_row)), (r, c, sp, per_row)
+        if not per_row:
+            newly = (got == 0) & (q != 0)
+            assert (q == 0).sum() + newly.sum() >= int(np.floor(sp * q.size))
+
+
+def test_prune_properties(cuda):
+    rng = np.random.default_rng(44)
+    q = np.clip(np.round(rng.normal(0, 20, (256, 512))), -127, 127).astype(np.int8)
+    qt = cuda.QuantizedTensor("p", q, 0.1, cuda.ScaleVector.identity(512))
+    st = cuda.ActivationStats("p", rng.lognormal(-1, 1, 512))
+    a = cuda.prune(qt, st, cuda.PruneConfig(0.2))
+    b = cuda.prune(a, st, cuda.PruneConfig(0.2))
+    assert np.array_equal(a.qvalues, b.qvalues)  # idempotent
+    c = cuda.prune(qt, st, cuda.PruneConfig(0.4))
+    assert np.all((a.qvalues == 0) <= (c.qvalues == 0))  # nested zero sets
