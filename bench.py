@@ -42,13 +42,13 @@ METRIC = "decode GB/s (decompressed INT8) vs HBM peak; tokens/s compressed vs IN
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--model", default="opt-1.3b")
     p.add_argument("--chunk-size", type=int, default=16 * 2**20)
     p.add_argument("--alpha", type=float, default=0.5)
-    p.add_argument("--seg-shift", type=int, default=9)
+    p.add_argument("--seg-shift", type=int, default=8)
     p.add_argument("--layers", type=int, default=None, help="limit layers (debug only)")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -81,7 +81,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -239,6 +239,8 @@ def main():
         if has_store:
             engine.store_copy(pm.image, pm.jobs, out)
 
+    clocks = ClockSampler(local).__enter__()
+    time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -250,7 +252,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    if True:
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()
         for _ in range(args.steps):
@@ -263,6 +265,7 @@ def main():
             engine.decode_segments(pm.image, pm.jobs, pm.index, pm.tasks, out, status)
         kend.record()
         torch.cuda.synchronize()
+    clocks.__exit__(None, None, None)
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)

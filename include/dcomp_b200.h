@@ -184,6 +184,16 @@ int dc_prune_tensor(const int8_t *q, const double *cm, int64_t rows, int64_t col
 int dc_prune_rows(const int8_t *q, const double *cm, int64_t rows, int64_t cols, int64_t k_per_row, int8_t *out,
                   void *stream);
 
+/* ------------------------------------------- W8A8 GEMM (kernel 3 core)
+ * acc[t, n] (+)= sum_k x[t, k] * w[n, k], int8 x int8 -> exact int32 on
+ * tcgen05 (kind::i8) with TMA-fed SWIZZLE_128B tiles and a TMEM accumulator.
+ * w: [n_rows][k], x: [ntok <= 32][k] row-major int8, k % 128 == 0; kslice
+ * (multiple of 128 dividing k) splits K across CTAs -- then results are
+ * atomically added into acc (caller zeroes it), else stored.
+ * replaces the integer product of scaling.py:148-151 (simulate_layer). */
+int dc_w8a8_gemm(const int8_t *w, int64_t n_rows, int64_t k, const int8_t *x, int64_t ntok, int32_t *acc,
+                 int64_t kslice, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,35 +35,41 @@ struct alignas(128) TableSmem {
     uint32_t warp_tot[4];
 };
 
-// 128 threads: unpack the u12 wire table (ans.py:256-262), fix up the
-// single-symbol case (ans.py:292-295), exclusive cumulative sums
-// (ans.py:301-304), and the slot table (ans.py:306-313) with a compact u32
-// entry.  Tables are validated beforehand by k_validate.
+// Whole CTA (blockDim a multiple of 32, >= 128): unpack the u12 wire table
+// (ans.py:256-262), fix up the single-symbol case (ans.py:292-295), exclusive
+// cumulative sums (ans.py:301-304), and the slot table (ans.py:306-313) with
+// a compact u32 entry.  Tables are validated beforehand by k_validate.
 __device__ void build_decode_table(const uint8_t* __restrict__ tb, TableSmem& T) {
     const int t = threadIdx.x;
-    uint32_t a, b;
-    unpack_pair(tb, t, a, b);
-    // pack (frequency sum, present count) and scan both at once
-    uint32_t v = (a + b) | (((a != 0) + (b != 0)) << 16);
-    uint32_t inc = v;
+    const bool owner = t < 128;  // warps 0-3 own symbol pairs (2t, 2t+1)
+    uint32_t a = 0, b = 0, v = 0, inc = 0;
+    if (owner) {
+        unpack_pair(tb, t, a, b);
+        // pack (frequency sum, present count) and scan both at once
+        v = (a + b) | (((a != 0) + (b != 0)) << 16);
+        inc = v;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if ((t & 31) >= d) inc += o;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if ((t & 31) >= d) inc += o;
+        }
+        if ((t & 31) == 31) T.warp_tot[t >> 5] = inc;
     }
-    if ((t & 31) == 31) T.warp_tot[t >> 5] = inc;
     __syncthreads();
-    uint32_t carry = 0;
-    for (int w = 0; w < (t >> 5); ++w) carry += T.warp_tot[w];
     const uint32_t total = T.warp_tot[0] + T.warp_tot[1] + T.warp_tot[2] + T.warp_tot[3];
-    uint32_t ex = carry + inc - v;
-    uint32_t c0 = ex & 0xFFFF, k0 = ex >> 16;
-    T.freq[2 * t] = a;
-    T.freq[2 * t + 1] = b;
-    T.cum[2 * t] = c0;
-    T.cum[2 * t + 1] = c0 + a;
-    if (a) T.present[k0++] = 2 * t;
-    if (b) T.present[k0] = 2 * t + 1;
+    if (owner) {
+        uint32_t carry = 0;
+        for (int w = 0; w < (t >> 5); ++w) carry += T.warp_tot[w];
+        const uint32_t ex = carry + inc - v;
+        const uint32_t c0 = ex & 0xFFFF;
+        uint32_t k0 = ex >> 16;
+        T.freq[2 * t] = a;
+        T.freq[2 * t + 1] = b;
+        T.cum[2 * t] = c0;
+        T.cum[2 * t + 1] = c0 + a;
+        if (a) T.present[k0++] = 2 * t;
+        if (b) T.present[k0] = 2 * t + 1;
+    }
     if (t == 0) {
         T.npresent = total >> 16;
         T.single = -1;
@@ -71,7 +77,7 @@ __device__ void build_decode_table(const uint8_t* __restrict__ tb, TableSmem& T)
     __syncthreads();
     if ((total & 0xFFFF) == kProbScale - 1) {  // validated: exactly one nonzero entry
         if (t == 0) {
-            int s = T.present[0];
+            const int s = T.present[0];
             T.single = s;
             T.freq[s] = kProbScale;
         }
@@ -80,8 +86,8 @@ __device__ void build_decode_table(const uint8_t* __restrict__ tb, TableSmem& T)
     }
     // fill: warps take present symbols round-robin, lanes stride the slots
     const int np = T.npresent;
-    const int lane = t & 31;
-    for (int i = t >> 5; i < np; i += 4) {
+    const int lane = t & 31, nw = blockDim.x >> 5;
+    for (int i = t >> 5; i < np; i += nw) {
         const uint32_t s = T.present[i];
         const uint32_t f = T.freq[s], c = T.cum[s];
         for (uint32_t k = lane; k < f; k += 32) T.tab[c + k] = s | (k << 8) | (f << 20);
@@ -203,103 +209,151 @@ __global__ void __launch_bounds__(kSerialThreads) k_decode_serial(
 }
 
 // ---------------------------------------------------------- segment decode
-constexpr int kDecThreads = 128;
+constexpr int kDecThreads = 256;                  // 8 warps
 constexpr int kDecWarps = kDecThreads / 32;
-constexpr int kDecIlp = 2;
+constexpr int kDecIlp = 2;                        // segments per lane, interleaved
 constexpr int kTaskSegs = kDecThreads * kDecIlp;  // segments per task
 constexpr uint32_t kStageCap = 64 * 1024;         // staged stream bytes per task
-constexpr uint32_t kStageSlack = 2 * 1024 + 128;  // over-read room (>= 2 * max segment)
-constexpr int kOutLine = 64;                      // bytes per lane-segment per flush
-constexpr int kOutStride = 80;                    // padded: conflict-free 16-B stores
+constexpr uint32_t kStageSlack = 2 * 1024 + 128;  // over-read room (>= 2 * max segment + 1)
+constexpr int kOutLine = 32;                      // bytes per lane-segment per flush
+constexpr int kOutStride = 32;                    // + XOR swizzle of the 16-B halves (see swz)
 constexpr int kOutWarpBytes = kDecIlp * 32 * kOutStride;
-constexpr size_t kDecSmem = sizeof(TableSmem) + kStageCap + kStageSlack + kDecWarps * kOutWarpBytes + 128;
-static_assert(sizeof(TableSmem) % 128 == 0 && (kStageCap + kStageSlack) % 128 == 0, "16-B aligned smem carve-up");
+// dynamic smem carve-up (constant offsets keep the shared address space visible)
+constexpr uint32_t kOffTab = 0;
+constexpr uint32_t kOffStage = ((sizeof(TableSmem) + 127) / 128) * 128;
+constexpr uint32_t kOffOut = kOffStage + kStageCap + kStageSlack;
+constexpr uint32_t kOffBar = kOffOut + kDecWarps * kOutWarpBytes;
+constexpr size_t kDecSmem = kOffBar + 16;
+static_assert(kOffStage % 128 == 0 && kOffOut % 16 == 0 && kOffBar % 8 == 0, "smem carve-up alignment");
 
-__device__ __forceinline__ uint32_t dec_step(uint32_t& x, uint32_t& p, const uint32_t* __restrict__ tab,
-                                             const uint8_t* __restrict__ stg) {
-    const uint32_t e = tab[x & (kProbScale - 1)];
-    x = (e >> 20) * (x >> 12) + ((e >> 8) & 0xFFF);
-    if (x < kStateLower) {
-        x = (x << 8) | stg[p];
-        ++p;
-        if (x < kStateLower) {
-            x = (x << 8) | stg[p];
-            ++p;
-        }
-    }
-    return e & 0xFF;
+// One symbol: table lookup, state update, renormalization.  `p` is the
+// 32-bit shared address of the next unread stream byte and `nb` that byte
+// (prefetched, so the common single-byte refill never waits on a load);
+// x = f*(x>>12) + bias is formed as (e>>20)*((x>>12) - 4096) + (e>>8), since
+// e>>8 == bias + 4096*f (mod 2^32, exact: the true value is < 2^28).  The
+// second refill (only symbols with f < 16 can need it) is a warp-uniform
+// branch when kConverged (all 32 lanes execute the step).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
 }
 
-// One warp decodes NU segments per lane (segment r = warp*32 + lane + u*128
+template <bool kConverged>
+__device__ __forceinline__ uint32_t dec_step(uint32_t& x, uint32_t& p, uint32_t& nb, uint32_t tab) {
+    uint32_t e;
+    // 16 SASS instructions: LOP3, LEA.HI, IMAD, LDS, 2x SHF, IMAD, then two
+    // predicated refills (ISETP + IADD + IMAD + LDS.U8 each).  The second
+    // refill is rare (f < 16) and only its predicate differs between lanes.
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
+        "and.b32 a, %0, 4095;\n\t"
+        "mad.lo.u32 a, a, 4, %4;\n\t"
+        "ld.shared.u32 %3, [a];\n\t"
+        "shr.u32 f, %3, 20;\n\t"
+        "shr.u32 b, %3, 8;\n\t"
+        "shr.u32 t, %0, 12;\n\t"
+        "sub.u32 t, t, 4096;\n\t"
+        "mad.lo.u32 %0, f, t, b;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q mad.lo.u32 %0, %0, 256, %2;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t"
+        "@q ld.shared.u8 %2, [%1];\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q mad.lo.u32 %0, %0, 256, %2;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t"
+        "@q ld.shared.u8 %2, [%1];\n\t}"
+        : "+r"(x), "+r"(p), "+r"(nb), "=r"(e)
+        : "r"(tab));
+    return e;
+}
+
+// 16-B half `h` of lane-segment `ls` in the output staging buffer.  Halves are
+// swapped when bit 2 of the lane is set, which makes both the per-lane
+// 16-B stores (8 lanes per phase) and the per-line 16-B reads conflict-free.
+__device__ __forceinline__ uint32_t swz(int ls, int h) { return (uint32_t)(ls * kOutStride + ((h ^ ((ls >> 2) & 1)) << 4)); }
+
+__device__ __forceinline__ uint32_t put_byte(uint32_t w, uint32_t e, int k) {
+    // byte k of the result <- byte 0 of e (PRMT)
+    return __byte_perm(w, e, k == 0 ? 0x3214 : k == 1 ? 0x3240 : k == 2 ? 0x3410 : 0x4210);
+}
+
+// One warp decodes NU segments per lane (segment r = warp*32 + lane + u*256
 // of the task) and writes them out through its staging buffer `ob`.
 template <int NU>
 __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, int64_t sb, uint32_t lo,
                                             uint32_t delta, uint32_t plen, uint64_t olen, uint32_t nseg_chunk,
                                             const uint32_t* __restrict__ seg_state,
-                                            const uint32_t* __restrict__ seg_off, const uint32_t* __restrict__ tab,
-                                            const uint8_t* __restrict__ stage, uint8_t* __restrict__ ob,
-                                            uint8_t* __restrict__ obase, bool out_aligned, int32_t* st) {
+                                            const uint32_t* __restrict__ seg_off, const uint32_t* tab_ptr,
+                                            const uint8_t* stage_ptr, uint8_t* ob, uint8_t* __restrict__ obase,
+                                            bool out_aligned, int32_t* st) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tab = smem_u32(tab_ptr), stage = smem_u32(stage_ptr);
     const uint32_t K = 1u << seg_shift;
     const int G = (int)(K >> 4);
-    uint32_t x[NU], p[NU], n[NU];
+    uint32_t x[NU], p[NU], n[NU], nb[NU];
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
         const int r = warp * 32 + lane + u * kDecThreads;
         const uint32_t rel = (uint32_t)(s0 + r);
         if (r < ns) {
             x[u] = seg_state[sb + rel];
-            p[u] = seg_off[sb + rel] - lo + delta;
+            p[u] = stage + seg_off[sb + rel] - lo + delta;
             const uint64_t rem = olen - ((uint64_t)rel << seg_shift);
             n[u] = rem < K ? (uint32_t)rem : K;
         } else {  // decodes harmless garbage from stage[0..2K), never written
             x[u] = kStateLower;
-            p[u] = 0;
+            p[u] = stage;
             n[u] = 0;
         }
+        nb[u] = lds_u8(p[u]);
     }
     for (int g = 0; g < G; ++g) {
         const uint32_t g0 = (uint32_t)g << 4;
         uint32_t w[NU][4];
         bool full = true;
 #pragma unroll
-        for (int u = 0; u < NU; ++u) {
-            w[u][0] = w[u][1] = w[u][2] = w[u][3] = 0;
-            full = full && (n[u] == 0 || g0 + 16 <= n[u]);
-        }
-        if (full) {
+        for (int u = 0; u < NU; ++u) full = full && (n[u] == 0 || g0 + 16 <= n[u]);
+        if (__all_sync(0xffffffffu, full)) {
 #pragma unroll
             for (int v = 0; v < 16; ++v) {
 #pragma unroll
                 for (int u = 0; u < NU; ++u) {
-                    const uint32_t sym = dec_step(x[u], p[u], tab, stage);
-                    w[u][v >> 2] |= sym << (8 * (v & 3));
+                    const uint32_t e = dec_step<true>(x[u], p[u], nb[u], tab);
+                    w[u][v >> 2] = put_byte(w[u][v >> 2], e, v & 3);
                 }
             }
         } else {
-#pragma unroll 1
+#pragma unroll
+            for (int u = 0; u < NU; ++u) w[u][0] = w[u][1] = w[u][2] = w[u][3] = 0;
+#pragma unroll
             for (int v = 0; v < 16; ++v) {
 #pragma unroll
                 for (int u = 0; u < NU; ++u) {
                     if (g0 + v < n[u]) {
-                        const uint32_t sym = dec_step(x[u], p[u], tab, stage);
-                        w[u][v >> 2] |= sym << (8 * (v & 3));
+                        const uint32_t e = dec_step<false>(x[u], p[u], nb[u], tab);
+                        w[u][v >> 2] = put_byte(w[u][v >> 2], e, v & 3);
                     }
                 }
             }
         }
-        const int slot = g & 3;
+        const int slot = g & 1;
 #pragma unroll
         for (int u = 0; u < NU; ++u)
-            *reinterpret_cast<uint4*>(ob + (u * 32 + lane) * kOutStride + slot * 16) =
+            *reinterpret_cast<uint4*>(ob + swz(u * 32 + lane, slot)) =
                 make_uint4(w[u][0], w[u][1], w[u][2], w[u][3]);
-        if (slot == 3) {  // G is a multiple of 4 (K >= 64)
+        if (slot == 1) {  // G is even (K >= 64)
             __syncwarp();
-            const uint32_t line0 = (uint32_t)(g >> 2) * kOutLine;
+            const uint32_t line0 = (uint32_t)(g >> 1) * kOutLine;
 #pragma unroll
-            for (int k = 0; k < NU * 4; ++k) {
+            for (int k = 0; k < NU * 2; ++k) {
                 const int pc = k * 32 + lane;
-                const int u = pc >> 7, ln = (pc >> 2) & 31, part = pc & 3;
+                const int u = pc >> 6, ln = (pc >> 1) & 31, part = pc & 1;
                 const int r = warp * 32 + ln + u * kDecThreads;
                 if (r >= ns) continue;
                 const uint64_t seg_start = (uint64_t)(s0 + r) << seg_shift;
@@ -307,7 +361,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
                 const uint32_t slen = rem < K ? (uint32_t)rem : K;
                 const uint32_t boff = line0 + part * 16;
                 if (boff >= slen) continue;
-                const uint8_t* src = ob + (u * 32 + ln) * kOutStride + part * 16;
+                const uint8_t* src = ob + swz(u * 32 + ln, part);
                 uint8_t* dst = obase + seg_start + boff;
                 const uint32_t nbytes = min(16u, slen - boff);
                 if (nbytes == 16 && out_aligned) {
@@ -333,7 +387,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
             xe = kStateLower;
             pe = plen;
         }
-        if (x[u] != xe || p[u] - delta + lo != pe) atomicExch(st, DC_CHUNK_CHAIN);
+        if (x[u] != xe || p[u] - stage - delta + lo != pe) atomicExch(st, DC_CHUNK_CHAIN);
     }
 }
 
@@ -343,21 +397,19 @@ __global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
     const int64_t* __restrict__ seg_base, const uint32_t* __restrict__ seg_state,
     const uint32_t* __restrict__ seg_off, const int4* __restrict__ tasks, int64_t n_tasks,
     uint8_t* __restrict__ out, int32_t* __restrict__ status) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
-    TableSmem& T = *reinterpret_cast<TableSmem*>(smem);
-    uint8_t* stage = smem + sizeof(TableSmem);
-    uint8_t* outbuf = stage + kStageCap + kStageSlack;
-    __shared__ uint64_t bar;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    TableSmem& T = *reinterpret_cast<TableSmem*>(smem + kOffTab);
+    uint8_t* stage = smem + kOffStage;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
 
     const int warp = threadIdx.x >> 5;
-    uint8_t* ob = outbuf + warp * kOutWarpBytes;
+    uint8_t* ob = smem + kOffOut + warp * kOutWarpBytes;
     const uint32_t K = 1u << seg_shift;
 
     const int64_t t_begin = (int64_t)blockIdx.x * n_tasks / gridDim.x;
     const int64_t t_end = (int64_t)(blockIdx.x + 1) * n_tasks / gridDim.x;
     if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
+        mbar_init(bar, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -384,16 +436,16 @@ __global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
         __syncthreads();  // previous task done with stage[] and T
         if (threadIdx.x == 0) {
             fence_proxy_async_smem();
-            const uint32_t nb = stage_ok ? bytes : 0u;
-            mbar_arrive_expect_tx(&bar, nb);
-            for (uint32_t off = 0; off < nb; off += 16384u)
-                bulk_g2s(stage + off, reinterpret_cast<const void*>(a16 + off), min(16384u, nb - off), &bar);
+            const uint32_t nbytes = stage_ok ? bytes : 0u;
+            mbar_arrive_expect_tx(bar, nbytes);
+            for (uint32_t off = 0; off < nbytes; off += 16384u)
+                bulk_g2s(stage + off, reinterpret_cast<const void*>(a16 + off), min(16384u, nbytes - off), bar);
         }
         if (c != cur_chunk) {
             build_decode_table(blob, T);  // overlaps the bulk copy
             cur_chunk = c;
         }
-        mbar_wait(&bar, phase);
+        mbar_wait(bar, phase);
         phase ^= 1u;
         if (!stage_ok) {  // index/host invariant broken: let the exact path decide
             if (threadIdx.x == 0) atomicExch(&status[c], DC_CHUNK_CHAIN);
@@ -415,7 +467,6 @@ __global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
             }
             continue;
         }
-
         if (warp * 32 >= ns) continue;  // idle warp in a short task
         if (warp * 32 + kDecThreads < ns)
             decode_warp<2>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state, seg_off, T.tab,

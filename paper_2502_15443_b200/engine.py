@@ -27,7 +27,7 @@ import torch
 from . import native as nv
 
 HEADER_BYTES = 388
-DEFAULT_SEG_SHIFT = 9          # 512-symbol segments: 8 B of index per 512 B of weights
+DEFAULT_SEG_SHIFT = 8          # 256-symbol segments: 8 B of index per 256 B of weights
 STAGE_CAP = 64 * 1024 - 16     # kStageCap in rans_decode.cu minus alignment slop
 
 

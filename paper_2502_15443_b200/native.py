@@ -63,6 +63,7 @@ SIGNATURES: dict[str, list] = {
     "dc_prune_scratch_bytes": [_I64, _I64, _P],
     "dc_prune_tensor": [_P, _P, _I64, _I64, _I64, _P, _P, _P],
     "dc_prune_rows": [_P, _P, _I64, _I64, _I64, _P, _P],
+    "dc_w8a8_gemm": [_P, _I64, _I64, _P, _I64, _P, _I64, _P],
 }
 _RESTYPES = {"dc_last_error": ctypes.c_char_p}
 
