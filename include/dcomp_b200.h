@@ -194,6 +194,37 @@ int dc_prune_rows(const int8_t *q, const double *cm, int64_t rows, int64_t cols,
 int dc_w8a8_gemm(const int8_t *w, int64_t n_rows, int64_t k, const int8_t *x, int64_t ntok, int32_t *acc,
                  int64_t kslice, void *stream);
 
+/* ------------------------------------- grouped + fused GEMMs (kernel 3)
+ * A "layer table" is a device array of 32-byte records
+ *   { const int8_t *x; int32_t *acc; int64_t t_off; int32_t n_rows; int32_t k; }
+ * (x: [ntok][k] int8 activations, acc: [ntok][n_rows] int32 accumulators the
+ * caller zeroes, t_off: the layer's byte offset in the DCC1 payload) and a
+ * unit table is int32 quads (layer, m0, k0, kslice): 128 weight rows x a
+ * K-slice each.  Every layer of a model runs in ONE launch.  ntok <= 16. */
+int dc_gemm_tensor_bytes(void);
+int dc_tmap_bytes(void);
+/* Host helper: 2 CUtensorMaps per layer (W box 128x128, X box 128x16, SW128)
+ * into maps_host (64-byte aligned). */
+int dc_w8a8_grouped_maps(const int8_t *const *w_host, const int8_t *const *x_host, const int64_t *rows_host,
+                         const int64_t *k_host, int n, int ntok, void *maps_host);
+/* Uncompressed INT8 weights: TMA -> smem -> tcgen05.mma.kind::i8 -> TMEM. */
+int dc_w8a8_grouped(const void *maps, const void *layers, const int32_t *units, int64_t n_units, int ntok,
+                    void *stream);
+
+/* Fused decompress -> W8A8 straight from DCC1 chunks (north-star kernel 3):
+ * each thread decodes one 256-symbol segment of one weight row from its
+ * split point into registers and tcgen05.st's it into the row's TMEM lane;
+ * tcgen05.mma takes A from TMEM (decoded weights never reach HBM).  Index
+ * with seg_shift 8; chunk_size, layer offsets and k multiples of
+ * dc_fused_slice_bytes(); a unit's rows span <= 2 chunks.  Broken chains
+ * set status[chunk] = DC_CHUNK_CHAIN (caller falls back to decode + GEMM).
+ * replaces scaling.py:148-151 on weights decoded by ans.py:71-94. */
+int dc_fused_slice_bytes(void);
+int dc_fused_decode_gemm(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
+                         const uint64_t *out_len, const uint8_t *codec, uint64_t chunk_size, const int64_t *seg_base,
+                         const uint32_t *seg_state, const uint32_t *seg_off, const void *layers,
+                         const int32_t *units, int64_t n_units, int ntok, int32_t *status, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -424,7 +424,7 @@ def unpack(data, index=None) -> ModelBundle:
     if isinstance(index, (bytes, bytearray)):
         index = engine.SegmentIndex.from_bytes(bytes(index), jobs_for(ent, base.device), binding_of(data))
     res = decode_and_verify(base, ent, index=index)
-    return _bundle(directory, res.out.cpu().numpy(), chunk_size)
+    return _bundle(directory, nv.to_host(res.out), chunk_size)
 
 
 def read_container(path) -> ModelBundle:

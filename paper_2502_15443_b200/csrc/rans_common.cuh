@@ -1,0 +1,132 @@
+// Shared rANS decode building blocks (table build, one-symbol step).
+// Reference semantics: /root/reference/pkg/src/dcomp/ans.py:71-94, :301-313.
+#pragma once
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace dc {
+
+// ------------------------------------------------------------------ tables
+struct alignas(128) TableSmem {
+    uint32_t tab[kProbScale];  // slot -> sym | (slot - cum) << 8 | f << 20
+    uint32_t freq[256];
+    uint32_t cum[256];
+    int32_t present[256];
+    int32_t npresent;
+    int32_t single;  // symbol of a single-symbol table, else -1
+    uint32_t warp_tot[4];
+};
+
+// Whole CTA (blockDim a multiple of 32, >= 128): unpack the u12 wire table
+// (ans.py:256-262), fix up the single-symbol case (ans.py:292-295), exclusive
+// cumulative sums (ans.py:301-304), and the slot table (ans.py:306-313) with
+// a compact u32 entry.  Tables are validated beforehand by k_validate.
+static __device__ void build_decode_table(const uint8_t* __restrict__ tb, TableSmem& T) {
+    const int t = threadIdx.x;
+    const bool owner = t < 128;  // warps 0-3 own symbol pairs (2t, 2t+1)
+    uint32_t a = 0, b = 0, v = 0, inc = 0;
+    if (owner) {
+        unpack_pair(tb, t, a, b);
+        // pack (frequency sum, present count) and scan both at once
+        v = (a + b) | (((a != 0) + (b != 0)) << 16);
+        inc = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if ((t & 31) >= d) inc += o;
+        }
+        if ((t & 31) == 31) T.warp_tot[t >> 5] = inc;
+    }
+    __syncthreads();
+    const uint32_t total = T.warp_tot[0] + T.warp_tot[1] + T.warp_tot[2] + T.warp_tot[3];
+    if (owner) {
+        uint32_t carry = 0;
+        for (int w = 0; w < (t >> 5); ++w) carry += T.warp_tot[w];
+        const uint32_t ex = carry + inc - v;
+        const uint32_t c0 = ex & 0xFFFF;
+        uint32_t k0 = ex >> 16;
+        T.freq[2 * t] = a;
+        T.freq[2 * t + 1] = b;
+        T.cum[2 * t] = c0;
+        T.cum[2 * t + 1] = c0 + a;
+        if (a) T.present[k0++] = 2 * t;
+        if (b) T.present[k0] = 2 * t + 1;
+    }
+    if (t == 0) {
+        T.npresent = total >> 16;
+        T.single = -1;
+    }
+    __syncthreads();
+    if ((total & 0xFFFF) == kProbScale - 1) {  // validated: exactly one nonzero entry
+        if (t == 0) {
+            const int s = T.present[0];
+            T.single = s;
+            T.freq[s] = kProbScale;
+        }
+        __syncthreads();
+        return;
+    }
+    // fill: warps take present symbols round-robin, lanes stride the slots
+    const int np = T.npresent;
+    const int lane = t & 31, nw = blockDim.x >> 5;
+    for (int i = t >> 5; i < np; i += nw) {
+        const uint32_t s = T.present[i];
+        const uint32_t f = T.freq[s], c = T.cum[s];
+        for (uint32_t k = lane; k < f; k += 32) T.tab[c + k] = s | (k << 8) | (f << 20);
+    }
+    __syncthreads();
+}
+
+// One symbol: table lookup, state update, renormalization.  `p` is the
+// 32-bit shared address of the next unread stream byte and `nb` that byte
+// (prefetched, so the common single-byte refill never waits on a load);
+// x = f*(x>>12) + bias is formed as (e>>20)*((x>>12) - 4096) + (e>>8), since
+// e>>8 == bias + 4096*f (mod 2^32, exact: the true value is < 2^28).  The
+// second refill (only symbols with f < 16 can need it) is a warp-uniform
+// branch when kConverged (all 32 lanes execute the step).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+template <bool kConverged>
+__device__ __forceinline__ uint32_t dec_step(uint32_t& x, uint32_t& p, uint32_t& nb, uint32_t tab) {
+    uint32_t e;
+    // 16 SASS instructions: LOP3, LEA.HI, IMAD, LDS, 2x SHF, IMAD, then two
+    // predicated refills (ISETP + IADD + IMAD + LDS.U8 each).  The second
+    // refill is rare (f < 16) and only its predicate differs between lanes.
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
+        "and.b32 a, %0, 4095;\n\t"
+        "mad.lo.u32 a, a, 4, %4;\n\t"
+        "ld.shared.u32 %3, [a];\n\t"
+        "shr.u32 f, %3, 20;\n\t"
+        "shr.u32 b, %3, 8;\n\t"
+        "shr.u32 t, %0, 12;\n\t"
+        "sub.u32 t, t, 4096;\n\t"
+        "mad.lo.u32 %0, f, t, b;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q mad.lo.u32 %0, %0, 256, %2;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t"
+        "@q ld.shared.u8 %2, [%1];\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q mad.lo.u32 %0, %0, 256, %2;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t"
+        "@q ld.shared.u8 %2, [%1];\n\t}"
+        : "+r"(x), "+r"(p), "+r"(nb), "=r"(e)
+        : "r"(tab));
+    return e;
+}
+
+__device__ __forceinline__ uint32_t put_byte(uint32_t w, uint32_t e, int k) {
+    // byte k of the result <- byte 0 of e (PRMT)
+    return __byte_perm(w, e, k == 0 ? 0x3214 : k == 1 ? 0x3240 : k == 2 ? 0x3410 : 0x4210);
+}
+
+}  // namespace dc

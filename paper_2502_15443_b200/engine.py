@@ -78,6 +78,7 @@ class SegmentIndex:
     d_seg_base: torch.Tensor   # int64 [n_chunks]
     d_state: torch.Tensor      # int32 storage of u32 [n_segs]
     d_off: torch.Tensor        # int32 storage of u32 [n_segs]
+    h_off: np.ndarray | None = None  # host copy of the offsets when already on the host
 
     @staticmethod
     def layout(out_len: np.ndarray, codec: np.ndarray, seg_shift: int) -> tuple[np.ndarray, int]:
@@ -104,6 +105,11 @@ class SegmentIndex:
         return (self.d_state[: self.n_segs].cpu().numpy().view(np.uint32),
                 self.d_off[: self.n_segs].cpu().numpy().view(np.uint32))
 
+    def host_offsets(self) -> np.ndarray:
+        if self.h_off is None:
+            self.h_off = self.d_off[: self.n_segs].cpu().numpy().view(np.uint32)
+        return self.h_off
+
     # ---- sidecar (".dcidx") -------------------------------------------------
     MAGIC = b"DCIX"
 
@@ -129,7 +135,7 @@ class SegmentIndex:
         off = np.frombuffer(body, np.uint32, n, 4 * n)
         dev = device or _dev()
         return cls(shift, base, n, _t(base, torch.int64, dev), _t(st.view(np.int32), torch.int32, dev),
-                   _t(off.view(np.int32), torch.int32, dev))
+                   _t(off.view(np.int32), torch.int32, dev), h_off=off)
 
     # ---- work decomposition -------------------------------------------------
     def tasks(self, jobs: JobTable, ok: np.ndarray, max_segs: int | None = None) -> torch.Tensor:
@@ -146,7 +152,7 @@ class SegmentIndex:
         nsg = np.repeat(nseg, ntask)
         cnt = np.minimum(max_segs, nsg - s0)
         # stream byte span per task: split the (rare) ones that overflow staging
-        _, off = self.host_arrays()
+        off = self.host_offsets()
         base = self.seg_base[chunk]
         plen = jobs.blob_len[chunk].astype(np.int64) - HEADER_BYTES
         lo = off[base + s0].astype(np.int64)

@@ -67,3 +67,115 @@ def w8a8_matmul_exact(qx: torch.Tensor, qw: torch.Tensor) -> torch.Tensor:
         if part.data_ptr() != out[t0:t1].data_ptr():
             out[t0:t1] = part
     return out
+
+
+# ----------------------------------------------------------------- grouped
+import ctypes  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+_GT_DTYPE = np.dtype([("x", "<u8"), ("acc", "<u8"), ("t_off", "<i8"), ("n_rows", "<i4"), ("k", "<i4")])
+
+
+class _LayerSet:
+    """Per-layer activations and int32 accumulators shared by the grouped
+    INT8 GEMM and the fused decode GEMM (one launch covers every layer)."""
+
+    def __init__(self, shapes, t_offs, xs, ntok: int):
+        assert _GT_DTYPE.itemsize == nv.call("dc_gemm_tensor_bytes")
+        self.shapes = [(int(r), int(k)) for r, k in shapes]
+        self.ntok = ntok
+        self.xs = [x.contiguous() for x in xs]
+        dev = self.xs[0].device
+        sizes = [ntok * r for r, _ in self.shapes]
+        self.acc_flat = torch.zeros(sum(sizes), dtype=torch.int32, device=dev)
+        self.accs, pos = [], 0
+        for (r, _), n in zip(self.shapes, sizes):
+            self.accs.append(self.acc_flat[pos:pos + n].view(ntok, r))
+            pos += n
+        gt = np.zeros(len(self.shapes), dtype=_GT_DTYPE)
+        gt["x"] = [x.data_ptr() for x in self.xs]
+        gt["acc"] = [a.data_ptr() for a in self.accs]
+        gt["t_off"] = np.asarray(t_offs, dtype=np.int64)
+        gt["n_rows"] = [r for r, _ in self.shapes]
+        gt["k"] = [k for _, k in self.shapes]
+        self.tens = torch.from_numpy(gt.view(np.uint8).copy()).to(dev)
+
+    def units(self, kslice_of) -> torch.Tensor:
+        rows = []
+        for li, (r, k) in enumerate(self.shapes):
+            ks = kslice_of(r, k)
+            for m0 in range(0, r, 128):
+                for k0 in range(0, k, ks):
+                    rows.append((li, m0, k0, ks))
+        return torch.tensor(rows, dtype=torch.int32, device=self.xs[0].device)
+
+
+class GroupedInt8:
+    """All linears of a model, uncompressed INT8 weights, one tcgen05 launch."""
+
+    def __init__(self, weights: list[torch.Tensor], xs: list[torch.Tensor], ntok: int):
+        if ntok > 16:
+            raise ValueError("grouped GEMM handles <= 16 tokens per launch")
+        self.layers = _LayerSet([w.shape for w in weights], [0] * len(weights), xs, ntok)
+        self.weights = [w.contiguous() for w in weights]
+        n = len(weights)
+        mb = nv.call("dc_tmap_bytes")
+        host = np.zeros(2 * n * mb + 64, dtype=np.uint8)
+        off = (-host.ctypes.data) % 64
+        maps = host[off:off + 2 * n * mb]
+        P = ctypes.c_void_p
+        w_ptrs = (P * n)(*[w.data_ptr() for w in self.weights])
+        x_ptrs = (P * n)(*[x.data_ptr() for x in self.layers.xs])
+        rows = (ctypes.c_int64 * n)(*[w.shape[0] for w in self.weights])
+        ks = (ctypes.c_int64 * n)(*[w.shape[1] for w in self.weights])
+        nv.lib().dc_w8a8_grouped_maps.argtypes = [P, P, P, P, ctypes.c_int, ctypes.c_int, P]
+        rc = nv.lib().dc_w8a8_grouped_maps(w_ptrs, x_ptrs, rows, ks, n, ntok, maps.ctypes.data)
+        if rc:
+            raise nv.NativeError(f"dc_w8a8_grouped_maps failed ({rc})")
+        self.maps = torch.from_numpy(maps.copy()).to(self.weights[0].device)
+        self.unit_t = self.layers.units(lambda r, k: k)
+
+    @property
+    def accs(self):
+        return self.layers.accs
+
+    def run(self) -> None:
+        self.layers.acc_flat.zero_()
+        nv.call("dc_w8a8_grouped", self.maps.data_ptr(), self.layers.tens.data_ptr(), self.unit_t.data_ptr(),
+                self.unit_t.shape[0], self.layers.ntok, nv.stream_ptr())
+
+
+class FusedCompressed:
+    """All linears of a model straight from the DCC1 container: the fused
+    decode -> TMEM -> tcgen05 W8A8 kernel (one launch)."""
+
+    def __init__(self, image: torch.Tensor, jobs, index, chunk_size: int, shapes, t_offs, xs, ntok: int):
+        if index is None or index.seg_shift != 8:
+            raise ValueError("fused path needs a split-point index with 256-symbol segments")
+        sl = nv.call("dc_fused_slice_bytes")
+        if chunk_size % sl or any(int(t) % sl for t in t_offs) or any(k % sl for _, k in shapes):
+            raise ValueError(f"fused path needs chunk_size, tensor offsets and K multiples of {sl}")
+        for (r, k), t in zip(shapes, t_offs):  # a 128-row tile may touch at most two chunks
+            if 128 * k > chunk_size:
+                raise ValueError("chunk too small for the fused path (128 rows x K must fit in one chunk)")
+        self.image, self.jobs, self.index, self.chunk_size = image, jobs, index, chunk_size
+        self.layers = _LayerSet(shapes, t_offs, xs, ntok)
+        self.unit_t = self.layers.units(lambda r, k: sl)
+        self.status = torch.zeros(max(jobs.n, 1), dtype=torch.int32, device=image.device)
+
+    @property
+    def accs(self):
+        return self.layers.accs
+
+    def run(self) -> None:
+        self.layers.acc_flat.zero_()
+        j, ix = self.jobs, self.index
+        nv.call("dc_fused_decode_gemm", self.image.data_ptr(), j.d_blob_off.data_ptr(), j.d_blob_len.data_ptr(),
+                j.d_out_len.data_ptr(), j.d_codec.data_ptr(), self.chunk_size, ix.d_seg_base.data_ptr(),
+                ix.d_state.data_ptr(), ix.d_off.data_ptr(), self.layers.tens.data_ptr(), self.unit_t.data_ptr(),
+                self.unit_t.shape[0], self.layers.ntok, self.status.data_ptr(), nv.stream_ptr())
+
+    def check(self) -> np.ndarray:
+        """Per-chunk status after run(); nonzero = chain broken / corrupt."""
+        return self.status[: self.jobs.n].cpu().numpy()

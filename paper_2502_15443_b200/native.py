@@ -64,6 +64,12 @@ SIGNATURES: dict[str, list] = {
     "dc_prune_tensor": [_P, _P, _I64, _I64, _I64, _P, _P, _P],
     "dc_prune_rows": [_P, _P, _I64, _I64, _I64, _P, _P],
     "dc_w8a8_gemm": [_P, _I64, _I64, _P, _I64, _P, _I64, _P],
+    "dc_gemm_tensor_bytes": [],
+    "dc_tmap_bytes": [],
+    "dc_w8a8_grouped_maps": [_P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P],
+    "dc_w8a8_grouped": [_P, _P, _P, _I64, ctypes.c_int, _P],
+    "dc_fused_slice_bytes": [],
+    "dc_fused_decode_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P],
 }
 _RESTYPES = {"dc_last_error": ctypes.c_char_p}
 
@@ -119,8 +125,30 @@ def device_bytes(nbytes: int, device=None) -> torch.Tensor:
     return raw[: int(nbytes)]
 
 
+_COPY_POOL = None
+
+
+def _parallel_copy(dst: "np.ndarray", src: "np.ndarray", piece: int = 32 << 20) -> None:
+    """Host memcpy in parallel slices (numpy releases the GIL on large copies)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    global _COPY_POOL
+    n = src.size
+    if n <= piece:
+        np.copyto(dst, src)
+        return
+    if _COPY_POOL is None:
+        _COPY_POOL = ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1))
+    futs = [_COPY_POOL.submit(np.copyto, dst[i:i + piece], src[i:i + piece]) for i in range(0, n, piece)]
+    for f in futs:
+        f.result()
+
+
 def to_device_bytes(data, device=None, pinned: bool = True) -> torch.Tensor:
-    """Host bytes-like / uint8 ndarray -> device buffer with read slack."""
+    """Host bytes-like / uint8 ndarray -> device buffer with read slack.
+    Large inputs go through a (caching-allocator) pinned staging buffer filled
+    by parallel host copies, then one async H2D DMA."""
     import numpy as np
 
     arr = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data.reshape(-1).view(np.uint8)
@@ -128,9 +156,18 @@ def to_device_bytes(data, device=None, pinned: bool = True) -> torch.Tensor:
     if arr.size:
         use_pin = pinned and arr.size >= (1 << 20)
         host = torch.empty(arr.size, dtype=torch.uint8, pin_memory=use_pin)
-        host.numpy()[:] = arr
+        _parallel_copy(host.numpy(), arr)
         out.copy_(host, non_blocking=use_pin)
     return out
+
+
+def to_host(t: torch.Tensor) -> "np.ndarray":
+    """Device tensor -> numpy array backed by pinned host memory (one DMA, no
+    extra host copy); the array keeps the pinned buffer alive."""
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return host.numpy()
 
 
 def exported_symbols() -> list[str]:

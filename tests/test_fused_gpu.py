@@ -1,0 +1,63 @@
+"""Grouped INT8 GEMM and the fused decode -> TMEM -> tcgen05 GEMM: exact
+int32 accumulators vs an int64 CPU product of the same weights."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(256, 512), (384, 1024), (130, 512), (1000, 1536)]
+
+
+def _weights(seed=0):
+    g = torch.Generator().manual_seed(seed)
+    ws = []
+    for r, k in SHAPES:
+        w = torch.round(torch.randn(r, k, generator=g) * 9).clamp_(-127, 127).to(torch.int8)
+        w[:, :17] = 0
+        ws.append(w)
+    return ws
+
+
+def _xs(ntok, seed=1):
+    g = torch.Generator().manual_seed(seed)
+    return [torch.randint(-127, 128, (ntok, k), generator=g, dtype=torch.int8) for _, k in SHAPES]
+
+
+@pytest.mark.parametrize("ntok", [1, 5, 16])
+def test_grouped_int8_exact(cuda, ntok):
+    from paper_2502_15443_b200.gemm import GroupedInt8
+    ws, xs = _weights(), _xs(ntok)
+    gi = GroupedInt8([w.cuda() for w in ws], [x.cuda() for x in xs], ntok)
+    gi.run()
+    for w, x, acc in zip(ws, xs, gi.accs):
+        assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
+
+
+@pytest.mark.parametrize("ntok,stored", [(1, False), (7, True), (16, False)])
+def test_fused_decode_gemm_exact(cuda, ntok, stored):
+    from paper_2502_15443_b200 import container, engine
+    from paper_2502_15443_b200.gemm import FusedCompressed
+    ws, xs = _weights(3), _xs(ntok, 4)
+    payload = torch.cat([w.reshape(-1).view(torch.uint8) for w in ws]).cuda()
+    t_offs = np.concatenate([[0], np.cumsum([w.numel() for w in ws])[:-1]])
+    chunk = 1 << 20
+    n = -(-payload.numel() // chunk)
+    plan = None
+    if stored:  # every other chunk stored raw: exercises the copy path
+        plan = np.array([i % 2 == 0 for i in range(n)])
+    header = b"\x00" * 8
+    image, enc, entries = container.pack_device(payload, header, chunk, plan, seg_shift=8)
+    jobs = container.jobs_for(entries, image.device)
+    fc = FusedCompressed(image, jobs, enc.index, chunk, [w.shape for w in ws], t_offs, [x.cuda() for x in xs], ntok)
+    fc.run()
+    torch.cuda.synchronize()
+    assert (fc.check() == 0).all()
+    for w, x, acc in zip(ws, xs, fc.accs):
+        assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
+    # a corrupted split point is detected (chain check) instead of trusted
+    enc.index.d_state[3] += 1
+    fc.run()
+    torch.cuda.synchronize()
+    assert (fc.check() != 0).any()
