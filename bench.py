@@ -281,6 +281,49 @@ def main():
     alg_bytes = ans_raw + ans_comp  # decompressed bytes written + compressed bytes read
     achieved = alg_bytes / (kms / 1e3) / 1e9
 
+    # decode-step tokens/s: every linear of the model once for B tokens,
+    # INT8 weights vs fused compressed (decode -> TMEM -> tcgen05) vs
+    # decode-to-HBM then INT8 GEMM.  Exactness is checked before timing.
+    from paper_2502_15443_b200.gemm import FusedCompressed, GroupedInt8
+    offs = m.offsets()[:-1]
+    w_int8 = [m.payload[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, m.shapes)]
+    w_dec = [out[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, m.shapes)]
+
+    def time_ms(fn, iters):
+        for _ in range(2):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters
+
+    tokens = {}
+    for B in (1, 16):
+        gx = torch.Generator(device=dev)
+        gx.manual_seed(7 + B)
+        xs = [torch.randint(-127, 128, (B, c), generator=gx, device=dev, dtype=torch.int8) for _, c in m.shapes]
+        gi = GroupedInt8(w_int8, xs, B)
+        gd = GroupedInt8(w_dec, xs, B)
+        fc = FusedCompressed(pm.image, pm.jobs, pm.index, pm.chunk_size, m.shapes, offs, xs, B)
+        gi.run()
+        fc.run()
+        torch.cuda.synchronize()
+        if (fc.check() != 0).any() or not all(torch.equal(a, b) for a, b in zip(gi.accs, fc.accs)):
+            raise SystemExit("fused decode-GEMM mismatch vs INT8 GEMM")
+        iters = max(5, args.steps // 5)
+        t_i8 = time_ms(gi.run, iters)
+        t_fu = time_ms(fc.run, iters)
+        t_un = time_ms(lambda: (step(), gd.run()), iters)
+        tokens[f"B{B}"] = {"int8_tok_s": B / (t_i8 / 1e3), "compressed_fused_tok_s": B / (t_fu / 1e3),
+                           "compressed_unfused_tok_s": B / (t_un / 1e3), "int8_ms": t_i8, "fused_ms": t_fu,
+                           "unfused_ms": t_un, "fused_vs_int8": t_i8 / t_fu,
+                           "int8_weight_gbs": raw / (t_i8 / 1e3) / 1e9}
+        del gi, gd, fc
+
     # e2e through the public API from host bytes (rank 0 reports its own)
     host_file = pm.image.cpu().numpy().tobytes()
     side = pm.index.to_bytes(container.binding_of(host_file))
@@ -324,6 +367,7 @@ def main():
                          "alg_bytes_per_launch": alg_bytes, "launch_ms": kms},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "decode_step_tokens": tokens,
             "gpu_launches": args.steps * (1 + int(has_store)),
             "clocks": clocks.summary(),
         }

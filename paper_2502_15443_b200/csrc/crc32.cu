@@ -93,12 +93,15 @@ __global__ void __launch_bounds__(kCrcThreads) k_crc_pieces(const uint8_t* __res
             const uintptr_t a0 = reinterpret_cast<uintptr_t>(pbeg) & ~(uintptr_t)3;
             const uint32_t sh = 8u * (uint32_t)(reinterpret_cast<uintptr_t>(pbeg) & 3);
             const uintptr_t lo_ok = reinterpret_cast<uintptr_t>(rbeg);
+            const uintptr_t hi_ok = lo_ok + L;
             auto ldw = [&](uintptr_t a) -> uint32_t {  // bytes before the range read as zero
-                if (a >= lo_ok) return *reinterpret_cast<const uint32_t*>(a);
+                if (a >= lo_ok && a + 4 <= hi_ok) return *reinterpret_cast<const uint32_t*>(a);
+                if (a >= hi_ok) return 0u;  // past the range: never read (buffers may lack slack)
                 if (a + 4 <= lo_ok) return 0u;
                 uint32_t v = 0;
                 for (int k = 0; k < 4; ++k)
-                    if (a + k >= lo_ok) v |= (uint32_t)(*reinterpret_cast<const uint8_t*>(a + k)) << (8 * k);
+                    if (a + k >= lo_ok && a + k < hi_ok)
+                        v |= (uint32_t)(*reinterpret_cast<const uint8_t*>(a + k)) << (8 * k);
                 return v;
             };
             uint32_t c = 0;

@@ -224,9 +224,20 @@ __global__ void __launch_bounds__(kEncLanes) k_encode(const uint8_t* __restrict_
     // walk the chunk backwards in aligned 16-byte blocks
     const uintptr_t a_beg = reinterpret_cast<uintptr_t>(src);
     const uintptr_t a_end = a_beg + len;
+    const uintptr_t data_end = reinterpret_cast<uintptr_t>(data) + total;
     uintptr_t blk = (a_end - 1) & ~(uintptr_t)15;
     for (; !stored && blk + 16 > a_beg; blk -= 16) {
-        const uint4 q = *reinterpret_cast<const uint4*>(blk);
+        uint4 q;
+        if (blk + 16 <= data_end) {
+            q = *reinterpret_cast<const uint4*>(blk);
+        } else {  // last block of the buffer: never read past its end
+            uint8_t b[16];
+            for (int k = 0; k < 16; ++k) b[k] = (blk + k < data_end) ? *reinterpret_cast<const uint8_t*>(blk + k) : 0;
+            q.x = b[0] | b[1] << 8 | b[2] << 16 | (uint32_t)b[3] << 24;
+            q.y = b[4] | b[5] << 8 | b[6] << 16 | (uint32_t)b[7] << 24;
+            q.z = b[8] | b[9] << 8 | b[10] << 16 | (uint32_t)b[11] << 24;
+            q.w = b[12] | b[13] << 8 | b[14] << 16 | (uint32_t)b[15] << 24;
+        }
         const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int k = 15; k >= 0; --k) {
