@@ -324,6 +324,22 @@ def main():
                            "int8_weight_gbs": raw / (t_i8 / 1e3) / 1e9}
         del gi, gd, fc
 
+    # config C5 under torchrun: LLaMA-13B-shaped tensor parallelism across
+    # the ranks (fused compressed vs INT8 per rank + NCCL int32 all-reduce)
+    tp = None
+    if world > 1:
+        try:
+            from paper_2502_15443_b200 import tp_step
+            tps = tp_step.TPDecodeStep("llama-13b", world, rank, ntok=1, device=dev)
+            ok = tps.check()
+            tp = tp_step.measure(tps, iters=10)
+            tp.update({"model": "llama-13b", "tp": world, "ntok": 1, "fused_equals_int8": ok,
+                       "int8_tok_s": 1e3 / tp["int8_step_ms"], "compressed_tok_s": 1e3 / tp["compressed_fused_step_ms"]})
+            del tps
+            torch.cuda.empty_cache()
+        except Exception as e:  # report, never hide
+            tp = {"error": repr(e)[:300]}
+
     # e2e through the public API from host bytes (rank 0 reports its own)
     host_file = pm.image.cpu().numpy().tobytes()
     side = pm.index.to_bytes(container.binding_of(host_file))
@@ -368,6 +384,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "decode_step_tokens": tokens,
+            "tp_decode": tp,
             "gpu_launches": args.steps * (1 + int(has_store)),
             "clocks": clocks.summary(),
         }

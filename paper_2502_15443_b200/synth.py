@@ -43,11 +43,17 @@ class DeviceModel:
 
 
 def build_model(model: str, alpha: float = 0.5, seed: int = 0, device=None, layers: int | None = None) -> DeviceModel:
-    dev = device or torch.device("cuda")
     layout = model_layout(model)
     if layers is not None:
         per = sum(1 for n, _, _ in layout if n.startswith("layers.0."))
         layout = layout[: per * layers]
+    return build_from_layout(model, layout, alpha, seed, device)
+
+
+def build_from_layout(model: str, layout, alpha: float = 0.5, seed: int = 0, device=None) -> DeviceModel:
+    """Random-init (SynthSpec distribution) weights of the given (name, rows,
+    cols) list, compression-aware quantized on the GPU."""
+    dev = device or torch.device("cuda")
     total = sum(r * c for _, r, c in layout)
     from .native import device_bytes
     payload = device_bytes(total, dev)
