@@ -416,15 +416,48 @@ def unpack(data, index=None) -> ModelBundle:
     """Decode and verify a container (inverse of pack).  ``index`` (a
     SegmentIndex or sidecar bytes) enables the split-point parallel decoder;
     without it each ANS chunk is decoded by one exact sequential walk."""
+    import time
+    clock = [time.perf_counter()]
+
+    def lap(name):
+        torch.cuda.synchronize()
+        now = time.perf_counter()
+        LAST_UNPACK_MS[name] = (now - clock[0]) * 1e3
+        clock[0] = now
+
     data = _file_bytes(data)
     chunk_size, directory, ent, _ = _parse(data)
     if len(ent) == 0:
         return _bundle(directory, np.empty(0, np.uint8), chunk_size)
+    LAST_UNPACK_MS.clear()
+    lap("parse")
+    if index is not None:  # split-point path: H2D / decode / D2H pipelined per chunk group
+        jobs = jobs_for(ent)
+        if isinstance(index, (bytes, bytearray)):
+            index = engine.SegmentIndex.from_bytes(bytes(index), jobs, binding_of(data))
+        lap("index")
+        if index is not None:
+            host, status, crc = engine.decode_file_pipelined(np.frombuffer(data, np.uint8), jobs, index)
+            lap("pipeline")
+            raise_decode_errors(status)
+            bad = np.nonzero(crc != ent["crc32"])[0]
+            if len(bad):
+                raise ChecksumError(int(bad[0]))
+            out = _bundle(directory, host, chunk_size)
+            lap("bundle")
+            return out
     base = nv.to_device_bytes(data)
-    if isinstance(index, (bytes, bytearray)):
-        index = engine.SegmentIndex.from_bytes(bytes(index), jobs_for(ent, base.device), binding_of(data))
+    lap("h2d")
     res = decode_and_verify(base, ent, index=index)
-    return _bundle(directory, nv.to_host(res.out), chunk_size)
+    lap("decode_crc")
+    host = nv.to_host(res.out)
+    lap("d2h")
+    out = _bundle(directory, host, chunk_size)
+    lap("bundle")
+    return out
+
+
+LAST_UNPACK_MS: dict[str, float] = {}  # phase timings of the last unpack() (diagnostics)
 
 
 def read_container(path) -> ModelBundle:

@@ -72,7 +72,8 @@ static __device__ void build_decode_table(const uint8_t* __restrict__ tb, TableS
     for (int i = t >> 5; i < np; i += nw) {
         const uint32_t s = T.present[i];
         const uint32_t f = T.freq[s], c = T.cum[s];
-        for (uint32_t k = lane; k < f; k += 32) T.tab[c + k] = s | (k << 8) | (f << 20);
+        // bounded even for an invalid table (callers skip such chunks anyway)
+        for (uint32_t k = lane; k < f && c + k < kProbScale; k += 32) T.tab[c + k] = s | (k << 8) | (f << 20);
     }
     __syncthreads();
 }

@@ -143,7 +143,7 @@ constexpr int kDecThreads = 256;                  // 8 warps
 constexpr int kDecWarps = kDecThreads / 32;
 constexpr int kDecIlp = 2;                        // segments per lane, interleaved
 constexpr int kTaskSegs = kDecThreads * kDecIlp;  // segments per task
-constexpr uint32_t kStageCap = 64 * 1024;         // staged stream bytes per task
+constexpr uint32_t kStageCap = 72 * 1024;         // staged stream bytes per task (2 CTAs/SM fit)
 constexpr uint32_t kStageSlack = 2 * 1024 + 128;  // over-read room (>= 2 * max segment + 1)
 constexpr int kOutLine = 32;                      // bytes per lane-segment per flush
 constexpr int kOutStride = 32;                    // + XOR swizzle of the 16-B halves (see swz)
@@ -297,6 +297,10 @@ __global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
     for (int64_t ti = t_begin; ti < t_end; ++ti) {
         const int4 task = tasks[ti];
         const int c = task.x, s0 = task.y, ns = task.z;
+        {  // prologue errors (k_validate, same stream) are never decoded
+            const int32_t st0 = status[c];
+            if (st0 >= DC_CHUNK_TRUNC_TABLE && st0 <= DC_CHUNK_EMPTY_BAD) continue;
+        }
         const uint8_t* blob = base + blob_off[c];
         const uint8_t* gstream = blob + kHeaderBytes;
         const uint32_t plen = (uint32_t)(blob_len[c] - kHeaderBytes);

@@ -147,17 +147,31 @@ def _parallel_copy(dst: "np.ndarray", src: "np.ndarray", piece: int = 32 << 20) 
 
 def to_device_bytes(data, device=None, pinned: bool = True) -> torch.Tensor:
     """Host bytes-like / uint8 ndarray -> device buffer with read slack.
-    Large inputs go through a (caching-allocator) pinned staging buffer filled
-    by parallel host copies, then one async H2D DMA."""
+    Large inputs stream through two pinned staging buffers: the host copy of
+    piece i+1 (parallel memcpy) overlaps the H2D DMA of piece i."""
     import numpy as np
 
     arr = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data.reshape(-1).view(np.uint8)
     out = device_bytes(arr.size, device)
-    if arr.size:
-        use_pin = pinned and arr.size >= (1 << 20)
-        host = torch.empty(arr.size, dtype=torch.uint8, pin_memory=use_pin)
-        _parallel_copy(host.numpy(), arr)
-        out.copy_(host, non_blocking=use_pin)
+    n = arr.size
+    if n == 0:
+        return out
+    if not pinned or n < (4 << 20):
+        out.copy_(torch.from_numpy(arr.copy()))
+        return out
+    piece = 64 << 20
+    stream = torch.cuda.current_stream()
+    bufs = [torch.empty(min(piece, n), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    done = [None, None]
+    for i, off in enumerate(range(0, n, piece)):
+        b = i & 1
+        if done[b] is not None:
+            done[b].synchronize()  # the DMA out of this staging buffer finished
+        ln = min(piece, n - off)
+        _parallel_copy(bufs[b].numpy()[:ln], arr[off:off + ln], piece=8 << 20)
+        out[off:off + ln].copy_(bufs[b][:ln], non_blocking=True)
+        done[b] = torch.cuda.Event()
+        done[b].record(stream)
     return out
 
 
