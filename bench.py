@@ -284,7 +284,7 @@ def main():
     # decode-step tokens/s: every linear of the model once for B tokens,
     # INT8 weights vs fused compressed (decode -> TMEM -> tcgen05) vs
     # decode-to-HBM then INT8 GEMM.  Exactness is checked before timing.
-    from paper_2502_15443_b200.gemm import FusedCompressed, GroupedInt8
+    from paper_2502_15443_b200.gemm import FusedRing, GroupedInt8
     offs = m.offsets()[:-1]
     w_int8 = [m.payload[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, m.shapes)]
     w_dec = [out[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, m.shapes)]
@@ -308,7 +308,7 @@ def main():
         xs = [torch.randint(-127, 128, (B, c), generator=gx, device=dev, dtype=torch.int8) for _, c in m.shapes]
         gi = GroupedInt8(w_int8, xs, B)
         gd = GroupedInt8(w_dec, xs, B)
-        fc = FusedCompressed(pm.image, pm.jobs, pm.index, pm.chunk_size, m.shapes, offs, xs, B)
+        fc = FusedRing(pm.image, pm.jobs, pm.index, pm.chunk_size, m.shapes, offs, xs, B)
         gi.run()
         fc.run()
         torch.cuda.synchronize()

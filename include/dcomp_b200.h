@@ -220,6 +220,19 @@ int dc_w8a8_grouped(const void *maps, const void *layers, const int32_t *units, 
  * set status[chunk] = DC_CHUNK_CHAIN (caller falls back to decode + GEMM).
  * replaces scaling.py:148-151 on weights decoded by ans.py:71-94. */
 int dc_fused_slice_bytes(void);
+
+/* TMEM-ring variant (the fast one): one persistent 17-warp CTA per SM; items
+ * (layer, m0, k0, klen) of dc_fused_item_rows() rows x klen <= dc_fused_item_k()
+ * bytes; 1024 decode chains write 16-byte groups into a 4-deep TMEM ring of
+ * 32-byte K-steps that one MMA warp turns into tcgen05.mma (A from TMEM)
+ * every 32 symbols.  Same layer table, index and status contract as
+ * dc_fused_decode_gemm (multiples of 256 instead of 512). */
+int dc_fused_item_rows(void);
+int dc_fused_item_k(void);
+int dc_fused_ring_gemm(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
+                       const uint64_t *out_len, const uint8_t *codec, uint64_t chunk_size, const int64_t *seg_base,
+                       const uint32_t *seg_state, const uint32_t *seg_off, const void *layers, const int32_t *items,
+                       int64_t n_items, int ntok, int32_t *status, void *stream);
 int dc_fused_decode_gemm(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
                          const uint64_t *out_len, const uint8_t *codec, uint64_t chunk_size, const int64_t *seg_base,
                          const uint32_t *seg_state, const uint32_t *seg_off, const void *layers,

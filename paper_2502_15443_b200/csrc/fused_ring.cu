@@ -1,0 +1,385 @@
+// Fused decompress -> W8A8 GEMM, TMEM-ring version (north-star kernel 3).
+//
+// One persistent CTA per SM: 16 decoder warps + 1 MMA warp.  A work item is
+// (layer, 8 row-tiles = 1024 weight rows, K-slice of up to kFK bytes).  Each
+// decoder thread owns TMEM lane 32*(warp&3)+lane and decodes two rows of
+// that lane (tiles 2*(warp>>2) and 2*(warp>>2)+1) along K, in lockstep with
+// every other chain of the CTA:
+//   * stream bytes come from a private 128-byte ring per chain, refilled 32 B
+//     at a time with cp.async (LDGSTS) ahead of consumption;
+//   * every 16 decoded bytes go registers -> TMEM (tcgen05.st) into a 4-deep
+//     ring of 32-byte K-steps; after each K-step the warp arrives on that
+//     slot's mbarrier;
+//   * the MMA warp waits for all 16 warps, issues one tcgen05.mma.kind::i8
+//     per tile (A from TMEM, X from SW128 smem) and commits to the slot's
+//     "empty" barrier; accumulators live in TMEM (8 tiles x 16 columns).
+// Decoded weights never touch shared memory or HBM.  Each chain is checked
+// at the end of its K-slice against the split-point index (or 2^20 / stream
+// end); a mismatch flags the chunk DC_CHUNK_CHAIN for an exact fallback.
+#include "common.cuh"
+#include "rans_common.cuh"
+#include "tc.cuh"
+
+namespace dc {
+
+struct GemmTensorR {  // identical layout to GemmTensor (fused_gemm.cu)
+    const int8_t* x;
+    int32_t* acc;
+    int64_t t_off;
+    int32_t n_rows;
+    int32_t k;
+};
+
+constexpr int kRDec = 16;                     // decoder warps
+constexpr int kRThreads = (kRDec + 1) * 32;   // + MMA warp
+constexpr int kRTiles = 8;                    // row-tiles per item (1024 rows)
+constexpr int kFK = 2048;                     // max K bytes per item
+constexpr int kRSlots = 4;                    // TMEM ring depth (32-byte K-steps)
+constexpr int kRRing = 128;                   // stream ring bytes per chain
+constexpr int kRNT = 16;                      // tokens (UMMA N)
+constexpr uint32_t kRAcc = 256;               // accumulator columns [256, 384)
+
+struct RingSmem {
+    TableSmem tab[2];
+    alignas(1024) uint8_t x[kFK / 128][kRNT * 128];      // X slice: SW128 atoms of 16 rows x 128 B
+    alignas(128) uint8_t ring[kRDec * 64][kRRing];       // chain (warp, u, lane)
+    uint64_t full[kRSlots];
+    uint64_t empty[kRSlots];
+    uint64_t done;
+    uint32_t tmem;
+    int32_t cur[2];
+};
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&w)[4]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(w[0]), "r"(w[1]),
+                 "r"(w[2]), "r"(w[3])
+                 : "memory");
+}
+
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// One decode step from the chain's stream ring.  `pr` = 32-bit shared address
+// of the next unread byte in a 128-B aligned ring; the increment wraps inside
+// the ring with one LOP3: ((pr + 1) & 127) | (pr & ~127).
+__device__ __forceinline__ uint32_t ring_step(uint32_t& x, uint32_t& pr, uint32_t& nb, uint32_t tab) {
+    uint32_t e;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t, n;\n\t"
+        "and.b32 a, %0, 4095;\n\t"
+        "mad.lo.u32 a, a, 4, %4;\n\t"
+        "ld.shared.u32 %3, [a];\n\t"
+        "shr.u32 f, %3, 20;\n\t"
+        "shr.u32 b, %3, 8;\n\t"
+        "shr.u32 t, %0, 12;\n\t"
+        "sub.u32 t, t, 4096;\n\t"
+        "mad.lo.u32 %0, f, t, b;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q mad.lo.u32 %0, %0, 256, %2;\n\t"
+        "@q add.u32 n, %1, 1;\n\t"
+        "@q lop3.b32 %1, n, %1, 127, 0xE4;\n\t"
+        "@q ld.shared.u8 %2, [%1];\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q mad.lo.u32 %0, %0, 256, %2;\n\t"
+        "@q add.u32 n, %1, 1;\n\t"
+        "@q lop3.b32 %1, n, %1, 127, 0xE4;\n\t"
+        "@q ld.shared.u8 %2, [%1];\n\t}"
+        : "+r"(x), "+r"(pr), "+r"(nb), "=r"(e)
+        : "r"(tab));
+    return e;
+}
+
+struct Chain {
+    uint32_t x, pr, nb, tab;
+    uint64_t gfill;   // next global address to request (16-B aligned)
+    uint32_t xe;      // expected end state
+    uint64_t gend;    // expected end position (global address of the next byte)
+    uint64_t gstart;  // global address of the first byte
+    int mode;         // 0 ANS, 1 stored raw, 2 single symbol, 3 inactive
+    int chunk;
+    uint32_t sym;
+};
+
+// bytes buffered ahead of the read position (ring invariant: < 128)
+__device__ __forceinline__ uint32_t ring_avail(const Chain& c) { return ((uint32_t)c.gfill - c.pr) & 127u; }
+
+__device__ __forceinline__ void ring_refill(Chain& c, uint32_t ring_base) {
+    if (c.mode <= 1 && ring_avail(c) < 96u) {
+        cp_async16(ring_base + ((uint32_t)c.gfill & 127u), reinterpret_cast<const void*>(c.gfill));
+        cp_async16(ring_base + ((uint32_t)(c.gfill + 16) & 127u), reinterpret_cast<const void*>(c.gfill + 16));
+        c.gfill += 32;
+    }
+}
+
+__global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
+    const uint8_t* __restrict__ base, const uint64_t* __restrict__ blob_off, const uint64_t* __restrict__ blob_len,
+    const uint64_t* __restrict__ out_len, const uint8_t* __restrict__ codec, uint64_t chunk_size,
+    const int64_t* __restrict__ seg_base, const uint32_t* __restrict__ seg_state,
+    const uint32_t* __restrict__ seg_off, const GemmTensorR* __restrict__ tens, const int4* __restrict__ items,
+    int n_items, int ntok, int32_t* __restrict__ status) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    RingSmem& S = *reinterpret_cast<RingSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool mma_warp = warp == kRDec;
+    const int q = warp & 3, jj = warp >> 2;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kRSlots; ++s) {
+            mbar_init(&S.full[s], kRDec);
+            mbar_init(&S.empty[s], 1);
+        }
+        mbar_init(&S.done, 1);
+        fence_mbar_init();
+        S.cur[0] = S.cur[1] = -1;
+    }
+    if (warp == 0) tmem_alloc(&S.tmem, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = S.tmem;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);  // this thread's TMEM lane quarter
+    uint32_t gstep = 0, dphase = 0;
+
+    for (int ii = blockIdx.x; ii < n_items; ii += gridDim.x) {
+        const int4 it = items[ii];
+        const GemmTensorR T = tens[it.x];
+        const int m0 = it.y, k0 = it.z, klen = it.w;
+        const int nsteps = klen / 32;
+        const int last_row = min(m0 + kRTiles * 128 - 1, T.n_rows - 1);
+        const int c_lo = (int)(((uint64_t)T.t_off + (uint64_t)m0 * T.k + k0) / chunk_size);
+        const int c_hi = (int)(((uint64_t)T.t_off + (uint64_t)last_row * T.k + k0 + klen - 1) / chunk_size);
+        __syncthreads();  // previous item: epilogue reads and X reads are finished
+        if (c_hi - c_lo > 1) {  // host never builds such items
+            if (threadIdx.x == 0) atomicExch(&status[c_lo], DC_CHUNK_CHAIN);
+            continue;
+        }
+        // ---- decode tables for the (at most two) chunks of this item
+        for (int t = 0; t <= c_hi - c_lo; ++t) {
+            const int ct = c_lo + t;
+            if (S.cur[t] != ct) {
+                __syncthreads();
+                if (codec[ct] == 1) build_decode_table(base + blob_off[ct], S.tab[t]);
+                __syncthreads();
+                if (threadIdx.x == 0) S.cur[t] = ct;
+            }
+        }
+
+        if (mma_warp) {
+            // ---- X slice -> SW128 atoms (generic stores, then proxy fence)
+            const int chunks16 = kRNT * (klen >> 4);
+            for (int i = lane; i < chunks16; i += 32) {
+                const int r = i % kRNT, cj = i / kRNT, s = cj >> 3, j = cj & 7;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (r < ntok) v = *reinterpret_cast<const uint4*>(T.x + (int64_t)r * T.k + k0 + (cj << 4));
+                *reinterpret_cast<uint4*>(&S.x[s][r * 128 + ((j ^ (r & 7)) << 4)]) = v;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            __syncthreads();  // pairs with the decoders' setup barrier
+            if (lane == 0) {
+                constexpr uint32_t idesc = idesc_i8(128, kRNT);
+                for (int st = 0; st < nsteps; ++st) {
+                    const uint32_t g = gstep + st, s = g % kRSlots, ph = (g / kRSlots) & 1;
+                    mbar_wait(&S.full[s], ph);
+                    tc_fence_after();
+                    const int kk = st * 32;
+                    const uint64_t bdesc = sw128_kmajor_desc(smem_u32(S.x[kk >> 7]) + (kk & 127));
+#pragma unroll
+                    for (int t = 0; t < kRTiles; ++t)
+                        mma_ts(tmem + kRAcc + t * kRNT, tmem + s * 64 + t * 8, bdesc, idesc, st > 0);
+                    mma_commit(&S.empty[s]);
+                }
+                mma_commit(&S.done);
+            }
+            __syncwarp();
+            gstep += nsteps;
+            mbar_wait(&S.done, dphase);
+            dphase ^= 1u;
+            continue;
+        }
+
+        // ---- decoder chains: u = 0, 1 -> tiles 2*jj, 2*jj+1
+        Chain ch[2];
+        uint32_t ring_base[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            Chain& c = ch[u];
+            const int t = 2 * jj + u;
+            const int row = m0 + t * 128 + q * 32 + lane;
+            const bool valid = row < T.n_rows;
+            const uint64_t g = (uint64_t)T.t_off + (uint64_t)(valid ? row : m0) * T.k + k0;
+            c.chunk = (int)(g / chunk_size);
+            const uint32_t o = (uint32_t)(g - (uint64_t)c.chunk * chunk_size);
+            const uint8_t* blob = base + blob_off[c.chunk];
+            const TableSmem& TB = S.tab[c.chunk - c_lo];
+            c.tab = smem_u32(TB.tab);
+            ring_base[u] = smem_u32(S.ring[(warp * 2 + u) * 32 + lane]);
+            c.x = kStateLower;
+            c.xe = kStateLower;
+            c.sym = 0;
+            if (!valid) {
+                c.mode = 3;
+                c.gstart = c.gend = reinterpret_cast<uint64_t>(blob);
+            } else if (codec[c.chunk] != 1) {
+                c.mode = 1;
+                c.gstart = reinterpret_cast<uint64_t>(blob) + o;
+                c.gend = c.gstart + klen;
+            } else {
+                const uint64_t nseg = (out_len[c.chunk] + 255) / 256;
+                const int64_t j = seg_base[c.chunk] + (o >> 8);
+                const int64_t je = j + (klen >> 8);
+                const uint64_t sbase = reinterpret_cast<uint64_t>(blob) + kHeaderBytes;
+                c.x = seg_state[j];
+                c.gstart = sbase + seg_off[j];
+                const bool tail = (uint64_t)(o >> 8) + (klen >> 8) >= nseg;
+                c.xe = tail ? kStateLower : seg_state[je];
+                c.gend = sbase + (tail ? (uint64_t)(blob_len[c.chunk] - kHeaderBytes) : (uint64_t)seg_off[je]);
+                c.mode = TB.single >= 0 ? 2 : 0;
+                c.sym = TB.single >= 0 ? (uint32_t)TB.single : 0u;
+            }
+            c.gfill = c.gstart & ~(uint64_t)15;
+            c.pr = ring_base[u] + ((uint32_t)c.gstart & 127u);
+            if (c.mode <= 1) {  // prime the ring with 128 B
+                for (int k = 0; k < 8; ++k) {
+                    cp_async16(ring_base[u] + ((uint32_t)c.gfill & 127u), reinterpret_cast<const void*>(c.gfill));
+                    c.gfill += 16;
+                }
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        ch[0].nb = lds_u8(ch[0].pr);
+        ch[1].nb = lds_u8(ch[1].pr);
+        __syncthreads();  // tables visible; X staged by the MMA warp
+        const bool fast = __all_sync(0xffffffffu, ch[0].mode == 0 && ch[1].mode == 0);
+
+        for (int st = 0; st < nsteps; ++st) {
+            const uint32_t g = gstep + st, s = g % kRSlots, ph = (g / kRSlots) & 1;
+            mbar_wait(&S.empty[s], ph ^ 1u);  // MMAs of 4 steps ago have consumed slot s
+            tc_fence_after();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t w[2][4];
+                if (fast) {
+#pragma unroll
+                    for (int v = 0; v < 16; ++v) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+                            w[u][v >> 2] = put_byte(w[u][v >> 2], ring_step(ch[u].x, ch[u].pr, ch[u].nb, ch[u].tab),
+                                                    v & 3);
+                    }
+                } else {
+#pragma unroll 1
+                    for (int v = 0; v < 16; ++v) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            Chain& c = ch[u];
+                            uint32_t e;
+                            if (c.mode == 0) {
+                                e = ring_step(c.x, c.pr, c.nb, c.tab);
+                            } else if (c.mode == 1) {
+                                e = c.nb;
+                                c.pr = ((c.pr + 1) & 127u) | (c.pr & ~127u);
+                                c.nb = lds_u8(c.pr);
+                            } else {
+                                e = c.sym;
+                            }
+                            w[u][v >> 2] = put_byte(w[u][v >> 2], e, v & 3);
+                        }
+                    }
+                }
+                const uint32_t col = s * 64 + h * 4;
+                tmem_st4(tl + col + (2 * jj) * 8, w[0]);
+                tmem_st4(tl + col + (2 * jj + 1) * 8, w[1]);
+                ring_refill(ch[0], ring_base[0]);
+                ring_refill(ch[1], ring_base[1]);
+                cp_async_commit();
+                cp_async_wait<1>();
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.full[s]);
+        }
+        gstep += nsteps;
+
+        // ---- chain checks (state and position must meet the next split point)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const Chain& c = ch[u];
+            if (c.mode == 0) {
+                const uint64_t pos = c.gfill - (uint64_t)(((uint32_t)c.gfill - c.pr) & 127u);
+                if (c.x != c.xe || pos != c.gend) atomicExch(&status[c.chunk], DC_CHUNK_CHAIN);
+            } else if (c.mode == 2 && (c.x != c.xe || c.gstart != c.gend)) {
+                atomicExch(&status[c.chunk], DC_CHUNK_CORRUPT);
+            }
+        }
+
+        // ---- epilogue: accumulators of tiles 2*jj, 2*jj+1 for this lane quarter
+        mbar_wait(&S.done, dphase);
+        dphase ^= 1u;
+        tc_fence_after();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            uint32_t acc[16];
+            tmem_ld_32x32b_x16(tl + kRAcc + (2 * jj + u) * kRNT, acc);
+            const int row = m0 + (2 * jj + u) * 128 + q * 32 + lane;
+            if (row < T.n_rows) {
+#pragma unroll
+                for (int t = 0; t < kRNT; ++t)
+                    if (t < ntok) atomicAdd(&T.acc[(int64_t)t * T.n_rows + row], (int32_t)acc[t]);
+            }
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+}  // namespace dc
+
+using namespace dc;
+
+extern "C" int dc_fused_item_rows(void) { return kRTiles * 128; }
+extern "C" int dc_fused_item_k(void) { return kFK; }
+
+// items: int4 (layer, m0, k0, klen): 1024 rows from m0, K-slice [k0, k0+klen),
+// klen a multiple of 256 and <= dc_fused_item_k(); index seg_shift 8;
+// chunk_size and layer offsets multiples of 256; an item's rows span <= 2 chunks.
+extern "C" int dc_fused_ring_gemm(const uint8_t* base, const uint64_t* blob_off, const uint64_t* blob_len,
+                                  const uint64_t* out_len, const uint8_t* codec, uint64_t chunk_size,
+                                  const int64_t* seg_base, const uint32_t* seg_state, const uint32_t* seg_off,
+                                  const void* tens, const int32_t* items, int64_t n_items, int ntok,
+                                  int32_t* status, void* stream) {
+    if (n_items <= 0 || ntok <= 0 || ntok > kRNT || chunk_size % 256) return DC_ERR_ARG;
+    const size_t smem = sizeof(RingSmem) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_fused_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = n_items < sms ? n_items : sms;
+    k_fused_ring<<<(unsigned)grid, kRThreads, smem, (cudaStream_t)stream>>>(
+        base, blob_off, blob_len, out_len, codec, chunk_size, seg_base, seg_state, seg_off,
+        reinterpret_cast<const GemmTensorR*>(tens), reinterpret_cast<const int4*>(items), (int)n_items, ntok, status);
+    DC_CHECK_LAUNCH("k_fused_ring");
+    return DC_OK;
+}

@@ -36,7 +36,7 @@ def _dev():
 
 
 def _t(a: np.ndarray, dtype, device) -> torch.Tensor:
-    return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dtype)
+    return torch.from_numpy(np.array(a, copy=True)).to(device=device, dtype=dtype)
 
 
 @dataclasses.dataclass
@@ -58,7 +58,9 @@ class JobTable:
     @classmethod
     def build(cls, blob_off, blob_len, out_off, out_len, codec, device=None) -> "JobTable":
         dev = device or _dev()
-        arrs = [np.ascontiguousarray(a, dtype=np.uint64) for a in (blob_off, blob_len, out_off, out_len)]
+        # np.array copies: a 1-element strided field view counts as "contiguous"
+        # for numpy but keeps its 29-byte stride, which torch rejects
+        arrs = [np.array(a, dtype=np.uint64) for a in (blob_off, blob_len, out_off, out_len)]
         cod = np.ascontiguousarray(codec, dtype=np.uint8)
         d = [_t(a.view(np.int64), torch.int64, dev) for a in arrs]
         return cls(len(cod), *arrs, cod, *d, _t(cod, torch.uint8, dev))

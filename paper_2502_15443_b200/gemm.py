@@ -179,3 +179,42 @@ class FusedCompressed:
     def check(self) -> np.ndarray:
         """Per-chunk status after run(); nonzero = chain broken / corrupt."""
         return self.status[: self.jobs.n].cpu().numpy()
+
+
+class FusedRing(FusedCompressed):
+    """Fused decode -> TMEM ring -> tcgen05 W8A8 (csrc/fused_ring.cu): one
+    persistent 17-warp CTA per SM, 1024 decode chains feeding the tensor core
+    every 32 symbols.  Items: 1024 rows x K-slice (<= 2048 bytes)."""
+
+    def __init__(self, image: torch.Tensor, jobs, index, chunk_size: int, shapes, t_offs, xs, ntok: int):
+        if index is None or index.seg_shift != 8:
+            raise ValueError("fused path needs a split-point index with 256-symbol segments")
+        rows_per = nv.call("dc_fused_item_rows")
+        kmax = nv.call("dc_fused_item_k")
+        if chunk_size % 256 or any(int(t) % 256 for t in t_offs) or any(k % 256 for _, k in shapes):
+            raise ValueError("fused path needs chunk_size, tensor offsets and K multiples of 256")
+        for (r, k), t in zip(shapes, t_offs):
+            if (rows_per - 1) * k + kmax > chunk_size:
+                raise ValueError("chunk too small for the fused path (1024 rows x K must fit in one chunk)")
+        self.image, self.jobs, self.index, self.chunk_size = image, jobs, index, chunk_size
+        self.layers = _LayerSet(shapes, t_offs, xs, ntok)
+        items = []
+        for li, (r, k) in enumerate(self.layers.shapes):
+            # a chain's K-slice must never straddle a chunk boundary: use the
+            # largest power of two <= kmax dividing K, the layer offset and the chunk size
+            ks = kmax
+            while ks > 256 and (k % ks or int(t_offs[li]) % ks or chunk_size % ks):
+                ks //= 2
+            for m0 in range(0, r, rows_per):
+                for k0 in range(0, k, ks):
+                    items.append((li, m0, k0, min(ks, k - k0)))
+        self.unit_t = torch.tensor(items, dtype=torch.int32, device=image.device)
+        self.status = torch.zeros(max(jobs.n, 1), dtype=torch.int32, device=image.device)
+
+    def run(self) -> None:
+        self.layers.acc_flat.zero_()
+        j, ix = self.jobs, self.index
+        nv.call("dc_fused_ring_gemm", self.image.data_ptr(), j.d_blob_off.data_ptr(), j.d_blob_len.data_ptr(),
+                j.d_out_len.data_ptr(), j.d_codec.data_ptr(), self.chunk_size, ix.d_seg_base.data_ptr(),
+                ix.d_state.data_ptr(), ix.d_off.data_ptr(), self.layers.tens.data_ptr(), self.unit_t.data_ptr(),
+                self.unit_t.shape[0], self.layers.ntok, self.status.data_ptr(), nv.stream_ptr())

@@ -70,6 +70,9 @@ SIGNATURES: dict[str, list] = {
     "dc_w8a8_grouped": [_P, _P, _P, _I64, ctypes.c_int, _P],
     "dc_fused_slice_bytes": [],
     "dc_fused_decode_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P],
+    "dc_fused_item_rows": [],
+    "dc_fused_item_k": [],
+    "dc_fused_ring_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P],
 }
 _RESTYPES = {"dc_last_error": ctypes.c_char_p}
 

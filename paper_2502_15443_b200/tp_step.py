@@ -15,7 +15,7 @@ import torch
 import torch.distributed as dist
 
 from . import container, synth
-from .gemm import FusedCompressed, GroupedInt8
+from .gemm import FusedRing, GroupedInt8
 from .parallel import tp_layout
 
 
@@ -38,7 +38,7 @@ class TPDecodeStep:
                    for _, c in m.shapes]
         w_views = [m.payload[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, m.shapes)]
         self.int8 = GroupedInt8(w_views, self.xs, ntok)
-        self.fused = FusedCompressed(image, self.jobs, enc.index, chunk_size, m.shapes, offs, self.xs, ntok)
+        self.fused = FusedRing(image, self.jobs, enc.index, chunk_size, m.shapes, offs, self.xs, ntok)
         self.row_idx = [i for i, s in enumerate(self.shards) if s.kind == "row"]
         self.raw_bytes = m.nbytes
         self.comp_bytes = int(entries["comp_len"].sum())

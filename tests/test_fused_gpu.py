@@ -61,3 +61,32 @@ def test_fused_decode_gemm_exact(cuda, ntok, stored):
     fc.run()
     torch.cuda.synchronize()
     assert (fc.check() != 0).any()
+
+
+@pytest.mark.parametrize("ntok,stored,chunk", [(1, False, 1 << 22), (5, True, 1 << 22), (16, False, 1 << 24)])
+def test_fused_ring_exact(cuda, ntok, stored, chunk):
+    from paper_2502_15443_b200 import container
+    from paper_2502_15443_b200.gemm import FusedRing
+    g = torch.Generator().manual_seed(ntok)
+    shapes = [(1024, 2048), (1500, 512), (300, 4096), (2048, 1280)]
+    ws = []
+    for r, k in shapes:
+        w = torch.round(torch.randn(r, k, generator=g) * 9).clamp_(-127, 127).to(torch.int8)
+        w[:, :33] = 0
+        ws.append(w)
+    xs = [torch.randint(-127, 128, (ntok, k), generator=g, dtype=torch.int8) for _, k in shapes]
+    payload = torch.cat([w.reshape(-1).view(torch.uint8) for w in ws]).cuda()
+    t_offs = np.concatenate([[0], np.cumsum([w.numel() for w in ws])[:-1]])
+    n = -(-payload.numel() // chunk)
+    plan = np.array([i % 2 == 0 for i in range(n)]) if stored else None
+    image, enc, entries = container.pack_device(payload, b"\x00" * 8, chunk, plan, seg_shift=8)
+    jobs = container.jobs_for(entries, image.device)
+    fr = FusedRing(image, jobs, enc.index, chunk, shapes, t_offs, [x.cuda() for x in xs], ntok)
+    fr.run()
+    torch.cuda.synchronize()
+    assert (fr.check() == 0).all()
+    for w, x, acc in zip(ws, xs, fr.accs):
+        assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
+    fr.run()  # re-run (ring / barrier phases carry over between launches)
+    torch.cuda.synchronize()
+    assert all(torch.equal(acc.cpu().long(), x.long() @ w.long().T) for w, x, acc in zip(ws, xs, fr.accs))

@@ -18,7 +18,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2502_15443_b200 import adaptive, container, synth  # noqa: E402
-from paper_2502_15443_b200.gemm import FusedCompressed, GroupedInt8  # noqa: E402
+from paper_2502_15443_b200.gemm import FusedRing, GroupedInt8  # noqa: E402
 from paper_2502_15443_b200.latency import CompressionPlan  # noqa: E402
 
 
@@ -75,7 +75,7 @@ def cmd_partial(a):
             header = b"\0" * 8
             image, enc, entries = container.pack_device(sub, header, cs, None, seg_shift=8)
             jobs = container.jobs_for(entries, image.device)
-            fc = FusedCompressed(image, jobs, enc.index, cs, [m.shapes[i] for i in comp_idx], sub_offs,
+            fc = FusedRing(image, jobs, enc.index, cs, [m.shapes[i] for i in comp_idx], sub_offs,
                                  [xs[i] for i in comp_idx], B)
             fns.append(fc.run)
             checks.append(fc)
