@@ -1,21 +1,24 @@
 // Fused decompress -> W8A8 GEMM, TMEM-ring version (north-star kernel 3).
 //
-// One persistent CTA per SM: 16 decoder warps + 1 MMA warp.  A work item is
+// One persistent CTA per SM of 16 decoder warps (512 threads: 4 warps per SM
+// sub-partition, so 128 registers per thread and no spills).  A work item is
 // (layer, 8 row-tiles = 1024 weight rows, K-slice of up to kFK bytes).  Each
-// decoder thread owns TMEM lane 32*(warp&3)+lane and decodes two rows of
-// that lane (tiles 2*(warp>>2) and 2*(warp>>2)+1) along K, in lockstep with
-// every other chain of the CTA:
+// thread owns TMEM lane 32*(warp&3)+lane and decodes two rows of that lane
+// (tiles 2*(warp>>2) and 2*(warp>>2)+1) along K, in lockstep with every other
+// chain of the CTA:
 //   * stream bytes come from a private 128-byte ring per chain, refilled 32 B
 //     at a time with cp.async (LDGSTS) ahead of consumption;
-//   * every 16 decoded bytes go registers -> TMEM (tcgen05.st) into a 4-deep
-//     ring of 32-byte K-steps; after each K-step the warp arrives on that
-//     slot's mbarrier;
-//   * the MMA warp waits for all 16 warps, issues one tcgen05.mma.kind::i8
-//     per tile (A from TMEM, X from SW128 smem) and commits to the slot's
-//     "empty" barrier; accumulators live in TMEM (8 tiles x 16 columns).
-// Decoded weights never touch shared memory or HBM.  Each chain is checked
-// at the end of its K-slice against the split-point index (or 2^20 / stream
-// end); a mismatch flags the chunk DC_CHUNK_CHAIN for an exact fallback.
+//   * every 16 decoded bytes go registers -> TMEM (tcgen05.st) into a ring of
+//     kRSlots 32-byte K-steps;
+//   * after each K-step every warp bumps the slot's arrival counter (shared
+//     atomic, acq_rel); the LAST warp to arrive issues one
+//     tcgen05.mma.kind::i8 per tile (A from TMEM, X from SW128 smem) and
+//     commits to the slot's "empty" mbarrier.  No dedicated MMA warp: the
+//     issue cost lands on whichever warp completes the step.
+// Accumulators live in TMEM (8 tiles x 16 columns).  Decoded weights never
+// touch shared memory or HBM.  Each chain is checked at the end of its
+// K-slice against the split-point index (or 2^20 / stream end); a mismatch
+// flags the chunk DC_CHUNK_CHAIN for an exact fallback.
 #include "common.cuh"
 #include "rans_common.cuh"
 #include "tc.cuh"
@@ -31,21 +34,22 @@ struct GemmTensorR {  // identical layout to GemmTensor (fused_gemm.cu)
 };
 
 constexpr int kRDec = 16;                     // decoder warps
-constexpr int kRThreads = (kRDec + 1) * 32;   // + MMA warp
+constexpr int kRThreads = kRDec * 32;
 constexpr int kRTiles = 8;                    // row-tiles per item (1024 rows)
 constexpr int kFK = 2048;                     // max K bytes per item
-constexpr int kRSlots = 4;                    // TMEM ring depth (32-byte K-steps)
+constexpr int kRSlots = 6;                    // TMEM ring depth (32-byte K-steps)
 constexpr int kRRing = 128;                   // stream ring bytes per chain
 constexpr int kRNT = 16;                      // tokens (UMMA N)
-constexpr uint32_t kRAcc = 256;               // accumulator columns [256, 384)
+constexpr uint32_t kRAcc = kRSlots * 64;      // accumulator columns [kRAcc, kRAcc + 128)
+static_assert(kRAcc + kRTiles * kRNT <= 512, "TMEM columns");
 
 struct RingSmem {
     TableSmem tab[2];
     alignas(1024) uint8_t x[kFK / 128][kRNT * 128];      // X slice: SW128 atoms of 16 rows x 128 B
     alignas(128) uint8_t ring[kRDec * 64][kRRing];       // chain (warp, u, lane)
-    uint64_t full[kRSlots];
     uint64_t empty[kRSlots];
     uint64_t done;
+    uint32_t cnt[kRSlots];
     uint32_t tmem;
     int32_t cur[2];
 };
@@ -64,6 +68,12 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
         "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
+}
+
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+    return old;
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
@@ -127,6 +137,18 @@ __device__ __forceinline__ void ring_refill(Chain& c, uint32_t ring_base) {
     }
 }
 
+// Generic (mixed-mode) step: returns the next weight byte of chain c.
+__device__ __forceinline__ uint32_t chain_step(Chain& c) {
+    if (c.mode == 0) return ring_step(c.x, c.pr, c.nb, c.tab);
+    if (c.mode == 1) {
+        const uint32_t e = c.nb;
+        c.pr = ((c.pr + 1) & 127u) | (c.pr & ~127u);
+        c.nb = lds_u8(c.pr);
+        return e;
+    }
+    return c.sym;
+}
+
 __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
     const uint8_t* __restrict__ base, const uint64_t* __restrict__ blob_off, const uint64_t* __restrict__ blob_len,
     const uint64_t* __restrict__ out_len, const uint8_t* __restrict__ codec, uint64_t chunk_size,
@@ -136,12 +158,11 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     RingSmem& S = *reinterpret_cast<RingSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool mma_warp = warp == kRDec;
     const int q = warp & 3, jj = warp >> 2;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kRSlots; ++s) {
-            mbar_init(&S.full[s], kRDec);
             mbar_init(&S.empty[s], 1);
+            S.cnt[s] = 0;
         }
         mbar_init(&S.done, 1);
         fence_mbar_init();
@@ -153,7 +174,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
     tc_fence_after();
     const uint32_t tmem = S.tmem;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);  // this thread's TMEM lane quarter
-    uint32_t gstep = 0, dphase = 0;
+    uint32_t slot = 0, sphase = 0, dphase = 0;               // ring position of the next K-step
 
     for (int ii = blockIdx.x; ii < n_items; ii += gridDim.x) {
         const int4 it = items[ii];
@@ -178,39 +199,16 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
                 if (threadIdx.x == 0) S.cur[t] = ct;
             }
         }
-
-        if (mma_warp) {
-            // ---- X slice -> SW128 atoms (generic stores, then proxy fence)
+        // ---- X slice -> SW128 atoms (generic stores, then proxy fence)
+        {
             const int chunks16 = kRNT * (klen >> 4);
-            for (int i = lane; i < chunks16; i += 32) {
+            for (int i = threadIdx.x; i < chunks16; i += kRThreads) {
                 const int r = i % kRNT, cj = i / kRNT, s = cj >> 3, j = cj & 7;
                 uint4 v = make_uint4(0, 0, 0, 0);
                 if (r < ntok) v = *reinterpret_cast<const uint4*>(T.x + (int64_t)r * T.k + k0 + (cj << 4));
                 *reinterpret_cast<uint4*>(&S.x[s][r * 128 + ((j ^ (r & 7)) << 4)]) = v;
             }
             fence_proxy_async_smem();
-            __syncwarp();
-            __syncthreads();  // pairs with the decoders' setup barrier
-            if (lane == 0) {
-                constexpr uint32_t idesc = idesc_i8(128, kRNT);
-                for (int st = 0; st < nsteps; ++st) {
-                    const uint32_t g = gstep + st, s = g % kRSlots, ph = (g / kRSlots) & 1;
-                    mbar_wait(&S.full[s], ph);
-                    tc_fence_after();
-                    const int kk = st * 32;
-                    const uint64_t bdesc = sw128_kmajor_desc(smem_u32(S.x[kk >> 7]) + (kk & 127));
-#pragma unroll
-                    for (int t = 0; t < kRTiles; ++t)
-                        mma_ts(tmem + kRAcc + t * kRNT, tmem + s * 64 + t * 8, bdesc, idesc, st > 0);
-                    mma_commit(&S.empty[s]);
-                }
-                mma_commit(&S.done);
-            }
-            __syncwarp();
-            gstep += nsteps;
-            mbar_wait(&S.done, dphase);
-            dphase ^= 1u;
-            continue;
         }
 
         // ---- decoder chains: u = 0, 1 -> tiles 2*jj, 2*jj+1
@@ -265,12 +263,11 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
         cp_async_wait<0>();
         ch[0].nb = lds_u8(ch[0].pr);
         ch[1].nb = lds_u8(ch[1].pr);
-        __syncthreads();  // tables visible; X staged by the MMA warp
+        __syncthreads();  // tables and X slice visible (generic and async proxies)
         const bool fast = __all_sync(0xffffffffu, ch[0].mode == 0 && ch[1].mode == 0);
 
         for (int st = 0; st < nsteps; ++st) {
-            const uint32_t g = gstep + st, s = g % kRSlots, ph = (g / kRSlots) & 1;
-            mbar_wait(&S.empty[s], ph ^ 1u);  // MMAs of 4 steps ago have consumed slot s
+            mbar_wait(&S.empty[slot], sphase ^ 1u);  // MMAs of kRSlots steps ago have consumed this slot
             tc_fence_after();
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -283,27 +280,20 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
                             w[u][v >> 2] = put_byte(w[u][v >> 2], ring_step(ch[u].x, ch[u].pr, ch[u].nb, ch[u].tab),
                                                     v & 3);
                     }
-                } else {
+                } else {  // bytes shift in from the top: no runtime index into w[]
 #pragma unroll 1
                     for (int v = 0; v < 16; ++v) {
 #pragma unroll
                         for (int u = 0; u < 2; ++u) {
-                            Chain& c = ch[u];
-                            uint32_t e;
-                            if (c.mode == 0) {
-                                e = ring_step(c.x, c.pr, c.nb, c.tab);
-                            } else if (c.mode == 1) {
-                                e = c.nb;
-                                c.pr = ((c.pr + 1) & 127u) | (c.pr & ~127u);
-                                c.nb = lds_u8(c.pr);
-                            } else {
-                                e = c.sym;
-                            }
-                            w[u][v >> 2] = put_byte(w[u][v >> 2], e, v & 3);
+                            const uint32_t e = chain_step(ch[u]);
+                            w[u][0] = __funnelshift_r(w[u][0], w[u][1], 8);
+                            w[u][1] = __funnelshift_r(w[u][1], w[u][2], 8);
+                            w[u][2] = __funnelshift_r(w[u][2], w[u][3], 8);
+                            w[u][3] = __funnelshift_r(w[u][3], e, 8);
                         }
                     }
                 }
-                const uint32_t col = s * 64 + h * 4;
+                const uint32_t col = slot * 64 + h * 4;
                 tmem_st4(tl + col + (2 * jj) * 8, w[0]);
                 tmem_st4(tl + col + (2 * jj + 1) * 8, w[1]);
                 ring_refill(ch[0], ring_base[0]);
@@ -314,9 +304,25 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&S.full[s]);
+            if (lane == 0 && atom_add_acq_rel(&S.cnt[slot], 1u) == kRDec - 1) {
+                // last warp of this K-step: every slice of the slot is in TMEM
+                S.cnt[slot] = 0;
+                tc_fence_after();
+                constexpr uint32_t idesc = idesc_i8(128, kRNT);
+                const int kk = st * 32;
+                const uint64_t bdesc = sw128_kmajor_desc(smem_u32(S.x[kk >> 7]) + (kk & 127));
+#pragma unroll
+                for (int t = 0; t < kRTiles; ++t)
+                    mma_ts(tmem + kRAcc + t * kRNT, tmem + slot * 64 + t * 8, bdesc, idesc, st > 0);
+                mma_commit(&S.empty[slot]);
+                if (st == nsteps - 1) mma_commit(&S.done);
+            }
+            __syncwarp();
+            if (++slot == kRSlots) {
+                slot = 0;
+                sphase ^= 1u;
+            }
         }
-        gstep += nsteps;
 
         // ---- chain checks (state and position must meet the next split point)
 #pragma unroll

@@ -10,14 +10,15 @@ import torch  # noqa: E402
 from paper_2502_15443_b200 import synth  # noqa: E402
 from paper_2502_15443_b200.gemm import FusedRing  # noqa: E402
 
-layers = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-m = synth.build_model("opt-1.3b", layers=layers)
+layers = int(sys.argv[1]) if len(sys.argv) > 1 else 4  # 0 = every layer
+model = sys.argv[2] if len(sys.argv) > 2 else "opt-1.3b"
+m = synth.build_model(model, layers=layers or None)
 pm = synth.pack_model(m, 16 << 20, seg_shift=8)
 g = torch.Generator(device="cuda")
 g.manual_seed(1)
 xs = [torch.randint(-127, 128, (1, c), generator=g, device="cuda", dtype=torch.int8) for _, c in m.shapes]
 fr = FusedRing(pm.image, pm.jobs, pm.index, pm.chunk_size, m.shapes, m.offsets()[:-1], xs, 1)
-for i in range(3):
+for i in range(int(os.environ.get("ITERS", 3))):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     fr.run()
