@@ -419,8 +419,9 @@ def unpack(data, index=None) -> ModelBundle:
     import time
     clock = [time.perf_counter()]
 
-    def lap(name):
-        torch.cuda.synchronize()
+    def lap(name):  # host-side phase times; DCOMP_PHASE_SYNC=1 serializes them against the GPU
+        if _PHASE_SYNC:
+            torch.cuda.synchronize()
         now = time.perf_counter()
         LAST_UNPACK_MS[name] = (now - clock[0]) * 1e3
         clock[0] = now
@@ -433,8 +434,8 @@ def unpack(data, index=None) -> ModelBundle:
     lap("parse")
     if index is not None:  # split-point path: H2D / decode / D2H pipelined per chunk group
         jobs = jobs_for(ent)
-        if isinstance(index, (bytes, bytearray)):
-            index = engine.SegmentIndex.from_bytes(bytes(index), jobs, binding_of(data))
+        if isinstance(index, (bytes, bytearray, memoryview)):
+            index = engine.SegmentIndex.from_bytes(index, jobs, binding_of(data))
         lap("index")
         if index is not None:
             host, status, crc = engine.decode_file_pipelined(np.frombuffer(data, np.uint8), jobs, index)
@@ -458,6 +459,7 @@ def unpack(data, index=None) -> ModelBundle:
 
 
 LAST_UNPACK_MS: dict[str, float] = {}  # phase timings of the last unpack() (diagnostics)
+_PHASE_SYNC = os.environ.get("DCOMP_PHASE_SYNC") == "1"
 
 
 def read_container(path) -> ModelBundle:

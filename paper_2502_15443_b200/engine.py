@@ -130,7 +130,6 @@ class SegmentIndex:
         if ver != 1 or bind != binding or not 6 <= shift <= 10:
             return None
         base, want = cls.layout(jobs.out_len, jobs.codec, shift)
-        body = buf[22:22 + 8 * n]
         # The body CRC is written but not re-verified here: a damaged index can
         # only slow decoding down (chain checks send the chunk to the exact path).
         if n != want or len(buf) != 22 + 8 * n + 4:
@@ -368,7 +367,7 @@ def _streams(dev):
     return _SIDE_STREAMS[dev]
 
 
-def decode_file_pipelined(data: np.ndarray, jobs: JobTable, index: SegmentIndex, groups: int = 8):
+def decode_file_pipelined(data: np.ndarray, jobs: JobTable, index: SegmentIndex, groups: int = 16):
     """Host container bytes -> host decoded bytes with H2D of chunk group g+1,
     decode + CRC of group g and D2H of group g-1 overlapped on three streams.
 
