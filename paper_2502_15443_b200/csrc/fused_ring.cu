@@ -85,13 +85,14 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// One decode step from the chain's stream ring.  `pr` = 32-bit shared address
-// of the next unread byte in a 128-B aligned ring; the increment wraps inside
-// the ring with one LOP3: ((pr + 1) & 127) | (pr & ~127).
-__device__ __forceinline__ uint32_t ring_step(uint32_t& x, uint32_t& pr, uint32_t& nb, uint32_t tab) {
+// One decode step from the chain's stream ring.  `pr` is a free-running
+// byte counter whose low 7 bits are the ring offset of the next unread byte;
+// the shared address of a byte is (pr & 127) | rb (one LOP3, rb = the
+// 128-B aligned ring base), so the counter itself never wraps.
+__device__ __forceinline__ uint32_t ring_step(uint32_t& x, uint32_t& pr, uint32_t& nb, uint32_t tab, uint32_t rb) {
     uint32_t e;
     asm volatile(
-        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t, n;\n\t"
+        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t, a1, a2;\n\t"
         "and.b32 a, %0, 4095;\n\t"
         "mad.lo.u32 a, a, 4, %4;\n\t"
         "ld.shared.u32 %3, [a];\n\t"
@@ -102,21 +103,21 @@ __device__ __forceinline__ uint32_t ring_step(uint32_t& x, uint32_t& pr, uint32_
         "mad.lo.u32 %0, f, t, b;\n\t"
         "setp.lt.u32 q, %0, 0x100000;\n\t"
         "@q mad.lo.u32 %0, %0, 256, %2;\n\t"
-        "@q add.u32 n, %1, 1;\n\t"
-        "@q lop3.b32 %1, n, %1, 127, 0xE4;\n\t"
-        "@q ld.shared.u8 %2, [%1];\n\t"
+        "@q add.u32 %1, %1, 1;\n\t"
+        "lop3.b32 a1, %1, 127, %5, 0xEA;\n\t"
+        "@q ld.shared.u8 %2, [a1];\n\t"
         "setp.lt.u32 q, %0, 0x100000;\n\t"
         "@q mad.lo.u32 %0, %0, 256, %2;\n\t"
-        "@q add.u32 n, %1, 1;\n\t"
-        "@q lop3.b32 %1, n, %1, 127, 0xE4;\n\t"
-        "@q ld.shared.u8 %2, [%1];\n\t}"
+        "@q add.u32 %1, %1, 1;\n\t"
+        "lop3.b32 a2, %1, 127, %5, 0xEA;\n\t"
+        "@q ld.shared.u8 %2, [a2];\n\t}"
         : "+r"(x), "+r"(pr), "+r"(nb), "=r"(e)
-        : "r"(tab));
+        : "r"(tab), "r"(rb));
     return e;
 }
 
 struct Chain {
-    uint32_t x, pr, nb, tab;
+    uint32_t x, pr, nb, tab, rb;  // pr: free-running ring counter, rb: ring base
     uint64_t gfill;   // next global address to request (16-B aligned)
     uint32_t xe;      // expected end state
     uint64_t gend;    // expected end position (global address of the next byte)
@@ -139,11 +140,11 @@ __device__ __forceinline__ void ring_refill(Chain& c, uint32_t ring_base) {
 
 // Generic (mixed-mode) step: returns the next weight byte of chain c.
 __device__ __forceinline__ uint32_t chain_step(Chain& c) {
-    if (c.mode == 0) return ring_step(c.x, c.pr, c.nb, c.tab);
+    if (c.mode == 0) return ring_step(c.x, c.pr, c.nb, c.tab, c.rb);
     if (c.mode == 1) {
         const uint32_t e = c.nb;
-        c.pr = ((c.pr + 1) & 127u) | (c.pr & ~127u);
-        c.nb = lds_u8(c.pr);
+        ++c.pr;
+        c.nb = lds_u8((c.pr & 127u) | c.rb);
         return e;
     }
     return c.sym;
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
                 c.sym = TB.single >= 0 ? (uint32_t)TB.single : 0u;
             }
             c.gfill = c.gstart & ~(uint64_t)15;
+            c.rb = ring_base[u];
             c.pr = ring_base[u] + ((uint32_t)c.gstart & 127u);
             if (c.mode <= 1) {  // prime the ring with 128 B
                 for (int k = 0; k < 8; ++k) {
@@ -277,7 +279,8 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
                     for (int v = 0; v < 16; ++v) {
 #pragma unroll
                         for (int u = 0; u < 2; ++u)
-                            w[u][v >> 2] = put_byte(w[u][v >> 2], ring_step(ch[u].x, ch[u].pr, ch[u].nb, ch[u].tab),
+                            w[u][v >> 2] = put_byte(w[u][v >> 2],
+                                                    ring_step(ch[u].x, ch[u].pr, ch[u].nb, ch[u].tab, ch[u].rb),
                                                     v & 3);
                     }
                 } else {  // bytes shift in from the top: no runtime index into w[]

@@ -96,6 +96,91 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
     return v;
 }
 
+// ---- word-window decoding ------------------------------------------------
+// The stream is read through an 8-byte window of two aligned shared words
+// (w0 holds the next unread byte at bit offset o, w1 the word after; wa is
+// the shared address of w1).  A step PAIR needs at most 4 stream bytes, so
+// both steps take their bytes from one funnel-shifted word v = bytes[p, p+4)
+// with PRMT (x = x << 8 | v.byte[s&3], selector s counts bytes used), and the
+// window moves at most one word per pair: one predicated LDS.32 per pair
+// instead of two predicated LDS.U8 per step.  Fully predicated-off shared
+// loads cost no wavefront, and only ~1 in 4 lanes crosses a word per pair.
+constexpr uint32_t kSelBase = 0x2104;  // PRMT: {x.b2, x.b1, x.b0, v.b[sel&3]}
+
+struct Win {
+    uint32_t w0, w1, wa, o;
+};
+
+__device__ __forceinline__ void win_init(Win& w, uint32_t p) {
+    const uint32_t a = p & ~3u;
+    w.w0 = lds_u32(a);
+    w.w1 = lds_u32(a + 4);
+    w.wa = a + 4;
+    w.o = (p & 3u) * 8u;
+}
+// shared address of the next unread byte
+__device__ __forceinline__ uint32_t win_pos(const Win& w) { return w.wa - 4u + (w.o >> 3); }
+
+__device__ __forceinline__ uint32_t win_bytes(const Win& w) {
+    uint32_t v;
+    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(v) : "r"(w.w0), "r"(w.w1), "r"(w.o));
+    return v;
+}
+
+// One symbol: table lookup, state update, up to two refill bytes from v.
+__device__ __forceinline__ uint32_t dec_sym(uint32_t& x, uint32_t& s, uint32_t v, uint32_t tab) {
+    uint32_t e;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
+        "and.b32 a, %0, 4095;\n\t"
+        "mad.lo.u32 a, a, 4, %4;\n\t"
+        "ld.shared.u32 %2, [a];\n\t"
+        "shr.u32 f, %2, 20;\n\t"
+        "shr.u32 b, %2, 8;\n\t"
+        "shr.u32 t, %0, 12;\n\t"
+        "sub.u32 t, t, 4096;\n\t"
+        "mad.lo.u32 %0, f, t, b;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q prmt.b32 %0, %0, %3, %1;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q prmt.b32 %0, %0, %3, %1;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t}"
+        : "+r"(x), "+r"(s), "=r"(e)
+        : "r"(v), "r"(tab));
+    return e;
+}
+
+// Consume s - kSelBase bytes; slide the window by a word when o crosses 32.
+// (o + 8*s is biased by 8*kSelBase = 0x10820, a multiple of 32.)
+__device__ __forceinline__ void win_advance(Win& w, uint32_t s) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "mad.lo.u32 %3, %4, 8, %3;\n\t"
+        "setp.ge.u32 q, %3, 0x10840;\n\t"
+        "@q mov.b32 %0, %1;\n\t"
+        "@q add.u32 %2, %2, 4;\n\t"
+        "@q ld.shared.u32 %1, [%2];\n\t"
+        "and.b32 %3, %3, 31;\n\t}"
+        : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
+        : "r"(s));
+}
+
+// Same inside a 128-byte ring (fused kernel): the word address wraps.
+__device__ __forceinline__ void win_advance_ring(Win& w, uint32_t s) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 n;\n\t"
+        "mad.lo.u32 %3, %4, 8, %3;\n\t"
+        "setp.ge.u32 q, %3, 0x10840;\n\t"
+        "@q mov.b32 %0, %1;\n\t"
+        "@q add.u32 n, %2, 4;\n\t"
+        "@q lop3.b32 %2, n, %2, 127, 0xE4;\n\t"
+        "@q ld.shared.u32 %1, [%2];\n\t"
+        "and.b32 %3, %3, 31;\n\t}"
+        : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
+        : "r"(s));
+}
+
 template <bool kConverged>
 __device__ __forceinline__ uint32_t dec_step(uint32_t& x, uint32_t& p, uint32_t& nb, uint32_t tab) {
     uint32_t e;

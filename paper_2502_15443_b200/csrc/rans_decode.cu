@@ -174,22 +174,24 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
     const uint32_t tab = smem_u32(tab_ptr), stage = smem_u32(stage_ptr);
     const uint32_t K = 1u << seg_shift;
     const int G = (int)(K >> 4);
-    uint32_t x[NU], p[NU], n[NU], nb[NU];
+    uint32_t x[NU], n[NU];
+    Win W[NU];
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
         const int r = warp * 32 + lane + u * kDecThreads;
         const uint32_t rel = (uint32_t)(s0 + r);
+        uint32_t p;
         if (r < ns) {
             x[u] = seg_state[sb + rel];
-            p[u] = stage + seg_off[sb + rel] - lo + delta;
+            p = stage + seg_off[sb + rel] - lo + delta;
             const uint64_t rem = olen - ((uint64_t)rel << seg_shift);
             n[u] = rem < K ? (uint32_t)rem : K;
         } else {  // decodes harmless garbage from stage[0..2K), never written
             x[u] = kStateLower;
-            p[u] = stage;
+            p = stage;
             n[u] = 0;
         }
-        nb[u] = lds_u8(p[u]);
+        win_init(W[u], p);
     }
     for (int g = 0; g < G; ++g) {
         const uint32_t g0 = (uint32_t)g << 4;
@@ -199,12 +201,22 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
         for (int u = 0; u < NU; ++u) full = full && (n[u] == 0 || g0 + 16 <= n[u]);
         if (__all_sync(0xffffffffu, full)) {
 #pragma unroll
-            for (int v = 0; v < 16; ++v) {
+            for (int v = 0; v < 16; v += 2) {  // step pairs share one window word
+                uint32_t wv[NU], sel[NU];
 #pragma unroll
                 for (int u = 0; u < NU; ++u) {
-                    const uint32_t e = dec_step<true>(x[u], p[u], nb[u], tab);
-                    w[u][v >> 2] = put_byte(w[u][v >> 2], e, v & 3);
+                    wv[u] = win_bytes(W[u]);
+                    sel[u] = kSelBase;
                 }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int u = 0; u < NU; ++u) {
+                        const uint32_t e = dec_sym(x[u], sel[u], wv[u], tab);
+                        w[u][(v + h) >> 2] = put_byte(w[u][(v + h) >> 2], e, (v + h) & 3);
+                    }
+#pragma unroll
+                for (int u = 0; u < NU; ++u) win_advance(W[u], sel[u]);
             }
         } else {
 #pragma unroll
@@ -214,7 +226,9 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
 #pragma unroll
                 for (int u = 0; u < NU; ++u) {
                     if (g0 + v < n[u]) {
-                        const uint32_t e = dec_step<false>(x[u], p[u], nb[u], tab);
+                        uint32_t sel = kSelBase;
+                        const uint32_t e = dec_sym(x[u], sel, win_bytes(W[u]), tab);
+                        win_advance(W[u], sel);
                         w[u][v >> 2] = put_byte(w[u][v >> 2], e, v & 3);
                     }
                 }
@@ -265,7 +279,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
             xe = kStateLower;
             pe = plen;
         }
-        if (x[u] != xe || p[u] - stage - delta + lo != pe) atomicExch(st, DC_CHUNK_CHAIN);
+        if (x[u] != xe || win_pos(W[u]) - stage - delta + lo != pe) atomicExch(st, DC_CHUNK_CHAIN);
     }
 }
 
