@@ -65,6 +65,20 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel: str, config: dict):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/traffic.json, tools/ncu_traffic.py) when it was taken on this
+    exact workload; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            e = json.load(f)[kernel]
+        if all(config.get(k) == v for k, v in e["config"].items()):
+            return e["dram_bytes_per_launch"], e["report"]
+    except Exception:
+        pass
+    return None, None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -369,6 +383,8 @@ def main():
         except Exception as e:  # report, never fake
             cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
 
+    traffic, traffic_src = ncu_traffic("k_decode_segments", {"model": args.model, "chunk_size": args.chunk_size,
+                                                            "seg_shift": args.seg_shift, "layers": args.layers})
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -382,8 +398,8 @@ def main():
                        "l2": "inputs (compressed) and outputs exceed the 126 MB L2", "parallelism": f"dp{world} (replicas)",
                        "build_s": t_build},
             "roofline": {"bound": "hbm", "kernel": "k_decode_segments", "achieved": achieved, "peak": hbm,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                         "alg_bytes_per_launch": alg_bytes, "launch_ms": kms},
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                         "traffic_src": traffic_src, "alg_bytes_per_launch": alg_bytes, "launch_ms": kms},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "decode_step_tokens": tokens,

@@ -89,7 +89,8 @@ __device__ __forceinline__ void cp_async_wait() {
 // byte counter whose low 7 bits are the ring offset of the next unread byte;
 // the shared address of a byte is (pr & 127) | rb (one LOP3, rb = the
 // 128-B aligned ring base), so the counter itself never wraps.
-__device__ __forceinline__ uint32_t ring_step(uint32_t& x, uint32_t& pr, uint32_t& nb, uint32_t tab, uint32_t rb) {
+__device__ __forceinline__ uint32_t ring_step(uint32_t& x, uint32_t& pr, uint32_t& nb, uint32_t tab, uint32_t rb,
+                                              const FmaK&) {  // FMA-pipe variant measured slower here
     uint32_t e;
     asm volatile(
         "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t, a1, a2;\n\t"
@@ -139,8 +140,8 @@ __device__ __forceinline__ void ring_refill(Chain& c, uint32_t ring_base) {
 }
 
 // Generic (mixed-mode) step: returns the next weight byte of chain c.
-__device__ __forceinline__ uint32_t chain_step(Chain& c) {
-    if (c.mode == 0) return ring_step(c.x, c.pr, c.nb, c.tab, c.rb);
+__device__ __forceinline__ uint32_t chain_step(Chain& c, const FmaK& k) {
+    if (c.mode == 0) return ring_step(c.x, c.pr, c.nb, c.tab, c.rb, k);
     if (c.mode == 1) {
         const uint32_t e = c.nb;
         ++c.pr;
@@ -155,8 +156,9 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
     const uint64_t* __restrict__ out_len, const uint8_t* __restrict__ codec, uint64_t chunk_size,
     const int64_t* __restrict__ seg_base, const uint32_t* __restrict__ seg_state,
     const uint32_t* __restrict__ seg_off, const GemmTensorR* __restrict__ tens, const int4* __restrict__ items,
-    int n_items, int ntok, int32_t* __restrict__ status) {
+    int n_items, int ntok, int32_t* __restrict__ status, uint32_t one) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const FmaK fk = fma_consts(one);
     RingSmem& S = *reinterpret_cast<RingSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = warp & 3, jj = warp >> 2;
@@ -276,19 +278,24 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
                 uint32_t w[2][4];
                 if (fast) {
 #pragma unroll
-                    for (int v = 0; v < 16; ++v) {
+                    for (int v = 0; v < 16; v += 2) {  // 3 PRMT per 4 output bytes
+                        uint32_t e0[2];
 #pragma unroll
                         for (int u = 0; u < 2; ++u)
-                            w[u][v >> 2] = put_byte(w[u][v >> 2],
-                                                    ring_step(ch[u].x, ch[u].pr, ch[u].nb, ch[u].tab, ch[u].rb),
-                                                    v & 3);
+                            e0[u] = ring_step(ch[u].x, ch[u].pr, ch[u].nb, ch[u].tab, ch[u].rb, fk);
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const uint32_t t = __byte_perm(
+                                e0[u], ring_step(ch[u].x, ch[u].pr, ch[u].nb, ch[u].tab, ch[u].rb, fk), 0x0040);
+                            w[u][v >> 2] = (v & 2) ? __byte_perm(w[u][v >> 2], t, 0x5410) : t;
+                        }
                     }
                 } else {  // bytes shift in from the top: no runtime index into w[]
 #pragma unroll 1
                     for (int v = 0; v < 16; ++v) {
 #pragma unroll
                         for (int u = 0; u < 2; ++u) {
-                            const uint32_t e = chain_step(ch[u]);
+                            const uint32_t e = chain_step(ch[u], fk);
                             w[u][0] = __funnelshift_r(w[u][0], w[u][1], 8);
                             w[u][1] = __funnelshift_r(w[u][1], w[u][2], 8);
                             w[u][2] = __funnelshift_r(w[u][2], w[u][3], 8);
@@ -388,7 +395,7 @@ extern "C" int dc_fused_ring_gemm(const uint8_t* base, const uint64_t* blob_off,
     const int64_t grid = n_items < sms ? n_items : sms;
     k_fused_ring<<<(unsigned)grid, kRThreads, smem, (cudaStream_t)stream>>>(
         base, blob_off, blob_len, out_len, codec, chunk_size, seg_base, seg_state, seg_off,
-        reinterpret_cast<const GemmTensorR*>(tens), reinterpret_cast<const int4*>(items), (int)n_items, ntok, status);
+        reinterpret_cast<const GemmTensorR*>(tens), reinterpret_cast<const int4*>(items), (int)n_items, ntok, status, 1u);
     DC_CHECK_LAUNCH("k_fused_ring");
     return DC_OK;
 }

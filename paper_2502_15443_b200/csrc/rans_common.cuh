@@ -151,6 +151,38 @@ __device__ __forceinline__ uint32_t dec_sym(uint32_t& x, uint32_t& s, uint32_t v
     return e;
 }
 
+// Pipe balancing: shifts and LEA run on the ALU pipe, which the decode loop
+// saturates; IMAD / IMAD.HI by a constant held in a register (opaque to ptxas,
+// so it cannot turn them back into shifts) run on the FMA pipe instead.
+struct FmaK {
+    uint32_t c4, c2p12, c2p24, c2p20, cm4096;
+};
+__device__ __forceinline__ FmaK fma_consts(uint32_t one) {
+    return FmaK{4u * one, 4096u * one, (1u << 24) * one, (1u << 20) * one, 0u - 4096u * one};
+}
+
+__device__ __forceinline__ uint32_t dec_sym(uint32_t& x, uint32_t& s, uint32_t v, uint32_t tab, const FmaK& k) {
+    uint32_t e;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
+        "and.b32 a, %0, 4095;\n\t"
+        "mad.lo.u32 a, a, %5, %4;\n\t"
+        "ld.shared.u32 %2, [a];\n\t"
+        "mul.hi.u32 f, %2, %6;\n\t"
+        "shr.u32 b, %2, 8;\n\t"
+        "mad.hi.u32 t, %0, %8, %9;\n\t"
+        "mad.lo.u32 %0, f, t, b;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q prmt.b32 %0, %0, %3, %1;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q prmt.b32 %0, %0, %3, %1;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t}"
+        : "+r"(x), "+r"(s), "=r"(e)
+        : "r"(v), "r"(tab), "r"(k.c4), "r"(k.c2p12), "r"(k.c2p24), "r"(k.c2p20), "r"(k.cm4096));
+    return e;
+}
+
 // Consume s - kSelBase bytes; slide the window by a word when o crosses 32.
 // (o + 8*s is biased by 8*kSelBase = 0x10820, a multiple of 32.)
 __device__ __forceinline__ void win_advance(Win& w, uint32_t s) {

@@ -169,7 +169,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
                                             const uint32_t* __restrict__ seg_state,
                                             const uint32_t* __restrict__ seg_off, const uint32_t* tab_ptr,
                                             const uint8_t* stage_ptr, uint8_t* ob, uint8_t* __restrict__ obase,
-                                            bool out_aligned, int32_t* st) {
+                                            bool out_aligned, int32_t* st, const FmaK& fk) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tab = smem_u32(tab_ptr), stage = smem_u32(stage_ptr);
     const uint32_t K = 1u << seg_shift;
@@ -208,13 +208,15 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
                     wv[u] = win_bytes(W[u]);
                     sel[u] = kSelBase;
                 }
+                uint32_t e0[NU];
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
+                for (int u = 0; u < NU; ++u) e0[u] = dec_sym(x[u], sel[u], wv[u], tab, fk);
 #pragma unroll
-                    for (int u = 0; u < NU; ++u) {
-                        const uint32_t e = dec_sym(x[u], sel[u], wv[u], tab);
-                        w[u][(v + h) >> 2] = put_byte(w[u][(v + h) >> 2], e, (v + h) & 3);
-                    }
+                for (int u = 0; u < NU; ++u) {
+                    // two symbols -> bytes 0,1 of t; two pairs -> one word (3 PRMT per 4 bytes)
+                    const uint32_t t = __byte_perm(e0[u], dec_sym(x[u], sel[u], wv[u], tab, fk), 0x0040);
+                    w[u][v >> 2] = (v & 2) ? __byte_perm(w[u][v >> 2], t, 0x5410) : t;
+                }
 #pragma unroll
                 for (int u = 0; u < NU; ++u) win_advance(W[u], sel[u]);
             }
@@ -227,7 +229,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
                 for (int u = 0; u < NU; ++u) {
                     if (g0 + v < n[u]) {
                         uint32_t sel = kSelBase;
-                        const uint32_t e = dec_sym(x[u], sel, win_bytes(W[u]), tab);
+                        const uint32_t e = dec_sym(x[u], sel, win_bytes(W[u]), tab, fk);
                         win_advance(W[u], sel);
                         w[u][v >> 2] = put_byte(w[u][v >> 2], e, v & 3);
                     }
@@ -288,8 +290,9 @@ __global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
     const uint64_t* __restrict__ out_off, const uint64_t* __restrict__ out_len, uint32_t seg_shift,
     const int64_t* __restrict__ seg_base, const uint32_t* __restrict__ seg_state,
     const uint32_t* __restrict__ seg_off, const int4* __restrict__ tasks, int64_t n_tasks,
-    uint8_t* __restrict__ out, int32_t* __restrict__ status) {
+    uint8_t* __restrict__ out, int32_t* __restrict__ status, uint32_t one) {
     extern __shared__ __align__(1024) uint8_t smem[];
+    const FmaK fk = fma_consts(one);
     TableSmem& T = *reinterpret_cast<TableSmem*>(smem + kOffTab);
     uint8_t* stage = smem + kOffStage;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
@@ -366,10 +369,10 @@ __global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
         if (warp * 32 >= ns) continue;  // idle warp in a short task
         if (warp * 32 + kDecThreads < ns)
             decode_warp<2>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state, seg_off, T.tab,
-                           stage, ob, obase, out_aligned, &status[c]);
+                           stage, ob, obase, out_aligned, &status[c], fk);
         else
             decode_warp<1>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state, seg_off, T.tab,
-                           stage, ob, obase, out_aligned, &status[c]);
+                           stage, ob, obase, out_aligned, &status[c], fk);
     }
 }
 
@@ -468,7 +471,7 @@ extern "C" int dc_ans_decode_segments(const uint8_t* base, const uint64_t* blob_
     const int64_t grid = n_tasks < cap ? n_tasks : cap;
     k_decode_segments<<<(unsigned)grid, kDecThreads, kDecSmem, (cudaStream_t)stream>>>(
         base, blob_off, blob_len, out_off, out_len, seg_shift, seg_base, seg_state, seg_off,
-        reinterpret_cast<const int4*>(tasks), n_tasks, out, status);
+        reinterpret_cast<const int4*>(tasks), n_tasks, out, status, 1u);
     DC_CHECK_LAUNCH("k_decode_segments");
     return DC_OK;
 }
