@@ -6,9 +6,9 @@
 //                exactly: floor allocation, largest-remainder top-up in
 //                (remainder desc, symbol asc) order, argmax repayment; then
 //                packs the 384-byte u12 wire table (ans.py:246-253)
-//   k_encode     one lane per chunk runs the reverse encoder (ans.py:55-68)
-//                with exact reciprocal division; per-lane symbol tables live
-//                in bank-private shared memory (lane l only touches bank l)
+//   k_encode     one warp per chunk, one lane runs the reverse encoder
+//                (ans.py:55-68) as a branch-free recurrence with exact
+//                reciprocal division; the warp builds the chunk's table
 //   k_assemble   scatters table | state | stream (or raw) into the file image
 #include "common.cuh"
 
@@ -171,107 +171,195 @@ __global__ void k_normalize(const uint32_t* __restrict__ hist, int64_t n_chunks,
 }
 
 // ----------------------------------------------------------------- encode
-// Per-lane symbol table in bank-private layout: word (s*2 + w)*32 + lane.
-//   w0 = reciprocal (ryg_rans style exact division for x < 2^31)
-//   w1 = f (13 bits) | cum << 13 (12 bits) | shift << 25 (4 bits)
-constexpr int kEncLanes = 32;
+// One chunk per WARP (four warps per CTA, one per SM sub-partition): the
+// reverse encoder (ans.py:55-68) is a serial recurrence per chunk, so every
+// lane of the warp runs the same chain (uniform, no divergence) and the chunk's
+// time is that chain.  The step is branch-free:
+//   p1 = x >= f<<16, p2 = x >= f<<24  (at most two renorm bytes: x < 2^28)
+//   xr = x >> 8*(p1+p2)
+//   x  = xr + bias + (umulhi(xr, rcp) >> sh) * (4096 - f)
+// with ryg_rans-style exact reciprocals (f == 1: rcp = 2^32-1 gives q = xr-1,
+// folded into bias = cum + 4095).  Renorm bytes go to a 256-byte shared ring
+// (32-bit addressing, one STS each) that the warp flushes to global memory
+// 128 bytes at a time with all 32 lanes.
+constexpr int kEncWarps = 4;
+constexpr uint32_t kEncRing = 256;
 
-__global__ void __launch_bounds__(kEncLanes) k_encode(const uint8_t* __restrict__ data, uint64_t total,
-                                                       uint64_t chunk_size, int64_t n_chunks,
-                                                       const uint8_t* __restrict__ todo,
-                                                       const uint32_t* __restrict__ freq, uint8_t* __restrict__ scratch,
-                                                       uint32_t* __restrict__ final_state,
-                                                       uint64_t* __restrict__ stream_len, uint32_t seg_shift,
-                                                       const int64_t* __restrict__ seg_base,
-                                                       uint32_t* __restrict__ seg_state,
-                                                       uint32_t* __restrict__ seg_emitted, uint32_t flags) {
-    extern __shared__ uint32_t etab[];  // 256 * 2 * 32 words = 64 KB
-    const int lane = threadIdx.x;
-    const int64_t c = (int64_t)blockIdx.x * kEncLanes + lane;
-    const bool active = c < n_chunks && todo[c];
-    uint64_t beg = 0, len = 0;
-    if (active) {
-        beg = (uint64_t)c * chunk_size;
-        len = total - beg < chunk_size ? total - beg : chunk_size;
-        const uint32_t* f = freq + c * 256;
-        uint32_t cum = 0;
-        for (int s = 0; s < 256; ++s) {
-            const uint32_t fs = f[s];
-            uint32_t rcp = 0, shift = 0;
-            if (fs >= 2) {
-                while (fs > (1u << shift)) ++shift;
-                rcp = (uint32_t)(((1ull << (shift + 31)) + fs - 1) / fs);
-                shift -= 1;
+struct __align__(16) EncEnt {
+    uint32_t rcp, xm1, xm2, sh;  // xm1 = f << 16; xm2 = f << 24 or 2^32-1 when f >= 16
+    uint32_t bias, gmul, pad0, pad1;  // gmul = 4096 - f
+};
+
+struct EncSmem {
+    EncEnt tab[256];
+    uint8_t ring[kEncRing];
+};
+
+__device__ __forceinline__ void enc_step(uint32_t& x, uint32_t& pos, const uint4& a, const uint2& b, uint32_t ring) {
+    // a = (rcp, xm1, xm2, sh), b = (bias, gmul); chain: setp -> selp -> selp -> mul.hi -> shr -> mad
+    asm volatile(
+        "{\n\t.reg .pred p1, p2;\n\t.reg .u32 x8, x16, xr, q, xb, r1, r2, n;\n\t"
+        "setp.ge.u32 p1, %0, %3;\n\t"
+        "setp.ge.u32 p2, %0, %4;\n\t"
+        "shr.u32 x8, %0, 8;\n\t"
+        "shr.u32 x16, %0, 16;\n\t"
+        "and.b32 r1, %1, 255;\n\t"
+        "add.u32 r1, r1, %8;\n\t"
+        "add.u32 r2, %1, 1;\n\t"
+        "and.b32 r2, r2, 255;\n\t"
+        "add.u32 r2, r2, %8;\n\t"
+        "@p1 st.shared.u8 [r1], %0;\n\t"
+        "@p2 st.shared.u8 [r2], x8;\n\t"
+        "selp.u32 n, 1, 0, p1;\n\t"
+        "@p2 add.u32 n, n, 1;\n\t"
+        "add.u32 %1, %1, n;\n\t"
+        "selp.u32 xr, x8, %0, p1;\n\t"
+        "selp.u32 xr, x16, xr, p2;\n\t"
+        "mul.hi.u32 q, xr, %2;\n\t"
+        "add.u32 xb, xr, %6;\n\t"
+        "shr.u32 q, q, %5;\n\t"
+        "mad.lo.u32 %0, q, %7, xb;\n\t}"
+        : "+r"(x), "+r"(pos)
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(ring)
+        : "memory");
+}
+
+__device__ __forceinline__ void enc_sym(uint32_t& x, uint32_t& pos, const EncEnt* __restrict__ T, uint32_t s,
+                                        uint8_t* ring) {
+    const uint4 a = *reinterpret_cast<const uint4*>(&T[s].rcp);
+    const uint2 b = *reinterpret_cast<const uint2*>(&T[s].bias);
+    enc_step(x, pos, a, b, (uint32_t)__cvta_generic_to_shared(ring));
+}
+
+// emissions [from, to) of the ring -> global bytes out_end - 1 - k (all lanes)
+__device__ __forceinline__ void enc_flush(const uint8_t* ring, uint8_t* out_end, uint32_t from, uint32_t to,
+                                          int lane) {
+    __syncwarp();
+    for (uint32_t k = from + lane; k < to; k += 32) *(out_end - 1 - k) = ring[k & (kEncRing - 1)];
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __restrict__ data, uint64_t total,
+                                                            uint64_t chunk_size, int64_t n_chunks,
+                                                            const uint8_t* __restrict__ todo,
+                                                            const uint32_t* __restrict__ freq,
+                                                            uint8_t* __restrict__ scratch,
+                                                            uint32_t* __restrict__ final_state,
+                                                            uint64_t* __restrict__ stream_len, uint32_t seg_shift,
+                                                            const int64_t* __restrict__ seg_base,
+                                                            uint32_t* __restrict__ seg_state,
+                                                            uint32_t* __restrict__ seg_emitted, uint32_t flags) {
+    __shared__ EncSmem sm[kEncWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * kEncWarps + warp;
+    if (c >= n_chunks || !todo[c]) return;  // whole warp; no block-level sync below
+    const uint64_t beg = (uint64_t)c * chunk_size;
+    const uint64_t len = total - beg < chunk_size ? total - beg : chunk_size;
+    EncEnt* T = sm[warp].tab;
+    uint8_t* ring = sm[warp].ring;
+    {  // lane owns symbols 8*lane .. 8*lane+7; cum = exclusive warp scan of f
+        uint32_t fs[8], loc = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            fs[k] = freq[c * 256 + lane * 8 + k];
+            loc += fs[k];
+        }
+        uint32_t inc = loc;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        uint32_t cum = inc - loc;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t f = fs[k];
+            EncEnt e;
+            e.sh = 0;
+            if (f >= 2) {
+                uint32_t shift = 0;
+                while (f > (1u << shift)) ++shift;
+                e.rcp = (uint32_t)(((1ull << (shift + 31)) + f - 1) / f);
+                e.sh = shift - 1;
             } else {
-                rcp = 0xFFFFFFFFu;  // f == 1: q = x - 1 via mulhi
+                e.rcp = 0xFFFFFFFFu;
             }
-            etab[(s * 2 + 0) * 32 + lane] = rcp;
-            etab[(s * 2 + 1) * 32 + lane] = fs | (cum << 13) | (shift << 25);
-            cum += fs;
+            e.xm1 = f << 16;
+            e.xm2 = f < 16 ? f << 24 : 0xFFFFFFFFu;
+            e.bias = f >= 2 ? cum : cum + (kProbScale - 1);
+            e.gmul = kProbScale - f;
+            e.pad0 = e.pad1 = 0;
+            T[lane * 8 + k] = e;
+            cum += f;
         }
     }
-    if (!active) return;  // no block-level sync below
+    __syncwarp();
+
     const uint8_t* src = data + beg;
-    uint8_t* slot_end = scratch + beg + len;  // bytes go backwards from here
+    uint8_t* out_end = scratch + beg + len;  // bytes go backwards from here
     // emitted >= limit -> the chunk will be stored (container.py:165); a
     // standalone blob (flags & 1) is always completed (ans.py:316-330)
     const uint64_t limit = (flags & 1) ? ~0ull : (len > kHeaderBytes ? len - kHeaderBytes : 0);
     const uint32_t K = 1u << seg_shift;
     const int64_t sb = seg_state ? seg_base[c] : 0;
-    uint32_t x = kStateLower;
-    uint64_t pos = 0;
+    const bool rec = seg_state != nullptr && lane == 0;
+    uint32_t x = kStateLower, pos = 0, flushed = 0;
     bool stored = (limit == 0);
-    // walk the chunk backwards in aligned 16-byte blocks
-    const uintptr_t a_beg = reinterpret_cast<uintptr_t>(src);
-    const uintptr_t a_end = a_beg + len;
-    const uintptr_t data_end = reinterpret_cast<uintptr_t>(data) + total;
-    uintptr_t blk = (a_end - 1) & ~(uintptr_t)15;
-    for (; !stored && blk + 16 > a_beg; blk -= 16) {
-        uint4 q;
-        if (blk + 16 <= data_end) {
-            q = *reinterpret_cast<const uint4*>(blk);
-        } else {  // last block of the buffer: never read past its end
-            uint8_t b[16];
-            for (int k = 0; k < 16; ++k) b[k] = (blk + k < data_end) ? *reinterpret_cast<const uint8_t*>(blk + k) : 0;
-            q.x = b[0] | b[1] << 8 | b[2] << 16 | (uint32_t)b[3] << 24;
-            q.y = b[4] | b[5] << 8 | b[6] << 16 | (uint32_t)b[7] << 24;
-            q.z = b[8] | b[9] << 8 | b[10] << 16 | (uint32_t)b[11] << 24;
-            q.w = b[12] | b[13] << 8 | b[14] << 16 | (uint32_t)b[15] << 24;
+    const uint64_t nblk = len >> 4;  // whole 16-symbol blocks [0, 16*nblk)
+    // tail symbols [16*nblk, len), last to first
+    for (uint64_t i = len; !stored && i > nblk * 16;) {
+        --i;
+        enc_sym(x, pos, T, src[i], ring);
+        if (rec && (i & (K - 1)) == 0) {
+            seg_state[sb + (i >> seg_shift)] = x;
+            seg_emitted[sb + (i >> seg_shift)] = pos;
         }
-        const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int k = 15; k >= 0; --k) {
-            const uintptr_t a = blk + k;
-            if (a < a_beg || a >= a_end) continue;
-            const uint32_t s = (wv[k >> 2] >> (8 * (k & 3))) & 0xFF;
-            const uint32_t rcp = etab[(s * 2 + 0) * 32 + lane];
-            const uint32_t meta = etab[(s * 2 + 1) * 32 + lane];
-            const uint32_t f = meta & 0x1FFF;
-            const uint32_t cum = (meta >> 13) & 0xFFF;
-            const uint32_t sh = meta >> 25;
-            const uint32_t x_max = f << 16;  // ans.py:62
-            while (x >= x_max) {             // ans.py:63-66
-                *(slot_end - 1 - pos) = (uint8_t)(x & 0xFF);
-                ++pos;
-                x >>= 8;
-            }
-            // ans.py:67: x = (x // f) * 4096 + cum + x % f, exact via reciprocal
-            const uint32_t qd = __umulhi(x, rcp) >> sh;
-            x = x + (f >= 2 ? cum : cum + (kProbScale - 1)) + qd * (f >= 2 ? kProbScale - f : kProbScale - 1);
-            const uint64_t i = (uint64_t)(a - a_beg);
-            if (seg_state && (i & (K - 1)) == 0) {
-                seg_state[sb + (i >> seg_shift)] = x;
-                seg_emitted[sb + (i >> seg_shift)] = (uint32_t)pos;
-            }
-            if (pos >= limit) {  // could not beat raw storage (container.py:165)
-                stored = true;
-                break;
-            }
-        }
-        if (blk < 16) break;
+        if (pos >= limit) stored = true;
     }
-    final_state[c] = x;
-    stream_len[c] = stored ? ~0ull : pos;
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+    const bool al16 = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    auto load_blk = [&](uint64_t b) -> uint4 {
+        if (al16) return __ldg(reinterpret_cast<const uint4*>(src + 16 * b));
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            w[k] = src[16 * b + 4 * k] | (uint32_t)src[16 * b + 4 * k + 1] << 8 |
+                   (uint32_t)src[16 * b + 4 * k + 2] << 16 | (uint32_t)src[16 * b + 4 * k + 3] << 24;
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    };
+    uint4 nxt = (!stored && nblk) ? load_blk(nblk - 1) : make_uint4(0, 0, 0, 0);
+    for (uint64_t b = nblk; !stored && b > 0;) {
+        --b;
+        const uint4 cur = nxt;
+        if (b) nxt = load_blk(b - 1);  // prefetch the next (lower) block
+        const uint32_t wv[4] = {cur.x, cur.y, cur.z, cur.w};
+        // table entries of the whole block first (they do not depend on x), then the chain
+        uint4 ea[16];
+        uint2 eb[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t sy = (wv[k >> 2] >> (8 * (k & 3))) & 0xFF;
+            ea[k] = *reinterpret_cast<const uint4*>(&T[sy].rcp);
+            eb[k] = *reinterpret_cast<const uint2*>(&T[sy].bias);
+        }
+#pragma unroll
+        for (int k = 15; k >= 0; --k) enc_step(x, pos, ea[k], eb[k], ring_s);
+        const uint64_t i = 16 * b;  // split points sit at multiples of K >= 16: only at k == 0
+        if (rec && (i & (K - 1)) == 0) {
+            seg_state[sb + (i >> seg_shift)] = x;
+            seg_emitted[sb + (i >> seg_shift)] = pos;
+        }
+        if (pos - flushed >= kEncRing / 2) {  // at most 32 bytes per block: the ring never overruns
+            enc_flush(ring, out_end, flushed, flushed + kEncRing / 2, lane);
+            flushed += kEncRing / 2;
+        }
+        if (pos >= limit) stored = true;  // could not beat raw storage (container.py:165)
+    }
+    if (!stored) enc_flush(ring, out_end, flushed, pos, lane);
+    if (lane == 0) {
+        final_state[c] = x;
+        stream_len[c] = stored ? ~0ull : pos;
+    }
 }
 
 // --------------------------------------------------------------- assemble
@@ -344,13 +432,7 @@ extern "C" int dc_ans_encode_chunks(const uint8_t* data, uint64_t total, uint64_
                                     uint32_t flags, void* stream) {
     if (n_chunks < 0 || chunk_size == 0 || (seg_state && (seg_shift < 4 || seg_shift > 20))) return DC_ERR_ARG;
     if (n_chunks == 0) return DC_OK;
-    const int smem = 256 * 2 * 32 * 4;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
-    k_encode<<<(unsigned)((n_chunks + kEncLanes - 1) / kEncLanes), kEncLanes, smem, (cudaStream_t)stream>>>(
+    k_encode<<<(unsigned)((n_chunks + kEncWarps - 1) / kEncWarps), kEncWarps * 32, 0, (cudaStream_t)stream>>>(
         data, total, chunk_size, n_chunks, todo, freq, scratch, final_state, stream_len, seg_shift, seg_base,
         seg_state, seg_emitted, flags);
     DC_CHECK_LAUNCH("k_encode");
