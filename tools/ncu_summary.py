@@ -25,7 +25,14 @@ RAW = ("dram__bytes_read.sum", "dram__bytes_write.sum", "l1tex__data_pipe_lsu_wa
        "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
        "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
        "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
-       "smsp__average_warps_issue_stalled_sleeping_per_issue_active.ratio")
+       "smsp__average_warps_issue_stalled_sleeping_per_issue_active.ratio",
+       "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+       "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+       "sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active",
+       "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active")
 
 
 def run(args):
