@@ -119,6 +119,7 @@ __device__ __forceinline__ uint32_t ring_step(uint32_t& x, uint32_t& pr, uint32_
 
 struct Chain {
     uint32_t x, pr, nb, tab, rb;  // pr: free-running ring counter, rb: ring base
+    uint32_t w0, w1, o;           // word window (kWindow): pr = ring counter of w1's byte address
     uint64_t gfill;   // next global address to request (16-B aligned)
     uint32_t xe;      // expected end state
     uint64_t gend;    // expected end position (global address of the next byte)
@@ -128,8 +129,47 @@ struct Chain {
     uint32_t sym;
 };
 
+// Stream reads: byte-at-a-time (LDS.U8 per refill) or through a two-word
+// window (one predicated LDS.32 per step pair, see rans_common.cuh Win).
+#ifndef DC_FUSED_WINDOW
+#define DC_FUSED_WINDOW 1
+#endif
+constexpr bool kWindow = DC_FUSED_WINDOW != 0;
+
 // bytes buffered ahead of the read position (ring invariant: < 128)
-__device__ __forceinline__ uint32_t ring_avail(const Chain& c) { return ((uint32_t)c.gfill - c.pr) & 127u; }
+__device__ __forceinline__ uint32_t ring_avail(const Chain& c) {
+    const uint32_t rd = kWindow ? c.pr - 4u + (c.o >> 3) : c.pr;
+    return ((uint32_t)c.gfill - rd) & 127u;
+}
+
+__device__ __forceinline__ void fwin_init(Chain& c, uint32_t p) {  // p: ring offset of the first byte
+    const uint32_t a = p & ~3u;
+    c.w0 = lds_u32(c.rb | a);
+    c.pr = a + 4u;
+    c.w1 = lds_u32(c.rb | (c.pr & 127u));
+    c.o = (p & 3u) * 8u;
+}
+
+__device__ __forceinline__ uint32_t fwin_bytes(const Chain& c) {
+    uint32_t v;
+    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(v) : "r"(c.w0), "r"(c.w1), "r"(c.o));
+    return v;
+}
+
+// consume s - kSelBase bytes (see win_advance); the word address wraps in the ring
+__device__ __forceinline__ void fwin_advance(Chain& c, uint32_t s) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 a;\n\t"
+        "mad.lo.u32 %3, %5, 8, %3;\n\t"
+        "setp.ge.u32 q, %3, 0x10840;\n\t"
+        "@q mov.b32 %0, %1;\n\t"
+        "@q add.u32 %2, %2, 4;\n\t"
+        "lop3.b32 a, %2, 127, %4, 0xEA;\n\t"
+        "@q ld.shared.u32 %1, [a];\n\t"
+        "and.b32 %3, %3, 31;\n\t}"
+        : "+r"(c.w0), "+r"(c.w1), "+r"(c.pr), "+r"(c.o)
+        : "r"(c.rb), "r"(s));
+}
 
 __device__ __forceinline__ void ring_refill(Chain& c, uint32_t ring_base) {
     if (c.mode <= 1 && ring_avail(c) < 96u) {
@@ -141,6 +181,20 @@ __device__ __forceinline__ void ring_refill(Chain& c, uint32_t ring_base) {
 
 // Generic (mixed-mode) step: returns the next weight byte of chain c.
 __device__ __forceinline__ uint32_t chain_step(Chain& c, const FmaK& k) {
+    if (kWindow) {
+        if (c.mode == 0) {
+            uint32_t sel = kSelBase;
+            const uint32_t e = dec_sym(c.x, sel, fwin_bytes(c), c.tab);
+            fwin_advance(c, sel);
+            return e;
+        }
+        if (c.mode == 1) {
+            const uint32_t e = fwin_bytes(c) & 0xFFu;
+            fwin_advance(c, kSelBase + 1);
+            return e;
+        }
+        return c.sym;
+    }
     if (c.mode == 0) return ring_step(c.x, c.pr, c.nb, c.tab, c.rb, k);
     if (c.mode == 1) {
         const uint32_t e = c.nb;
@@ -256,8 +310,9 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
             c.gfill = c.gstart & ~(uint64_t)15;
             c.rb = ring_base[u];
             c.pr = ring_base[u] + ((uint32_t)c.gstart & 127u);
-            if (c.mode <= 1) {  // prime the ring with 128 B
-                for (int k = 0; k < 8; ++k) {
+            if (c.mode <= 1) {  // prime the ring with 112 B: buffered bytes stay < 128, so
+                                // (gfill - read) & 127 never aliases a full ring to empty
+                for (int k = 0; k < 7; ++k) {
                     cp_async16(ring_base[u] + ((uint32_t)c.gfill & 127u), reinterpret_cast<const void*>(c.gfill));
                     c.gfill += 16;
                 }
@@ -265,8 +320,13 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
         }
         cp_async_commit();
         cp_async_wait<0>();
-        ch[0].nb = lds_u8(ch[0].pr);
-        ch[1].nb = lds_u8(ch[1].pr);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (kWindow)
+                fwin_init(ch[u], (uint32_t)ch[u].gstart & 127u);
+            else
+                ch[u].nb = lds_u8(ch[u].pr);
+        }
         __syncthreads();  // tables and X slice visible (generic and async proxies)
         const bool fast = __all_sync(0xffffffffu, ch[0].mode == 0 && ch[1].mode == 0);
 
@@ -276,7 +336,25 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 uint32_t w[2][4];
-                if (fast) {
+                if (fast && kWindow) {
+#pragma unroll
+                    for (int v = 0; v < 16; v += 2) {  // a step pair shares one window word
+                        uint32_t wv[2], sel[2], e0[2];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            wv[u] = fwin_bytes(ch[u]);
+                            sel[u] = kSelBase;
+                            e0[u] = dec_sym(ch[u].x, sel[u], wv[u], ch[u].tab);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const uint32_t t = __byte_perm(e0[u], dec_sym(ch[u].x, sel[u], wv[u], ch[u].tab), 0x0040);
+                            w[u][v >> 2] = (v & 2) ? __byte_perm(w[u][v >> 2], t, 0x5410) : t;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) fwin_advance(ch[u], sel[u]);
+                    }
+                } else if (fast) {
 #pragma unroll
                     for (int v = 0; v < 16; v += 2) {  // 3 PRMT per 4 output bytes
                         uint32_t e0[2];
@@ -339,7 +417,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
         for (int u = 0; u < 2; ++u) {
             const Chain& c = ch[u];
             if (c.mode == 0) {
-                const uint64_t pos = c.gfill - (uint64_t)(((uint32_t)c.gfill - c.pr) & 127u);
+                const uint64_t pos = c.gfill - (uint64_t)ring_avail(c);
                 if (c.x != c.xe || pos != c.gend) atomicExch(&status[c.chunk], DC_CHUNK_CHAIN);
             } else if (c.mode == 2 && (c.x != c.xe || c.gstart != c.gend)) {
                 atomicExch(&status[c.chunk], DC_CHUNK_CORRUPT);
