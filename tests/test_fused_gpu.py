@@ -90,3 +90,31 @@ def test_fused_ring_exact(cuda, ntok, stored, chunk):
     fr.run()  # re-run (ring / barrier phases carry over between launches)
     torch.cuda.synchronize()
     assert all(torch.equal(acc.cpu().long(), x.long() @ w.long().T) for w, x, acc in zip(ws, xs, fr.accs))
+
+
+def test_fused_ring_skewed_streams(cuda):
+    """Edge distributions: ~99.8% zeros (symbols that consume no stream byte
+    for many steps), an all-zero tensor (single-symbol table, empty stream)
+    and uniform bytes (incompressible -> stored chunk), in one launch."""
+    from paper_2502_15443_b200 import container
+    from paper_2502_15443_b200.gemm import FusedRing
+    g = torch.Generator().manual_seed(5)
+    dense = torch.randint(-128, 128, (2048, 2048), generator=g, dtype=torch.int8)  # 8 bits/byte: stored
+    sparse = torch.where(torch.rand(1024, 2048, generator=g) < 0.002, dense[:1024], torch.zeros_like(dense[:1024]))
+    ws = [sparse, torch.zeros(1024, 2048, dtype=torch.int8), dense, torch.zeros(2048, 2048, dtype=torch.int8),
+          sparse[:, :1024].contiguous()]
+    shapes = [tuple(w.shape) for w in ws]
+    ntok = 3
+    xs = [torch.randint(-127, 128, (ntok, k), generator=g, dtype=torch.int8) for _, k in shapes]
+    payload = torch.cat([w.reshape(-1).view(torch.uint8) for w in ws]).cuda()
+    t_offs = np.concatenate([[0], np.cumsum([w.numel() for w in ws])[:-1]])
+    chunk = 1 << 22
+    image, enc, entries = container.pack_device(payload, b"\x00" * 8, chunk, None, seg_shift=8)
+    assert list(entries["codec"]) == [1, 0, 1, 1]  # ANS, stored (dense), single-symbol ANS, ANS
+    jobs = container.jobs_for(entries, image.device)
+    fr = FusedRing(image, jobs, enc.index, chunk, shapes, t_offs, [x.cuda() for x in xs], ntok)
+    fr.run()
+    torch.cuda.synchronize()
+    assert (fr.check() == 0).all()
+    for w, x, acc in zip(ws, xs, fr.accs):
+        assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
