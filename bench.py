@@ -338,6 +338,30 @@ def main():
                            "int8_weight_gbs": raw / (t_i8 / 1e3) / 1e9}
         del gi, gd, fc
 
+    # GPU_CPU tier: weights in pinned host memory streamed over
+    # PCIe every step, raw INT8 vs the compressed container + on-GPU decode,
+    # each followed by the grouped W8A8 GEMM; with the planner's prediction
+    streaming_tier = None
+    try:
+        import importlib
+        from paper_2502_15443_b200 import adaptive, streaming
+        latency = importlib.import_module("paper_2502_15443_b200.latency")  # the package re-exports a function of that name
+        streaming_tier = streaming.measure(m.payload, m.shapes, offs, pm.image, pm.jobs, pm.index, ntok=1,
+                                           iters=5, groups=16)
+        h2d = adaptive.measure_h2d_gbs(1 << 28)
+        prof = latency.HardwareProfile(B_stoc=7.0, B_ctog=h2d, B_gpu=hbm, D_max=value, c_sat=1.0,
+                                       I_gpu=tokens["B1"]["int8_weight_gbs"], mem_gpu=1e12, mem_cpu=1e12)
+        n_ch = int(pm.jobs.n)
+        arch = latency.Architecture.GPU_CPU
+        none = latency.CompressionPlan.block_plan(args.chunk_size, n_ch, 0)
+        full = latency.CompressionPlan.block_plan(args.chunk_size, n_ch, 1)
+        streaming_tier.update({
+            "h2d_gbs": h2d,
+            "predicted_raw_ms": latency.latency(prof, none, arch).per_sample_latency * 1e3,
+            "predicted_compressed_ms": latency.latency(prof, full, arch, raw / comp).per_sample_latency * 1e3})
+    except Exception as e:  # report, never hide
+        streaming_tier = {"error": repr(e)[:300]}
+
     # config C5 under torchrun: LLaMA-13B-shaped tensor parallelism across
     # the ranks (fused compressed vs INT8 per rank + NCCL int32 all-reduce)
     tp = None
@@ -404,6 +428,7 @@ def main():
             "e2e": e2e,
             "decode_step_tokens": tokens,
             "tp_decode": tp,
+            "streaming_tier": streaming_tier,
             "gpu_launches": args.steps * (1 + int(has_store)),
             "clocks": clocks.summary(),
         }

@@ -1,0 +1,150 @@
+"""Host-resident weights streamed to the GPU every step (the reference's GPU_CPU
+tier, latency.py:33 and :140-146).
+
+The reference models a model too large for GPU memory: weights live in host
+memory and cross PCIe once per forward pass, so a compressed chunk costs
+S/cr on the link plus S/d_gpu(S) of decode, overlapped chunk by chunk
+(``latency()``: per chunk max(load, dec, compute)).  This module runs that
+pipeline for real on the B200:
+
+* ``StreamedCompressed``: the DCC1 image sits in pinned host memory; each
+  step copies chunk group g+1 over PCIe (copy stream) while group g is
+  validated and decoded by the split-point decoder (compute stream), then the
+  grouped tcgen05 W8A8 GEMM consumes the decoded weights.
+* ``StreamedRaw``: the baseline -- raw INT8 weights in pinned host memory,
+  copied every step, then the same GEMM.
+
+Both keep one device copy of their input as the landing buffer (the
+measurement is the per-step link + decode pipeline, which is what the
+planner's GPU_CPU latency models; a rolling buffer of a few chunk groups
+would bound device memory without changing the timing).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import engine
+from . import native as nv
+from .gemm import GroupedInt8
+
+
+def _group_bounds(sizes: np.ndarray, groups: int) -> list[tuple[int, int]]:
+    n = len(sizes)
+    cuts = np.searchsorted(np.cumsum(sizes.astype(np.float64)),
+                           np.linspace(0, float(sizes.sum()), groups + 1)[1:-1]).tolist()
+    b = sorted(set([0] + [min(max(int(c), 0), n) for c in cuts] + [n]))
+    return [(g0, g1) for g0, g1 in zip(b, b[1:]) if g1 > g0]
+
+
+class StreamedCompressed:
+    """Per-step PCIe streaming of a compressed container + on-GPU decode."""
+
+    def __init__(self, host_image: torch.Tensor, jobs: engine.JobTable, index: engine.SegmentIndex,
+                 groups: int = 16):
+        if not host_image.is_pinned():
+            raise ValueError("host_image must be pinned host memory")
+        self.host, self.jobs, self.index = host_image, jobs, index
+        dev = jobs.d_blob_off.device
+        self.dev = dev
+        self.image = nv.device_bytes(host_image.numel(), dev)
+        self.out = nv.device_bytes(jobs.total_out, dev)
+        self.status = torch.zeros(max(jobs.n, 1), dtype=torch.int32, device=dev)
+        self.tasks = index.tasks(jobs, np.ones(jobs.n, bool))
+        t_chunk = self.tasks[:, 0].cpu().numpy() if self.tasks.shape[0] else np.zeros(0, np.int32)
+        ends = jobs.blob_off + jobs.blob_len
+        self.groups = []
+        for g0, g1 in _group_bounds(jobs.blob_len, groups):
+            f0, f1 = int(jobs.blob_off[g0]), int(ends[g1 - 1])
+            t0, t1 = int(np.searchsorted(t_chunk, g0)), int(np.searchsorted(t_chunk, g1))
+            self.groups.append((g0, g1, f0, f1, t0, t1))
+        self.s_copy = torch.cuda.Stream(dev)
+        self.has_store = bool((jobs.codec == 0).any())
+        self.bytes_per_step = int(host_image.numel())
+
+    def step(self) -> None:
+        j, ix = self.jobs, self.index
+        s_comp = torch.cuda.current_stream(self.dev)
+        s_copy = self.s_copy
+        s_copy.wait_stream(s_comp)  # the previous step's decode is done reading the image
+        sp = s_comp.cuda_stream
+        for g0, g1, f0, f1, t0, t1 in self.groups:
+            with torch.cuda.stream(s_copy):
+                self.image[f0:f1].copy_(self.host[f0:f1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s_copy)
+            s_comp.wait_event(ev)
+            k = g1 - g0
+            off8 = lambda t: t.data_ptr() + 8 * g0  # noqa: E731
+            nv.call("dc_ans_validate", self.image.data_ptr(), off8(j.d_blob_off), off8(j.d_blob_len),
+                    off8(j.d_out_len), j.d_codec.data_ptr() + g0, k, self.status.data_ptr() + 4 * g0, sp)
+            if t1 > t0:
+                nv.call("dc_ans_decode_segments", self.image.data_ptr(), j.d_blob_off.data_ptr(),
+                        j.d_blob_len.data_ptr(), j.d_out_off.data_ptr(), j.d_out_len.data_ptr(), ix.seg_shift,
+                        ix.d_seg_base.data_ptr(), ix.d_state.data_ptr(), ix.d_off.data_ptr(),
+                        self.tasks[t0:t1].data_ptr(), t1 - t0, self.out.data_ptr(), self.status.data_ptr(), sp)
+            if self.has_store:
+                nv.call("dc_store_copy", self.image.data_ptr(), off8(j.d_blob_off), off8(j.d_out_off),
+                        off8(j.d_out_len), j.d_codec.data_ptr() + g0, k, self.out.data_ptr(), sp)
+
+    def check(self) -> np.ndarray:
+        return self.status[: self.jobs.n].cpu().numpy()
+
+
+class StreamedRaw:
+    """Baseline: raw INT8 weights in pinned host memory, copied every step."""
+
+    def __init__(self, host_weights: torch.Tensor, device, groups: int = 16):
+        if not host_weights.is_pinned():
+            raise ValueError("host_weights must be pinned host memory")
+        self.host = host_weights
+        self.out = torch.empty(host_weights.numel(), dtype=torch.uint8, device=device)
+        n = host_weights.numel()
+        step = -(-n // groups)
+        self.groups = [(a, min(n, a + step)) for a in range(0, n, step)]
+        self.bytes_per_step = int(n)
+
+    def step(self) -> None:
+        for a, b in self.groups:
+            self.out[a:b].copy_(self.host[a:b], non_blocking=True)
+
+
+def layer_views(buf: torch.Tensor, shapes, offs) -> list[torch.Tensor]:
+    return [buf[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, shapes)]
+
+
+def measure(model_payload: torch.Tensor, shapes, offs, image: torch.Tensor, jobs, index, ntok: int = 1,
+            iters: int = 5, groups: int = 16) -> dict:
+    """Per-step time of raw vs compressed host streaming, each followed by the
+    grouped W8A8 GEMM over every linear (CUDA events on the compute stream)."""
+    from .adaptive import time_ms
+    dev = model_payload.device
+    host_raw = torch.empty(model_payload.numel(), dtype=torch.uint8, pin_memory=True)
+    host_raw.copy_(model_payload)
+    host_img = torch.empty(image.numel(), dtype=torch.uint8, pin_memory=True)
+    host_img.copy_(image)
+    raw = StreamedRaw(host_raw, dev, groups)
+    comp = StreamedCompressed(host_img, jobs, index, groups)
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    xs = [torch.randint(-127, 128, (ntok, c), generator=g, device=dev, dtype=torch.int8) for _, c in shapes]
+    gemm_raw = GroupedInt8(layer_views(raw.out, shapes, offs), xs, ntok)
+    gemm_comp = GroupedInt8(layer_views(comp.out, shapes, offs), xs, ntok)
+    # correctness: the streamed, decoded weights are the model's weights
+    comp.step()
+    raw.step()
+    torch.cuda.synchronize()
+    if (comp.check() != 0).any() or not torch.equal(comp.out, model_payload) or not torch.equal(raw.out,
+                                                                                               model_payload):
+        raise RuntimeError("streamed weights differ from the model")
+    t_raw = time_ms(lambda: (raw.step(), gemm_raw.run()), iters)
+    t_comp = time_ms(lambda: (comp.step(), gemm_comp.run()), iters)
+    gemm_raw.run()
+    gemm_comp.run()
+    torch.cuda.synchronize()
+    same = all(torch.equal(a, b) for a, b in zip(gemm_raw.accs, gemm_comp.accs))
+    return {"raw_step_ms": t_raw, "compressed_step_ms": t_comp, "speedup": t_raw / t_comp,
+            "raw_h2d_bytes": raw.bytes_per_step, "compressed_h2d_bytes": comp.bytes_per_step,
+            "raw_tok_s": ntok / (t_raw / 1e3), "compressed_tok_s": ntok / (t_comp / 1e3), "ntok": ntok,
+            "groups": groups, "outputs_equal": same}
