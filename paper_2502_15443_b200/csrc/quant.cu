@@ -86,6 +86,21 @@ __device__ __forceinline__ int8_t q_of(double v, double w_scale) {
     return (int8_t)(int)sg;
 }
 
+// Same result as q_of without the IEEE division on the common path: x' = v * (1/w_scale)
+// is within 2 ulp of the correctly rounded quotient x (|x| <= 127.5 + ulp), so
+// floor(|x| + 0.5) and the clip can only differ from the exact ones when |x'| is
+// within 1e-9 of a half-integer; those (rare) elements take the exact division.
+__device__ __forceinline__ int8_t q_of_fast(double v, double w_scale, double inv) {
+    const double xa = __dmul_rn(v, inv);
+    const double a = fabs(xa);
+    const double h = a - floor(a);  // fractional part
+    if (fabs(h - 0.5) < 1e-9) return q_of(v, w_scale);
+    double r = floor(a + 0.5);
+    r = r > 127.0 ? 127.0 : r;
+    const double sg = xa < 0.0 ? -r : (xa > 0.0 ? r : 0.0);
+    return (int8_t)(int)sg;
+}
+
 // q[r, c] plus, optionally, the per-(column, |q|) histogram used by pruning
 // (counts[c * 129 + |q|], u32, must be zeroed).
 template <int T>
@@ -102,6 +117,140 @@ __global__ void __launch_bounds__(kQThreads) k_quantize(const typename In<T>::ty
             q[r * cols + c] = q_of(v, w_scale);
         }
     }
+}
+
+// ---- vectorized grid-stride variants (cols % 8 == 0, 16-B aligned input) --
+// A thread owns 8 consecutive elements of one row: 16-byte loads of W (4 for
+// f64, 2 for f32, 1 for bf16/f16) and of s, one 8-byte store of q.  Enough
+// CTAs to keep every SM's load queue full; HBM-bound.
+template <int T>
+__device__ __forceinline__ void load8(const typename In<T>::type* __restrict__ w, int64_t e, double (&v)[8]) {
+    if constexpr (T == kF64) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2 d = __ldg(reinterpret_cast<const double2*>(w + e) + k);
+            v[2 * k] = d.x;
+            v[2 * k + 1] = d.y;
+        }
+    } else if constexpr (T == kF32) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(w + e) + k);
+            v[4 * k] = f.x;
+            v[4 * k + 1] = f.y;
+            v[4 * k + 2] = f.z;
+            v[4 * k + 3] = f.w;
+        }
+    } else {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(w + e));
+        const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            typename In<T>::type lo, hi;
+            const uint16_t a = (uint16_t)(uw[k] & 0xFFFF), b = (uint16_t)(uw[k] >> 16);
+            memcpy(&lo, &a, 2);
+            memcpy(&hi, &b, 2);
+            v[2 * k] = In<T>::f64(lo);
+            v[2 * k + 1] = In<T>::f64(hi);
+        }
+    }
+}
+
+__device__ __forceinline__ void load_s8(const double* __restrict__ s, int64_t c, double (&sc)[8]) {
+    if (s) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2 d = __ldg(reinterpret_cast<const double2*>(s + c) + k);
+            sc[2 * k] = d.x;
+            sc[2 * k + 1] = d.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sc[k] = 1.0;
+    }
+}
+
+// Thread layout: t = rp * gpr + cg owns the 8 columns [8*cg, 8*cg+8) of rows
+// rp, rp + rows_par, ...; its 8 scales are loaded once.
+template <int T>
+__global__ void __launch_bounds__(kQThreads) k_absmax_v(const typename In<T>::type* __restrict__ w,
+                                                         const double* __restrict__ s, int64_t rows, int64_t cols,
+                                                         int64_t rows_par, unsigned long long* __restrict__ out,
+                                                         int* __restrict__ nonfinite) {
+    double m = 0.0;
+    bool bad = false;
+    const int64_t gpr = cols / 8, t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t cg = t % gpr, rp = t / gpr;
+    double sc[8];
+    load_s8(s, cg * 8, sc);
+    for (int64_t r = rp; r < rows && rp < rows_par; r += rows_par) {
+        const int64_t e = r * cols + cg * 8;
+        double v[8];
+        load8<T>(w, e, v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            bad |= !isfinite(v[k]);
+            const double a = fabs(__dmul_rn(v[k], sc[k]));
+            m = a > m ? a : m;
+        }
+    }
+    __shared__ double red[kQThreads / 32];
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, m, d);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    const int anybad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int i = 0; i < kQThreads / 32; ++i) b = red[i] > b ? red[i] : b;
+        atomicMax(out, (unsigned long long)__double_as_longlong(b));
+        if (anybad) atomicExch(nonfinite, 1);
+    }
+}
+
+template <int T>
+__global__ void __launch_bounds__(kQThreads) k_quantize_v(const typename In<T>::type* __restrict__ w,
+                                                           const double* __restrict__ s, int64_t rows, int64_t cols,
+                                                           int64_t rows_par, double w_scale, int8_t* __restrict__ q) {
+    const double inv = 1.0 / w_scale;
+    const int64_t gpr = cols / 8, t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t cg = t % gpr, rp = t / gpr;
+    double sc[8];
+    load_s8(s, cg * 8, sc);
+    for (int64_t r = rp; r < rows && rp < rows_par; r += rows_par) {
+        const int64_t e = r * cols + cg * 8;
+        double v[8];
+        load8<T>(w, e, v);
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t b = (uint8_t)q_of_fast(__dmul_rn(v[k], sc[k]), w_scale, inv);
+            if (k < 4)
+                lo |= b << (8 * k);
+            else
+                hi |= b << (8 * (k - 4));
+        }
+        *reinterpret_cast<uint2*>(q + e) = make_uint2(lo, hi);
+    }
+}
+
+static bool vec_ok(const void* w, const double* s, int64_t cols, const void* q) {
+    return cols % 8 == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0 && (reinterpret_cast<uintptr_t>(s) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(q) & 7) == 0;
+}
+
+// rows processed in parallel so that rows_par * (cols/8) threads ~ 8 CTAs per SM
+static void vec_shape(int64_t rows, int64_t cols, int64_t& rows_par, unsigned& grid) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t cap = (int64_t)sms * 8 * kQThreads, gpr = cols / 8;
+    rows_par = cap / gpr;
+    if (rows_par < 1) rows_par = 1;
+    if (rows_par > rows) rows_par = rows;
+    grid = (unsigned)((rows_par * gpr + kQThreads - 1) / kQThreads);
 }
 
 // v = q * w_scale / s[c]   (scaling.py:114-117, dequantize)
@@ -139,6 +288,19 @@ extern "C" int dc_quant_absmax(const void* w, int dtype, const double* s, int64_
     cudaMemsetAsync(absmax_bits, 0, sizeof(unsigned long long), st);
     cudaMemsetAsync(nonfinite, 0, sizeof(int), st);
     if (rows == 0 || cols == 0) return DC_OK;
+    if (vec_ok(w, s, cols, nullptr)) {
+        int64_t rp;
+        unsigned g;
+        vec_shape(rows, cols, rp, g);
+        switch (dtype) {
+            case kF64: k_absmax_v<kF64><<<g, kQThreads, 0, st>>>((const double*)w, s, rows, cols, rp, absmax_bits, nonfinite); break;
+            case kF32: k_absmax_v<kF32><<<g, kQThreads, 0, st>>>((const float*)w, s, rows, cols, rp, absmax_bits, nonfinite); break;
+            case kBF16: k_absmax_v<kBF16><<<g, kQThreads, 0, st>>>((const __nv_bfloat16*)w, s, rows, cols, rp, absmax_bits, nonfinite); break;
+            default: k_absmax_v<kF16><<<g, kQThreads, 0, st>>>((const __half*)w, s, rows, cols, rp, absmax_bits, nonfinite); break;
+        }
+        DC_CHECK_LAUNCH("k_absmax_v");
+        return DC_OK;
+    }
     const int64_t rp = rows_per(rows, cols);
     const unsigned grid = (unsigned)((rows + rp - 1) / rp);
     switch (dtype) {
@@ -156,6 +318,19 @@ extern "C" int dc_quantize(const void* w, int dtype, const double* s, int64_t ro
     if (rows < 0 || cols < 0 || dtype < 0 || dtype > 3 || !(w_scale > 0.0)) return DC_ERR_ARG;
     if (rows == 0 || cols == 0) return DC_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    if (vec_ok(w, s, cols, q)) {
+        int64_t rp;
+        unsigned g;
+        vec_shape(rows, cols, rp, g);
+        switch (dtype) {
+            case kF64: k_quantize_v<kF64><<<g, kQThreads, 0, st>>>((const double*)w, s, rows, cols, rp, w_scale, q); break;
+            case kF32: k_quantize_v<kF32><<<g, kQThreads, 0, st>>>((const float*)w, s, rows, cols, rp, w_scale, q); break;
+            case kBF16: k_quantize_v<kBF16><<<g, kQThreads, 0, st>>>((const __nv_bfloat16*)w, s, rows, cols, rp, w_scale, q); break;
+            default: k_quantize_v<kF16><<<g, kQThreads, 0, st>>>((const __half*)w, s, rows, cols, rp, w_scale, q); break;
+        }
+        DC_CHECK_LAUNCH("k_quantize_v");
+        return DC_OK;
+    }
     const int64_t rp = rows_per(rows, cols);
     const unsigned grid = (unsigned)((rows + rp - 1) / rp);
     switch (dtype) {
