@@ -164,7 +164,316 @@ __global__ void __launch_bounds__(kPrThreads) k_apply(const int8_t* __restrict__
     }
 }
 
+__global__ void k_sel_init(SelectState* st, unsigned long long k) {
+    st->prefix = 0;
+    st->k = k;
+    st->below = 0;
+}
+
+// ------------------------------------------------- per tensor, fast path
+// (column, |q|) histogram: CTA = 64 columns x a row range, u32 bins in
+// shared memory (thread = column x row phase, coalesced byte loads), partial
+// histograms written whole (no global atomics) and summed by k_colhist_sum.
+constexpr int kHcCols = 64;
+
+__global__ void __launch_bounds__(kPrThreads) k_colhist2(const int8_t* __restrict__ q, int64_t rows, int64_t cols,
+                                                          int64_t rows_per, uint32_t* __restrict__ partial) {
+    __shared__ uint32_t bins[kHcCols * kBins];
+    for (int i = threadIdx.x; i < kHcCols * kBins; i += blockDim.x) bins[i] = 0;
+    __syncthreads();
+    const int cl = threadIdx.x % kHcCols, rph = threadIdx.x / kHcCols;  // 4 row phases
+    const int64_t c = (int64_t)blockIdx.y * kHcCols + cl;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(rows, r0 + rows_per);
+    if (c < cols)
+        for (int64_t r = r0 + rph; r < r1; r += kPrThreads / kHcCols) atomicAdd(&bins[cl * kBins + absq(q[r * cols + c])], 1u);
+    __syncthreads();
+    uint32_t* out = partial + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * (kHcCols * kBins);
+    for (int i = threadIdx.x; i < kHcCols * kBins; i += blockDim.x) out[i] = bins[i];
+}
+
+// counts[c * 129 + a] = sum over row blocks of the partials
+__global__ void k_colhist_sum(const uint32_t* __restrict__ partial, int64_t n_rb, int64_t n_cb, int64_t cols,
+                              uint32_t* __restrict__ counts) {
+    const int64_t per_rb = n_cb * kHcCols * kBins;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols * kBins;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t s = 0;
+        for (int64_t rb = 0; rb < n_rb; ++rb) s += partial[rb * per_rb + i];
+        counts[i] = s;
+    }
+}
+
+// single CTA: find the 16-bit digit bucket holding rank st->k.  Coalesced
+// 1024-bin tiles -> 2048 partial sums of 32 bins -> block scan -> one warp
+// resolves the bin inside its 32.
+__global__ void __launch_bounds__(1024) k_select_pick2(const unsigned long long* __restrict__ hist,
+                                                       SelectState* __restrict__ st) {
+    __shared__ unsigned long long part[2048];
+    __shared__ unsigned long long wsum[32];
+    __shared__ int s_part;
+    __shared__ unsigned long long s_base;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    for (int i = 0; i < 64; ++i) {
+        unsigned long long v = hist[i * 1024 + t];
+#pragma unroll
+        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        if (lane == 0) part[i * 32 + w] = v;
+    }
+    __syncthreads();
+    const unsigned long long a = part[2 * t], b = part[2 * t + 1], s = a + b;
+    unsigned long long inc = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long v = wsum[lane], x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long o = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += o;
+        }
+        wsum[lane] = x - v;  // exclusive
+    }
+    __syncthreads();
+    inc += wsum[w];
+    const unsigned long long k = st->k, excl = inc - s;
+    if (excl < k && k <= inc) {  // exactly one thread owns the rank
+        const bool first = k <= excl + a;
+        s_part = 2 * t + (first ? 0 : 1);
+        s_base = first ? excl : excl + a;
+    }
+    __syncthreads();
+    if (w == 0) {  // resolve inside the 32 bins of partial s_part
+        const int bin0 = s_part * 32;
+        const unsigned long long v = hist[bin0 + lane];
+        unsigned long long x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long o = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += o;
+        }
+        const unsigned long long lo = s_base + x - v, hi = s_base + x;
+        if (lo < k && k <= hi) {
+            st->prefix = (st->prefix << 16) | (unsigned long long)(bin0 + lane);
+            st->k = k - lo;
+            st->below += lo;
+        }
+    }
+}
+
+// per column: |q| < lo -> score < T; lo <= |q| < hi -> score == T (cm >= 0, so
+// the score is non-decreasing in |q|; strictly increasing when cm > 0)
+__global__ void k_col_bounds(const double* __restrict__ cm, int64_t cols, const SelectState* __restrict__ st,
+                             uint8_t* __restrict__ lo, uint8_t* __restrict__ hi) {
+    const unsigned long long T = st->prefix;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
+        int l = 0, h;
+        while (l < kBins && key_of(cm[c], l) < T) ++l;
+        h = l;
+        while (h < kBins && key_of(cm[c], h) == T) ++h;
+        lo[c] = (uint8_t)l;
+        hi[c] = (uint8_t)h;
+    }
+}
+
+// 16 consecutive elements per thread (one 4096-element block per CTA):
+// lt / eq flags from the column bounds, no f64 work per element
+__device__ __forceinline__ void flags16(const int8_t* __restrict__ q, const uint8_t* __restrict__ lo,
+                                        const uint8_t* __restrict__ hi, int64_t n, int64_t cols, int64_t i0,
+                                        bool vec, int8_t (&v)[16], uint32_t& ltm, uint32_t& eqm) {
+    ltm = eqm = 0;
+    if (vec && i0 + 16 <= n) {  // cols % 16 == 0: one row, 16-B aligned
+        const int64_t c0 = i0 % cols;
+        const uint4 qv = *reinterpret_cast<const uint4*>(q + i0);
+        const uint4 lv = *reinterpret_cast<const uint4*>(lo + c0);
+        const uint4 hv = *reinterpret_cast<const uint4*>(hi + c0);
+        memcpy(v, &qv, 16);
+        uint8_t l8[16], h8[16];
+        memcpy(l8, &lv, 16);
+        memcpy(h8, &hv, 16);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int a = absq(v[k]);
+            ltm |= (uint32_t)(a < l8[k]) << k;
+            eqm |= (uint32_t)(a >= l8[k] && a < h8[k]) << k;
+        }
+        return;
+    }
+    int64_t c = i0 % cols;
+    for (int k = 0; k < 16; ++k) {
+        const int64_t i = i0 + k;
+        v[k] = 0;
+        if (i < n) {
+            v[k] = q[i];
+            const int a = absq(v[k]);
+            ltm |= (uint32_t)(a < lo[c]) << k;
+            eqm |= (uint32_t)(a >= lo[c] && a < hi[c]) << k;
+        }
+        if (++c == cols) c = 0;
+    }
+}
+
+__global__ void __launch_bounds__(kPrThreads) k_eq_count2(const int8_t* __restrict__ q, const uint8_t* __restrict__ lo,
+                                                           const uint8_t* __restrict__ hi, int64_t n, int64_t cols,
+                                                           bool vec, uint32_t* __restrict__ blk_cnt) {
+    int8_t v[16];
+    uint32_t ltm, eqm;
+    flags16(q, lo, hi, n, cols, (int64_t)blockIdx.x * kEqBlock + threadIdx.x * 16, vec, v, ltm, eqm);
+    uint32_t cnt = __popc(eqm);
+    __shared__ uint32_t red[kPrThreads / 32];
+#pragma unroll
+    for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int w = 0; w < kPrThreads / 32; ++w) s += red[w];
+        blk_cnt[blockIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kPrThreads) k_apply2(const int8_t* __restrict__ q, const uint8_t* __restrict__ lo,
+                                                        const uint8_t* __restrict__ hi, int64_t n, int64_t cols,
+                                                        bool vec, const SelectState* __restrict__ st,
+                                                        const uint32_t* __restrict__ blk_prefix,
+                                                        int8_t* __restrict__ out) {
+    const unsigned long long r = st->k;
+    const int64_t i0 = (int64_t)blockIdx.x * kEqBlock + threadIdx.x * 16;
+    int8_t v[16];
+    uint32_t ltm, eqm;
+    flags16(q, lo, hi, n, cols, i0, vec, v, ltm, eqm);
+    // block-exclusive scan of per-thread tie counts (row-major order)
+    const uint32_t cnt = __popc(eqm);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    __shared__ uint32_t ws[kPrThreads / 32];
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int k = 0; k < w; ++k) before += ws[k];
+    unsigned long long rank = (unsigned long long)blk_prefix[blockIdx.x] + before + inc - cnt;
+    uint32_t zero = ltm;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if ((eqm >> k) & 1) {
+            if (rank < r) zero |= 1u << k;
+            ++rank;
+        }
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if ((zero >> k) & 1) v[k] = 0;
+    if (vec && i0 + 16 <= n) {
+        uint4 o;
+        memcpy(&o, v, 16);
+        *reinterpret_cast<uint4*>(out + i0) = o;
+    } else {
+        for (int k = 0; k < 16; ++k)
+            if (i0 + k < n) out[i0 + k] = v[k];
+    }
+}
+
 // ---------------------------------------------------------------- per row
+// Register path (cols <= 4096): a CTA per row, 16 columns per thread, keys
+// computed once; 8 x 8-bit radix passes over a shared 256-bin histogram with a
+// block-scan bucket pick; then the ordered tie pass.
+constexpr int kRowMax = kPrThreads * 16;
+
+__device__ __forceinline__ void block_pick256(const uint32_t* hist, unsigned long long& prefix, unsigned long long& kk,
+                                              unsigned long long* s_prefix, unsigned long long* s_k,
+                                              uint32_t* wsum) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const uint32_t v = hist[t];
+    uint32_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int i = 0; i < w; ++i) before += wsum[i];
+    inc += before;
+    const unsigned long long lo = inc - v;
+    if (lo < kk && kk <= (unsigned long long)inc) {
+        *s_prefix = (prefix << 8) | (unsigned long long)t;
+        *s_k = kk - lo;
+    }
+    __syncthreads();
+    prefix = *s_prefix;
+    kk = *s_k;
+}
+
+__global__ void __launch_bounds__(kPrThreads) k_prune_rows2(const int8_t* __restrict__ q, const double* __restrict__ cm,
+                                                             int64_t cols, int64_t k, int8_t* __restrict__ out) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t wsum[kPrThreads / 32];
+    __shared__ unsigned long long s_prefix, s_k;
+    const int t = threadIdx.x;
+    const int8_t* qr = q + (int64_t)blockIdx.x * cols;
+    int8_t* orow = out + (int64_t)blockIdx.x * cols;
+    const int c0 = t * 16;
+    int8_t v[16];
+    unsigned long long key[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int c = c0 + j;
+        v[j] = c < cols ? qr[c] : 0;
+        key[j] = c < cols ? key_of(cm[c], absq(v[j])) : ~0ull;
+    }
+    unsigned long long prefix = 0, kk = (unsigned long long)k;
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        hist[t] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (c0 + j < cols && (pass == 0 || (key[j] >> (shift + 8)) == prefix))
+                atomicAdd(&hist[(key[j] >> shift) & 0xFF], 1u);
+        __syncthreads();
+        block_pick256(hist, prefix, kk, &s_prefix, &s_k, wsum);
+    }
+    // ordered ties: zero key < T, and the first kk entries with key == T
+    const unsigned long long T = prefix;
+    uint32_t eqm = 0, ltm = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        eqm |= (uint32_t)(c0 + j < cols && key[j] == T) << j;
+        ltm |= (uint32_t)(key[j] < T) << j;
+    }
+    const uint32_t cnt = __popc(eqm);
+    const int lane = t & 31, w = t >> 5;
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    __syncthreads();
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int i = 0; i < w; ++i) before += wsum[i];
+    unsigned long long rank = before + inc - cnt;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if ((eqm >> j) & 1) {
+            if (rank < kk) ltm |= 1u << j;
+            ++rank;
+        }
+        if (c0 + j < cols) orow[c0 + j] = ((ltm >> j) & 1) ? (int8_t)0 : v[j];
+    }
+}
+
 __global__ void __launch_bounds__(kPrThreads) k_prune_rows(const int8_t* __restrict__ q, const double* __restrict__ cm,
                                                             int64_t cols, int64_t k, int8_t* __restrict__ out) {
     __shared__ uint32_t hist[256];
@@ -238,7 +547,9 @@ using namespace dc;
 // Per-tensor prune.  scratch: >= 8*65536 + 64 + 4*ceil(n/4096) + 4*cols*129 bytes.
 extern "C" int dc_prune_scratch_bytes(int64_t rows, int64_t cols, uint64_t* out) {
     const int64_t n = rows * cols;
-    *out = 8ull * 65536 + 64 + 4ull * (uint64_t)((n + kEqBlock - 1) / kEqBlock) + 4ull * (uint64_t)cols * kBins + 256;
+    const uint64_t n_cb = (uint64_t)((cols + kHcCols - 1) / kHcCols);
+    *out = 8ull * 65536 + 64 + 4ull * (uint64_t)((n + kEqBlock - 1) / kEqBlock) + 4ull * (uint64_t)cols * kBins + 256 +
+           2ull * (uint64_t)cols + 256 + 4ull * kHcCols * kBins * n_cb * 16 + 256;
     return DC_OK;
 }
 
@@ -267,32 +578,45 @@ extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, 
     p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255);
     auto* counts = reinterpret_cast<uint32_t*>(p);
 
-    cudaMemsetAsync(counts, 0, 4ull * cols * kBins, st);
-    SelectState init{0ull, (unsigned long long)k, 0ull};
-    cudaMemcpyAsync(sel, &init, sizeof(init), cudaMemcpyHostToDevice, st);
-    const int64_t rp = rows < 4096 ? rows : 4096;  // u16 private bins
-    dim3 g1((unsigned)((rows + rp - 1) / rp), (unsigned)((cols + kPrThreads - 1) / kPrThreads));
-    const int smem = kPrThreads * 130 * 2;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_colhist, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
-    k_colhist<<<g1, kPrThreads, smem, st>>>(q, rows, cols, rp, counts);
-    DC_CHECK_LAUNCH("k_colhist");
+    p += 4ull * cols * kBins;
+    p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255);
+    uint8_t* lo = p;
+    uint8_t* hi = p + cols;
+    p += 2ull * cols;
+    p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255);
+    auto* partial = reinterpret_cast<uint32_t*>(p);
+
+    k_sel_init<<<1, 1, 0, st>>>(sel, (unsigned long long)k);  // (a pageable H2D copy would synchronize)
+    DC_CHECK_LAUNCH("k_sel_init");
+    // (column, |q|) histogram: <= 16 row blocks, ~4 CTAs per SM
+    const int64_t n_cb = (cols + kHcCols - 1) / kHcCols;
+    int64_t n_rb = (4 * 148 + n_cb - 1) / n_cb;
+    n_rb = n_rb < 1 ? 1 : (n_rb > 16 ? 16 : n_rb);
+    if (n_rb > rows) n_rb = rows;
+    const int64_t rows_per = (rows + n_rb - 1) / n_rb;
+    n_rb = (rows + rows_per - 1) / rows_per;
+    k_colhist2<<<dim3((unsigned)n_rb, (unsigned)n_cb), kPrThreads, 0, st>>>(q, rows, cols, rows_per, partial);
+    DC_CHECK_LAUNCH("k_colhist2");
+    k_colhist_sum<<<(unsigned)((cols * kBins + 255) / 256 < 1184 ? (cols * kBins + 255) / 256 : 1184), 256, 0, st>>>(partial, n_rb, n_cb, cols,
+                                                                                          counts);
+    DC_CHECK_LAUNCH("k_colhist_sum");
     for (int pass = 0; pass < 4; ++pass) {
         cudaMemsetAsync(hist, 0, 8ull * 65536, st);
         k_select_hist<<<592, 256, 0, st>>>(counts, cm, cols, 48 - 16 * pass, sel, hist);
         DC_CHECK_LAUNCH("k_select_hist");
-        k_select_pick<<<1, 1024, 0, st>>>(hist, sel);
-        DC_CHECK_LAUNCH("k_select_pick");
+        k_select_pick2<<<1, 1024, 0, st>>>(hist, sel);
+        DC_CHECK_LAUNCH("k_select_pick2");
     }
-    k_eq_count<<<(unsigned)nblk, kPrThreads, 0, st>>>(q, cm, n, cols, sel, blk);
-    DC_CHECK_LAUNCH("k_eq_count");
+    k_col_bounds<<<(unsigned)((cols + 255) / 256 < 1184 ? (cols + 255) / 256 : 1184), 256, 0, st>>>(cm, cols, sel, lo, hi);
+    DC_CHECK_LAUNCH("k_col_bounds");
+    const bool vec = cols % 16 == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    k_eq_count2<<<(unsigned)nblk, kPrThreads, 0, st>>>(q, lo, hi, n, cols, vec, blk);
+    DC_CHECK_LAUNCH("k_eq_count2");
     k_excl_scan<<<1, 1024, 0, st>>>(blk, nblk);
     DC_CHECK_LAUNCH("k_excl_scan");
-    k_apply<<<(unsigned)nblk, kPrThreads, 0, st>>>(q, cm, n, cols, sel, blk, out);
-    DC_CHECK_LAUNCH("k_apply");
+    k_apply2<<<(unsigned)nblk, kPrThreads, 0, st>>>(q, lo, hi, n, cols, vec, sel, blk, out);
+    DC_CHECK_LAUNCH("k_apply2");
     return DC_OK;
 }
 
@@ -300,6 +624,11 @@ extern "C" int dc_prune_rows(const int8_t* q, const double* cm, int64_t rows, in
                              void* stream) {
     if (rows < 0 || cols < 0 || k < 0 || k > cols) return DC_ERR_ARG;
     if (rows == 0 || cols == 0) return DC_OK;
+    if (k > 0 && cols <= kRowMax) {
+        k_prune_rows2<<<(unsigned)rows, kPrThreads, 0, (cudaStream_t)stream>>>(q, cm, cols, k, out);
+        DC_CHECK_LAUNCH("k_prune_rows2");
+        return DC_OK;
+    }
     k_prune_rows<<<(unsigned)rows, kPrThreads, 0, (cudaStream_t)stream>>>(q, cm, cols, k, out);
     DC_CHECK_LAUNCH("k_prune_rows");
     return DC_OK;
