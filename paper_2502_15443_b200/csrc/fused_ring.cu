@@ -344,11 +344,12 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
                         for (int u = 0; u < 2; ++u) {
                             wv[u] = fwin_bytes(ch[u]);
                             sel[u] = kSelBase;
-                            e0[u] = dec_sym(ch[u].x, sel[u], wv[u], ch[u].tab);
+                            e0[u] = dec_sym_fa(ch[u].x, sel[u], wv[u], ch[u].tab - (1u << 26), fk);
                         }
 #pragma unroll
                         for (int u = 0; u < 2; ++u) {
-                            const uint32_t t = __byte_perm(e0[u], dec_sym(ch[u].x, sel[u], wv[u], ch[u].tab), 0x0040);
+                            const uint32_t t = __byte_perm(
+                                e0[u], dec_sym_fa(ch[u].x, sel[u], wv[u], ch[u].tab - (1u << 26), fk), 0x0040);
                             w[u][v >> 2] = (v & 2) ? __byte_perm(w[u][v >> 2], t, 0x5410) : t;
                         }
 #pragma unroll

@@ -172,6 +172,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
                                             bool out_aligned, int32_t* st, const FmaK& fk) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tab = smem_u32(tab_ptr), stage = smem_u32(stage_ptr);
+    const uint32_t tabm = tab - (1u << 26);
     const uint32_t K = 1u << seg_shift;
     const int G = (int)(K >> 4);
     uint32_t x[NU], n[NU];
@@ -210,11 +211,11 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
                 }
                 uint32_t e0[NU];
 #pragma unroll
-                for (int u = 0; u < NU; ++u) e0[u] = dec_sym(x[u], sel[u], wv[u], tab, fk);
+                for (int u = 0; u < NU; ++u) e0[u] = dec_sym_fa(x[u], sel[u], wv[u], tabm, fk);
 #pragma unroll
                 for (int u = 0; u < NU; ++u) {
                     // two symbols -> bytes 0,1 of t; two pairs -> one word (3 PRMT per 4 bytes)
-                    const uint32_t t = __byte_perm(e0[u], dec_sym(x[u], sel[u], wv[u], tab, fk), 0x0040);
+                    const uint32_t t = __byte_perm(e0[u], dec_sym_fa(x[u], sel[u], wv[u], tabm, fk), 0x0040);
                     w[u][v >> 2] = (v & 2) ? __byte_perm(w[u][v >> 2], t, 0x5410) : t;
                 }
 #pragma unroll
