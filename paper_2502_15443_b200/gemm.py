@@ -183,8 +183,12 @@ class FusedCompressed:
 
 class FusedRing(FusedCompressed):
     """Fused decode -> TMEM ring -> tcgen05 W8A8 (csrc/fused_ring.cu): one
-    persistent 17-warp CTA per SM, 1024 decode chains feeding the tensor core
-    every 32 symbols.  Items: 1024 rows x K-slice (<= 2048 bytes)."""
+    persistent 16-warp CTA per SM, 1024 decode chains feeding the tensor core
+    every 32 symbols.  Items: 1024 rows x K-slice (<= 2048 bytes).
+
+    ``run()`` trusts the split-point index and reports broken chains through
+    ``check()``; ``run_checked()`` verifies and, if any chain broke (stale or
+    corrupt index), recomputes the outputs exactly from the container."""
 
     def __init__(self, image: torch.Tensor, jobs, index, chunk_size: int, shapes, t_offs, xs, ntok: int):
         if index is None or index.seg_shift != 8:
@@ -197,6 +201,7 @@ class FusedRing(FusedCompressed):
             if (rows_per - 1) * k + kmax > chunk_size:
                 raise ValueError("chunk too small for the fused path (1024 rows x K must fit in one chunk)")
         self.image, self.jobs, self.index, self.chunk_size = image, jobs, index, chunk_size
+        self.t_offs = [int(t) for t in t_offs]
         self.layers = _LayerSet(shapes, t_offs, xs, ntok)
         items = []
         for li, (r, k) in enumerate(self.layers.shapes):
@@ -213,8 +218,29 @@ class FusedRing(FusedCompressed):
 
     def run(self) -> None:
         self.layers.acc_flat.zero_()
+        self.status.zero_()
         j, ix = self.jobs, self.index
         nv.call("dc_fused_ring_gemm", self.image.data_ptr(), j.d_blob_off.data_ptr(), j.d_blob_len.data_ptr(),
                 j.d_out_len.data_ptr(), j.d_codec.data_ptr(), self.chunk_size, ix.d_seg_base.data_ptr(),
                 ix.d_state.data_ptr(), ix.d_off.data_ptr(), self.layers.tens.data_ptr(), self.unit_t.data_ptr(),
                 self.unit_t.shape[0], self.layers.ntok, self.status.data_ptr(), nv.stream_ptr())
+
+    def run_checked(self) -> bool:
+        """run(), verify every chain (one host sync) and fall back to the exact
+        path -- container decode with serial re-decode of broken chunks, then
+        the INT8 GEMM -- if any split point did not hold.  Returns True when
+        the fused result stood."""
+        from . import engine
+        from .errors import CorruptStreamError
+        self.run()
+        if not (self.check() != 0).any():
+            return True
+        res = engine.decode_jobs(self.image, self.jobs, self.index)
+        bad = np.nonzero(res.status != 0)[0]
+        if len(bad):
+            raise CorruptStreamError(f"corrupt stream (chunk {int(bad[0])})")
+        views = [res.out[t:t + r * k].view(torch.int8).view(r, k) for (r, k), t in zip(self.layers.shapes, self.t_offs)]
+        gi = GroupedInt8(views, self.layers.xs, self.layers.ntok)
+        gi.run()
+        self.layers.acc_flat.copy_(gi.layers.acc_flat)
+        return False

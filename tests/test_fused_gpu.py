@@ -118,3 +118,25 @@ def test_fused_ring_skewed_streams(cuda):
     assert (fr.check() == 0).all()
     for w, x, acc in zip(ws, xs, fr.accs):
         assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
+
+
+def test_fused_ring_checked_fallback(cuda):
+    """A corrupted split point never yields a wrong product: run_checked()
+    detects the broken chain and recomputes exactly."""
+    from paper_2502_15443_b200 import container
+    from paper_2502_15443_b200.gemm import FusedRing
+    g = torch.Generator().manual_seed(9)
+    shapes = [(1024, 1024), (2048, 512)]
+    ws = [torch.round(torch.randn(r, k, generator=g) * 9).clamp_(-127, 127).to(torch.int8) for r, k in shapes]
+    xs = [torch.randint(-127, 128, (2, k), generator=g, dtype=torch.int8) for _, k in shapes]
+    payload = torch.cat([w.reshape(-1).view(torch.uint8) for w in ws]).cuda()
+    t_offs = np.concatenate([[0], np.cumsum([w.numel() for w in ws])[:-1]])
+    chunk = 1 << 21
+    image, enc, entries = container.pack_device(payload, b"\x00" * 8, chunk, None, seg_shift=8)
+    jobs = container.jobs_for(entries, image.device)
+    fr = FusedRing(image, jobs, enc.index, chunk, shapes, t_offs, [x.cuda() for x in xs], 2)
+    assert fr.run_checked()
+    enc.index.d_state[40] ^= 0x5A5A  # corrupt one split point
+    assert not fr.run_checked()
+    for w, x, acc in zip(ws, xs, fr.accs):
+        assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
