@@ -356,6 +356,8 @@ def main():
     # each followed by the grouped W8A8 GEMM; with the planner's prediction
     streaming_tier = None
     try:
+        if world > 1:  # N ranks would share one host's PCIe links: single-GPU measurement only
+            raise RuntimeError("measured at N=1 only")
         import importlib
         from paper_2502_15443_b200 import adaptive, streaming
         latency = importlib.import_module("paper_2502_15443_b200.latency")  # the package re-exports a function of that name
@@ -373,7 +375,7 @@ def main():
             "predicted_raw_ms": latency.latency(prof, none, arch).per_sample_latency * 1e3,
             "predicted_compressed_ms": latency.latency(prof, full, arch, raw / comp).per_sample_latency * 1e3})
     except Exception as e:  # report, never hide
-        streaming_tier = {"error": repr(e)[:300]}
+        streaming_tier = {"skipped" if world > 1 else "error": repr(e)[:300]}
 
     # config C5 under torchrun: LLaMA-13B-shaped tensor parallelism across
     # the ranks (fused compressed vs INT8 per rank + NCCL int32 all-reduce)
