@@ -221,12 +221,12 @@ int dc_w8a8_grouped(const void *maps, const void *layers, const int32_t *units, 
  * replaces scaling.py:148-151 on weights decoded by ans.py:71-94. */
 int dc_fused_slice_bytes(void);
 
-/* TMEM-ring variant (the fast one): one persistent 17-warp CTA per SM; items
+/* TMEM-ring variant (the fast one): one persistent 16-warp CTA per SM; items
  * (layer, m0, k0, klen) of dc_fused_item_rows() rows x klen <= dc_fused_item_k()
- * bytes; 1024 decode chains write 16-byte groups into a 4-deep TMEM ring of
- * 32-byte K-steps that one MMA warp turns into tcgen05.mma (A from TMEM)
- * every 32 symbols.  Same layer table, index and status contract as
- * dc_fused_decode_gemm (multiples of 256 instead of 512). */
+ * bytes; 1024 decode chains write 16-byte groups into a 6-deep TMEM ring of
+ * 32-byte K-steps; the last warp to finish a K-step issues its tcgen05.mma
+ * (A from TMEM) for all 8 row tiles.  Same layer table, index and status
+ * contract as dc_fused_decode_gemm (multiples of 256 instead of 512). */
 int dc_fused_item_rows(void);
 int dc_fused_item_k(void);
 int dc_fused_ring_gemm(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
