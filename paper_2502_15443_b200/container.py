@@ -233,46 +233,89 @@ class _Cursor:
         return struct.unpack(f, self.take(struct.calcsize(f)))
 
 
+def _check_stats(names, sv, cv, lens, upto: int) -> None:
+    """Reference order (container.py:216-229): for tensor i < upto, first a
+    bad scale vector, then bad channel maxima; raise the earliest."""
+    if upto == 0:
+        return
+    n = int(lens[:upto].sum())
+    s_bad = (sv[:n] <= 0) | ~np.isfinite(sv[:n])
+    c_bad = (cv[:n] < 0) | ~np.isfinite(cv[:n])
+    if not (s_bad.any() or c_bad.any()):
+        return
+    ends = np.cumsum(lens[:upto])
+    first = lambda m: int(np.searchsorted(ends, int(np.argmax(m)), side="right")) if m.any() else upto  # noqa: E731
+    i_s, i_c = first(s_bad), first(c_bad)
+    if i_s <= i_c:
+        raise DataFormatError(f"{names[i_s]}: scale vector not positive finite")
+    raise DataFormatError(f"{names[i_c]}: channel maxima not finite non-negative")
+
+
 def _parse_header(header: bytes):
+    """Reference container.py:201-235.  One walk over the entries (no copies:
+    memoryview slices), then the per-channel checks of every s / cm vector in
+    one vectorized pass; errors keep the reference's order.  s / cm come back
+    as f32 views (the file's values); ScaleVector / ActivationStats widen them
+    to f64 exactly when the bundle is built (overlapped with the GPU in
+    unpack)."""
     if len(header) < 4:
         raise DataFormatError("header too small to hold its checksum")
-    body = header[:-4]
-    if zlib.crc32(body) != struct.unpack("<I", header[-4:])[0]:
+    mv = memoryview(header)
+    body = mv[:-4]
+    if zlib.crc32(body) != struct.unpack_from("<I", mv, len(mv) - 4)[0]:
         raise ChecksumError(-1, "header checksum mismatch")
     cur = _Cursor(body)
     chunk_size, count = cur.fmt("<II")
     if chunk_size < 1:
         raise DataFormatError("invalid chunk size 0")
-    directory = []
-    for _ in range(count):
-        (nl,) = cur.fmt("<H")
-        try:
-            name = cur.take(nl).decode("utf-8")
-        except UnicodeDecodeError as e:
-            raise DataFormatError(f"tensor name is not valid UTF-8: {e}") from None
-        rows, cols, w_scale, alpha = cur.fmt("<IIdd")
-        if rows < 1 or cols < 1:
-            raise DataFormatError(f"{name}: invalid dims {rows}x{cols}")
-        if not (np.isfinite(w_scale) and w_scale > 0):
-            raise DataFormatError(f"{name}: invalid w_scale {w_scale}")
-        s = np.frombuffer(cur.take(4 * cols), dtype="<f4").astype(np.float64)
-        cm = np.frombuffer(cur.take(4 * cols), dtype="<f4").astype(np.float64)
-        if (s <= 0).any() or not np.isfinite(s).all():
-            raise DataFormatError(f"{name}: scale vector not positive finite")
-        if (cm < 0).any() or not np.isfinite(cm).all():
-            raise DataFormatError(f"{name}: channel maxima not finite non-negative")
-        directory.append((name, rows, cols, w_scale, alpha, s, cm))
+    meta, s_parts, c_parts = [], [], []
+
+    def stats():
+        names = [m[0] for m in meta]
+        lens = np.array([m[2] for m in meta], dtype=np.int64)
+        sv = np.concatenate(s_parts) if s_parts else np.empty(0, np.float32)
+        cv = np.concatenate(c_parts) if c_parts else np.empty(0, np.float32)
+        return names, sv, cv, lens
+
+    try:
+        for _ in range(count):
+            (nl,) = cur.fmt("<H")
+            try:
+                name = bytes(cur.take(nl)).decode("utf-8")
+            except UnicodeDecodeError as e:
+                raise DataFormatError(f"tensor name is not valid UTF-8: {e}") from None
+            rows, cols, w_scale, alpha = cur.fmt("<IIdd")
+            if rows < 1 or cols < 1:
+                raise DataFormatError(f"{name}: invalid dims {rows}x{cols}")
+            if not (np.isfinite(w_scale) and w_scale > 0):
+                raise DataFormatError(f"{name}: invalid w_scale {w_scale}")
+            s_parts.append(np.frombuffer(cur.take(4 * cols), dtype="<f4"))
+            c_parts.append(np.frombuffer(cur.take(4 * cols), dtype="<f4"))
+            meta.append((name, rows, cols, w_scale, alpha))
+    except (DataFormatError, TruncatedError):
+        # an earlier tensor's stats error comes first in the reference's walk
+        names, sv, cv, lens = stats()
+        _check_stats(names, sv, cv, lens, len(meta))
+        raise
+    names, sv, cv, lens = stats()
+    _check_stats(names, sv, cv, lens, len(meta))
     if cur.pos != len(body):
         raise DataFormatError(f"{len(body) - cur.pos} stray bytes in header")
-    names = [d[0] for d in directory]
     if len(set(names)) != len(names):
         raise DataFormatError("duplicate tensor names in header")
+    directory, pos = [], 0
+    for name, rows, cols, w_scale, alpha in meta:
+        directory.append((name, rows, cols, w_scale, alpha, sv[pos:pos + cols], cv[pos:pos + cols]))
+        pos += cols
     return chunk_size, directory
 
 
-def _parse(data: bytes):
+def _parse(data: bytes, total: int | None = None):
     """Structure + chunk table validation (reference container.py:238-274),
-    vectorized over chunks with the reference's first-error order."""
+    vectorized over chunks with the reference's first-error order.  ``data``
+    may be just the file's prefix through the chunk table when ``total`` (the
+    file length) is given."""
+    total = len(data) if total is None else total
     cur = _Cursor(data)
     if cur.take(4) != MAGIC:
         raise BadMagicError("not a DCC1 container")
@@ -282,7 +325,7 @@ def _parse(data: bytes):
     (hlen,) = cur.fmt("<I")
     chunk_size, directory = _parse_header(cur.take(hlen))
     (count,) = cur.fmt("<I")
-    avail = (len(data) - cur.pos) // _ENTRY.size
+    avail = (total - cur.pos) // _ENTRY.size
     if avail < count:
         raise TruncatedError(f"truncated file at offset {cur.pos + avail * _ENTRY.size}")
     ent = np.frombuffer(data, dtype=ENTRY_DTYPE, count=count, offset=cur.pos)
@@ -323,10 +366,10 @@ def _parse(data: bytes):
         end = int(expected[-1]) + int(clen[-1])
     else:
         end = start
-    if end > len(data):
-        raise TruncatedError(f"chunk payloads extend past end of file ({end} > {len(data)})")
-    if end < len(data):
-        raise DataFormatError(f"{len(data) - end} trailing bytes after last chunk")
+    if end > total:
+        raise TruncatedError(f"chunk payloads extend past end of file ({end} > {total})")
+    if end < total:
+        raise DataFormatError(f"{total - end} trailing bytes after last chunk")
     total = int(ent["uncomp_len"].sum(dtype=np.uint64)) if count else 0
     want = sum(r * c for _, r, c, *_ in directory)
     if total != want:
@@ -335,10 +378,13 @@ def _parse(data: bytes):
 
 
 def binding_of(data: bytes) -> int:
-    """Ties a sidecar index to its container: CRC32 of the header + chunk table."""
+    """Ties a sidecar index to its container: CRC32 of the file prefix fields,
+    the header's own stored CRC32 (which fingerprints the whole header) and
+    the chunk table (offsets, lengths and per-chunk CRC32s) -- a few KB."""
     (hlen,) = struct.unpack_from("<I", data, 6)
     (count,) = struct.unpack_from("<I", data, 10 + hlen)
-    return zlib.crc32(memoryview(data)[: 14 + hlen + count * _ENTRY.size])
+    mv = memoryview(data)
+    return zlib.crc32(mv[6 + hlen: 14 + hlen + count * _ENTRY.size], zlib.crc32(mv[:10]))
 
 
 def _file_bytes(data) -> bytes:
@@ -412,10 +458,24 @@ def _bundle(directory, host: np.ndarray, chunk_size: int) -> ModelBundle:
     return ModelBundle(tensors=tensors, stats=stats, chunk_size=chunk_size)
 
 
+def _prefix(view: np.ndarray) -> bytes:
+    """The file's bytes through the end of the chunk table (header + table),
+    for parsing a container that lives in a pinned tensor."""
+    if view.size < 14:
+        return bytes(view)
+    (hlen,) = struct.unpack_from("<I", view, 6)
+    if 14 + hlen > view.size:
+        return bytes(view)
+    (count,) = struct.unpack_from("<I", view, 10 + hlen)
+    return bytes(view[: min(view.size, 14 + hlen + count * _ENTRY.size)])
+
+
 def unpack(data, index=None) -> ModelBundle:
     """Decode and verify a container (inverse of pack).  ``index`` (a
     SegmentIndex or sidecar bytes) enables the split-point parallel decoder;
-    without it each ANS chunk is decoded by one exact sequential walk."""
+    without it each ANS chunk is decoded by one exact sequential walk.
+    ``data`` (and a sidecar ``index``) may also be pinned CPU uint8 tensors:
+    the container is then copied to the GPU straight from that memory."""
     import time
     clock = [time.perf_counter()]
 
@@ -426,26 +486,38 @@ def unpack(data, index=None) -> ModelBundle:
         LAST_UNPACK_MS[name] = (now - clock[0]) * 1e3
         clock[0] = now
 
-    data = _file_bytes(data)
-    chunk_size, directory, ent, _ = _parse(data)
+    src = None
+    if isinstance(data, torch.Tensor):
+        if data.dtype != torch.uint8 or data.is_cuda or data.dim() != 1:
+            raise DcompError("container tensor must be a 1-D uint8 CPU tensor")
+        src = data if data.is_pinned() else None
+        view = data.numpy()
+        head, total = _prefix(view), view.size
+        data = view
+    else:
+        data = _file_bytes(data)
+        head, total = data, len(data)
+    LAST_UNPACK_MS.clear()
+    chunk_size, directory, ent, _ = _parse(head, total)
     if len(ent) == 0:
         return _bundle(directory, np.empty(0, np.uint8), chunk_size)
-    LAST_UNPACK_MS.clear()
     lap("parse")
     if index is not None:  # split-point path: H2D / decode / D2H pipelined per chunk group
         jobs = jobs_for(ent)
-        if isinstance(index, (bytes, bytearray, memoryview)):
-            index = engine.SegmentIndex.from_bytes(index, jobs, binding_of(data))
+        if isinstance(index, (bytes, bytearray, memoryview, torch.Tensor)):
+            index = engine.SegmentIndex.from_bytes(index, jobs, binding_of(head))
         lap("index")
         if index is not None:
-            host, status, crc = engine.decode_file_pipelined(np.frombuffer(data, np.uint8), jobs, index)
+            pd = engine.PipelinedDecode(src if src is not None else np.frombuffer(data, np.uint8), jobs, index)
+            lap("launch")
+            out = _bundle(directory, pd.host_out.numpy(), chunk_size)  # views; filled by the pipeline
+            lap("bundle")
+            _, status, crc = pd.finish()
             lap("pipeline")
             raise_decode_errors(status)
             bad = np.nonzero(crc != ent["crc32"])[0]
             if len(bad):
                 raise ChecksumError(int(bad[0]))
-            out = _bundle(directory, host, chunk_size)
-            lap("bundle")
             return out
     base = nv.to_device_bytes(data)
     lap("h2d")

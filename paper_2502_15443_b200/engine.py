@@ -122,9 +122,14 @@ class SegmentIndex:
         return head + body + struct.pack("<I", zlib.crc32(body))
 
     @classmethod
-    def from_bytes(cls, buf: bytes, jobs: JobTable, binding: int, device=None) -> "SegmentIndex | None":
-        """Load a sidecar; None if it does not belong to this container."""
-        if len(buf) < 26 or buf[:4] != cls.MAGIC:
+    def from_bytes(cls, buf, jobs: JobTable, binding: int, device=None) -> "SegmentIndex | None":
+        """Load a sidecar (bytes-like, or a pinned CPU uint8 tensor that is
+        copied to the device directly); None if it does not belong to this
+        container."""
+        src = None
+        if isinstance(buf, torch.Tensor):
+            src, buf = buf, buf.numpy()
+        if len(buf) < 26 or bytes(buf[:4]) != cls.MAGIC:
             return None
         ver, shift, bind, n = struct.unpack_from("<HIIQ", buf, 4)
         if ver != 1 or bind != binding or not 6 <= shift <= 10:
@@ -135,7 +140,11 @@ class SegmentIndex:
         if n != want or len(buf) != 22 + 8 * n + 4:
             return None
         dev = device or _dev()
-        d = nv.to_device_bytes(np.frombuffer(buf, np.uint8, 8 * n, 22), dev)  # pinned, pipelined upload
+        if src is not None and src.is_pinned():
+            d = nv.device_bytes(8 * n, dev)
+            d[:8 * n].copy_(src[22:22 + 8 * n], non_blocking=True)
+        else:
+            d = nv.to_device_bytes(np.frombuffer(buf, np.uint8, 8 * n, 22), dev)  # pinned, pipelined upload
         off = np.frombuffer(buf, np.uint32, n, 22 + 4 * n)
         return cls(shift, base, n, _t(base, torch.int64, dev), d[:4 * n].view(torch.int32),
                    d[4 * n:8 * n].view(torch.int32), h_off=off)
@@ -183,7 +192,8 @@ class SegmentIndex:
             hi = np.where(end < nsg, off[np.minimum(base + end, nmax)].astype(np.int64), plen)
         out = np.stack([chunk, s0, cnt, np.zeros_like(cnt)], axis=1).astype(np.int32)
         out = out[np.lexsort((out[:, 1], out[:, 0]))]
-        return torch.from_numpy(np.ascontiguousarray(out)).to(_dev())
+        self.last_tasks_host = np.ascontiguousarray(out)
+        return torch.from_numpy(self.last_tasks_host).to(_dev())
 
 
 # ------------------------------------------------------------------ decode
@@ -367,73 +377,95 @@ def _streams(dev):
     return _SIDE_STREAMS[dev]
 
 
-def decode_file_pipelined(data: np.ndarray, jobs: JobTable, index: SegmentIndex, groups: int = 16):
-    """Host container bytes -> host decoded bytes with H2D of chunk group g+1,
-    decode + CRC of group g and D2H of group g-1 overlapped on three streams.
+class PipelinedDecode:
+    """Host container bytes -> host decoded bytes: H2D of chunk group g+1,
+    validate + split-point decode + CRC of group g and D2H of group g-1
+    overlapped on three streams.  ``src`` is the file as a uint8 numpy array
+    (pageable: staged through pinned buffers) or a pinned CPU uint8 tensor
+    (copied directly).  The constructor only enqueues work; ``host_out`` may
+    be wrapped (views) before ``finish()``, which waits, re-decodes chunks
+    whose split-point chain broke (exact serial kernel) and returns
+    (decoded host bytes, per-chunk status, per-chunk CRC32)."""
 
-    Returns (pinned host uint8 array of all decoded bytes, per-chunk status,
-    per-chunk CRC32 of the decoded bytes).  Chunks whose split-point chain
-    breaks are re-decoded exactly (serial kernel) before returning."""
-    dev = jobs.d_blob_off.device
-    s_copy, s_out = _streams(dev)
-    s_comp = torch.cuda.current_stream(dev)
-    n = jobs.n
-    image = nv.device_bytes(data.size, dev)
-    out = nv.device_bytes(jobs.total_out, dev)
-    host_out = torch.empty(jobs.total_out, dtype=torch.uint8, pin_memory=True)
-    status = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
-    crc = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
-    tasks = index.tasks(jobs, np.ones(n, bool))
-    t_chunk = tasks[:, 0].cpu().numpy() if tasks.shape[0] else np.zeros(0, np.int32)
-    # contiguous chunk groups of ~equal file bytes
-    ends = jobs.blob_off + jobs.blob_len
-    cuts = np.searchsorted(np.cumsum(jobs.blob_len.astype(np.float64)),
-                           np.linspace(0, float(jobs.blob_len.sum()), groups + 1)[1:-1]).tolist()
-    bounds = sorted(set([0] + [min(max(c, 0), n) for c in cuts] + [n]))
-    sp_comp = s_comp.cuda_stream
-    max_len = int(jobs.out_len.max()) if n else 0
-    for g0, g1 in zip(bounds, bounds[1:]):
-        if g1 <= g0:
-            continue
-        f0, f1 = int(jobs.blob_off[g0]), int(ends[g1 - 1])
-        stage = torch.empty(f1 - f0, dtype=torch.uint8, pin_memory=True)
-        nv._parallel_copy(stage.numpy(), data[f0:f1], piece=8 << 20)
-        with torch.cuda.stream(s_copy):
-            image[f0:f1].copy_(stage, non_blocking=True)
-            ev_h2d = torch.cuda.Event()
-            ev_h2d.record(s_copy)
-        s_comp.wait_event(ev_h2d)
-        k = g1 - g0
-        off8 = lambda t: t.data_ptr() + 8 * g0  # noqa: E731
-        nv.call("dc_ans_validate", image.data_ptr(), off8(jobs.d_blob_off), off8(jobs.d_blob_len),
-                off8(jobs.d_out_len), jobs.d_codec.data_ptr() + g0, k, status.data_ptr() + 4 * g0, sp_comp)
-        t0, t1 = np.searchsorted(t_chunk, g0), np.searchsorted(t_chunk, g1)
-        if t1 > t0:
-            nv.call("dc_ans_decode_segments", image.data_ptr(), jobs.d_blob_off.data_ptr(), jobs.d_blob_len.data_ptr(),
-                    jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(), index.seg_shift,
-                    index.d_seg_base.data_ptr(), index.d_state.data_ptr(), index.d_off.data_ptr(),
-                    tasks[t0:t1].data_ptr(), int(t1 - t0), out.data_ptr(), status.data_ptr(), sp_comp)
-        nv.call("dc_store_copy", image.data_ptr(), off8(jobs.d_blob_off), off8(jobs.d_out_off), off8(jobs.d_out_len),
-                jobs.d_codec.data_ptr() + g0, k, out.data_ptr(), sp_comp)
-        nv.call("dc_crc32_ranges", out.data_ptr(), off8(jobs.d_out_off), off8(jobs.d_out_len), k, max_len,
-                crc.data_ptr() + 4 * g0, sp_comp)
-        ev_dec = torch.cuda.Event()
-        ev_dec.record(s_comp)
-        s_out.wait_event(ev_dec)
-        o0 = int(jobs.out_off[g0])
-        o1 = int(jobs.out_off[g1 - 1] + jobs.out_len[g1 - 1])
-        with torch.cuda.stream(s_out):
-            host_out[o0:o1].copy_(out[o0:o1], non_blocking=True)
-    torch.cuda.synchronize(dev)
-    st = status[:n].cpu().numpy()
-    redo = np.nonzero(st == nv.CHUNK_CHAIN)[0]
-    if len(redo):  # broken split points: exact serial decode, then refresh CRC + host bytes
-        decode_serial(image, jobs, redo, out, status, None)
-        nv.call("dc_crc32_ranges", out.data_ptr(), jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(), n, max_len,
-                crc.data_ptr(), sp_comp)
-        torch.cuda.synchronize(dev)
-        for c in redo:
-            a, b = int(jobs.out_off[c]), int(jobs.out_off[c] + jobs.out_len[c])
-            host_out[a:b].copy_(out[a:b])
-        st = status[:n].cpu().numpy()
-    return host_out.numpy(), st, crc[:n].cpu().numpy().view(np.uint32)
+    def __init__(self, src, jobs: JobTable, index: SegmentIndex, groups: int = 16):
+        dev = jobs.d_blob_off.device
+        self.dev, self.jobs = dev, jobs
+        s_copy, s_out = _streams(dev)
+        s_comp = torch.cuda.current_stream(dev)
+        self.s_comp = s_comp
+        n = jobs.n
+        pinned = isinstance(src, torch.Tensor)
+        size = src.numel() if pinned else src.size
+        self.image = image = nv.device_bytes(size, dev)
+        self.out = out = nv.device_bytes(jobs.total_out, dev)
+        self.host_out = host_out = torch.empty(jobs.total_out, dtype=torch.uint8, pin_memory=True)
+        self.status = status = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        self.crc = crc = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        tasks = index.tasks(jobs, np.ones(n, bool))
+        t_host = index.last_tasks_host
+        t_chunk = t_host[:, 0] if len(t_host) else np.zeros(0, np.int32)
+        # contiguous chunk groups of ~equal file bytes
+        ends = jobs.blob_off + jobs.blob_len
+        cuts = np.searchsorted(np.cumsum(jobs.blob_len.astype(np.float64)),
+                               np.linspace(0, float(jobs.blob_len.sum()), groups + 1)[1:-1]).tolist()
+        bounds = sorted(set([0] + [min(max(c, 0), n) for c in cuts] + [n]))
+        sp_comp = s_comp.cuda_stream
+        self.max_len = max_len = int(jobs.out_len.max()) if n else 0
+        self._keep = [tasks]
+        for g0, g1 in zip(bounds, bounds[1:]):
+            if g1 <= g0:
+                continue
+            f0, f1 = int(jobs.blob_off[g0]), int(ends[g1 - 1])
+            if pinned:
+                stage = src[f0:f1]
+            else:
+                stage = torch.empty(f1 - f0, dtype=torch.uint8, pin_memory=True)
+                nv._parallel_copy(stage.numpy(), src[f0:f1], piece=8 << 20)
+            with torch.cuda.stream(s_copy):
+                image[f0:f1].copy_(stage, non_blocking=True)
+                ev_h2d = torch.cuda.Event()
+                ev_h2d.record(s_copy)
+            s_comp.wait_event(ev_h2d)
+            k = g1 - g0
+            off8 = lambda t: t.data_ptr() + 8 * g0  # noqa: E731
+            nv.call("dc_ans_validate", image.data_ptr(), off8(jobs.d_blob_off), off8(jobs.d_blob_len),
+                    off8(jobs.d_out_len), jobs.d_codec.data_ptr() + g0, k, status.data_ptr() + 4 * g0, sp_comp)
+            t0, t1 = np.searchsorted(t_chunk, g0), np.searchsorted(t_chunk, g1)
+            if t1 > t0:
+                nv.call("dc_ans_decode_segments", image.data_ptr(), jobs.d_blob_off.data_ptr(),
+                        jobs.d_blob_len.data_ptr(), jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(),
+                        index.seg_shift, index.d_seg_base.data_ptr(), index.d_state.data_ptr(),
+                        index.d_off.data_ptr(), tasks[t0:t1].data_ptr(), int(t1 - t0), out.data_ptr(),
+                        status.data_ptr(), sp_comp)
+            nv.call("dc_store_copy", image.data_ptr(), off8(jobs.d_blob_off), off8(jobs.d_out_off),
+                    off8(jobs.d_out_len), jobs.d_codec.data_ptr() + g0, k, out.data_ptr(), sp_comp)
+            nv.call("dc_crc32_ranges", out.data_ptr(), off8(jobs.d_out_off), off8(jobs.d_out_len), k, max_len,
+                    crc.data_ptr() + 4 * g0, sp_comp)
+            ev_dec = torch.cuda.Event()
+            ev_dec.record(s_comp)
+            s_out.wait_event(ev_dec)
+            o0 = int(jobs.out_off[g0])
+            o1 = int(jobs.out_off[g1 - 1] + jobs.out_len[g1 - 1])
+            with torch.cuda.stream(s_out):
+                host_out[o0:o1].copy_(out[o0:o1], non_blocking=True)
+
+    def finish(self):
+        jobs, n, out, host_out = self.jobs, self.jobs.n, self.out, self.host_out
+        torch.cuda.synchronize(self.dev)
+        st = self.status[:n].cpu().numpy()
+        redo = np.nonzero(st == nv.CHUNK_CHAIN)[0]
+        if len(redo):  # broken split points: exact serial decode, then refresh CRC + host bytes
+            decode_serial(self.image, jobs, redo, out, self.status, None)
+            nv.call("dc_crc32_ranges", out.data_ptr(), jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(), n,
+                    self.max_len, self.crc.data_ptr(), self.s_comp.cuda_stream)
+            torch.cuda.synchronize(self.dev)
+            for c in redo:
+                a, b = int(jobs.out_off[c]), int(jobs.out_off[c] + jobs.out_len[c])
+                host_out[a:b].copy_(out[a:b])
+            st = self.status[:n].cpu().numpy()
+        return host_out.numpy(), st, self.crc[:n].cpu().numpy().view(np.uint32)
+
+
+def decode_file_pipelined(data, jobs: JobTable, index: SegmentIndex, groups: int = 16):
+    """One-shot PipelinedDecode (see there)."""
+    return PipelinedDecode(data, jobs, index, groups).finish()

@@ -93,6 +93,32 @@ def test_broken_index_falls_back_exactly(cuda):
     assert np.array_equal(cuda.unpack(data, index=index).tensors[0].qvalues, q)
 
 
+def test_unpack_from_pinned_tensors(cuda):
+    """unpack() straight from pinned host tensors (container + sidecar) gives the
+    bytes-input result; a corrupted pinned payload raises the same error."""
+    from paper_2502_15443_b200 import container
+    rng = np.random.default_rng(6)
+    ts, st = [], {}
+    for i, (r, c) in enumerate([(300, 1000), (128, 4096), (77, 513)]):
+        q = np.clip(np.round(rng.normal(0, 9, (r, c))), -127, 127).astype(np.int8)
+        ts.append(cuda.QuantizedTensor(f"w{i}", q, 0.01, cuda.ScaleVector.identity(c)))
+        st[f"w{i}"] = cuda.ActivationStats(f"w{i}", np.ones(c))
+    data, index = container.pack_indexed(ts, st, chunk_size=65536, seg_shift=8)
+    side = index.to_bytes(container.binding_of(data))
+    pin = torch.empty(len(data), dtype=torch.uint8, pin_memory=True)
+    pin.numpy()[:] = np.frombuffer(data, np.uint8)
+    pside = torch.empty(len(side), dtype=torch.uint8, pin_memory=True)
+    pside.numpy()[:] = np.frombuffer(side, np.uint8)
+    a = container.unpack(pin, index=pside)
+    b = container.unpack(data, index=side)
+    for x, y, t in zip(a.tensors, b.tensors, ts):
+        assert np.array_equal(x.qvalues, t.qvalues) and np.array_equal(y.qvalues, t.qvalues)
+    last = container._parse(data)[2][-1]
+    pin.numpy()[int(last["file_offset"]) + 500] ^= 0x40  # payload bit flip in the last chunk
+    with pytest.raises((cuda.CorruptStreamError, cuda.ChecksumError)):
+        container.unpack(pin, index=pside)
+
+
 def test_sidecar_roundtrip(cuda, tmp_path):
     rng = np.random.default_rng(5)
     q = np.clip(np.round(rng.normal(0, 9, (200, 1000))), -127, 127).astype(np.int8)

@@ -29,6 +29,18 @@ def main():
     host_file = pm.image.cpu().numpy().tobytes()
     side = pm.index.to_bytes(container.binding_of(host_file))
     raw = m.nbytes
+    import numpy as np
+    pin_file = torch.empty(len(host_file), dtype=torch.uint8, pin_memory=True)
+    pin_file.numpy()[:] = np.frombuffer(host_file, np.uint8)
+    pin_side = torch.empty(len(side), dtype=torch.uint8, pin_memory=True)
+    pin_side.numpy()[:] = np.frombuffer(side, np.uint8)
+    for i in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        container.unpack(pin_file, index=pin_side)
+        dt = time.perf_counter() - t0
+        print(f"pinned call {i}: {dt * 1e3:.1f} ms  {raw / dt / 1e9:.1f} GB/s  phases {container.LAST_UNPACK_MS}",
+              flush=True)
     for i in range(4):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
