@@ -127,8 +127,10 @@ int dc_hist_chunks(const uint8_t *data, uint64_t total, uint64_t chunk_size, int
 int dc_normalize_tables(const uint32_t *hist, int64_t n_chunks, uint32_t *freq, uint8_t *table_bytes,
                         void *stream);
 
-/* Reverse rANS encode of every chunk with todo[i] != 0, one lane per chunk.
- * Emitted bytes are written BACKWARDS from the end of the chunk's slot in
+/* Reverse rANS encode of every chunk with todo[i] != 0: pass 1 runs each
+ * chunk's serial state chain (one warp per chunk), pass 2 writes the
+ * renormalization bytes in parallel from the recorded states (see
+ * dc_ans_encode_work_bytes).  Emitted bytes are written BACKWARDS from the end of the chunk's slot in
  * `scratch` (slot i = [i*chunk_size, i*chunk_size + len_i)), so the decoder-
  * order stream is scratch[slot_end - stream_len[i] .. slot_end).  Encoding
  * stops early once the blob could not beat raw storage (388 + emitted >=
@@ -142,7 +144,13 @@ int dc_ans_encode_chunks(const uint8_t *data, uint64_t total, uint64_t chunk_siz
                          const uint8_t *todo, const uint32_t *freq, uint8_t *scratch,
                          uint32_t *final_state, uint64_t *stream_len, uint32_t seg_shift,
                          const int64_t *seg_base, uint32_t *seg_state, uint32_t *seg_emitted,
-                         uint32_t flags, void *stream);
+                         uint32_t flags, void *work, uint64_t work_bytes, void *stream);
+
+/* Device work space dc_ans_encode_chunks needs (caller-owned): the per-symbol
+ * encoder states of pass 1 (4 B/symbol) and the byte counts every 256
+ * symbols that let pass 2 emit the stream bytes in parallel.  flags bit 0:
+ * standalone blob (never abort to store); bit 1: lengths only (skip pass 2). */
+int dc_ans_encode_work_bytes(uint64_t total, uint64_t chunk_size, int64_t n_chunks, uint64_t *out);
 
 /* Assemble chunk payloads into the container byte image: chunk i goes to
  * dst[file_off[i]]: ANS = table_bytes[i] | u32 LE final_state | stream;

@@ -136,8 +136,9 @@ def _encode_one(u8: np.ndarray) -> tuple[np.ndarray, bytes, int]:
     sp = nv.stream_ptr()
     nv.call("dc_hist_chunks", d.data_ptr(), n, n, 1, hist.data_ptr(), sp)
     nv.call("dc_normalize_tables", hist.data_ptr(), 1, freq.data_ptr(), tb.data_ptr(), sp)
+    work, wbytes = nv.encode_work(n, n, 1, dev)
     nv.call("dc_ans_encode_chunks", d.data_ptr(), n, n, 1, todo.data_ptr(), freq.data_ptr(), slot,
-            state.data_ptr(), slen.data_ptr(), 0, None, None, None, 1, sp)
+            state.data_ptr(), slen.data_ptr(), 0, None, None, None, 1, work.data_ptr(), wbytes, sp)
     sl = int(slen.item())
     stream = scratch[room - sl:room].cpu().numpy().tobytes() if sl else b""
     return freq[0].cpu().numpy().view(np.uint32), stream, int(state.item()) & 0xFFFFFFFF

@@ -171,45 +171,35 @@ __global__ void k_normalize(const uint32_t* __restrict__ hist, int64_t n_chunks,
 }
 
 // ----------------------------------------------------------------- encode
-// One chunk per WARP (four warps per CTA, one per SM sub-partition): the
-// reverse encoder (ans.py:55-68) is a serial recurrence per chunk, so every
-// lane of the warp runs the same chain (uniform, no divergence) and the chunk's
-// time is that chain.  The step is branch-free:
+// Two passes.  The reverse encoder (ans.py:55-68) is a serial recurrence per
+// chunk, so pass 1 runs ONLY the state chain -- one chunk per warp, four warps
+// per CTA (one per SM sub-partition), every lane running the same branch-free
+// step so there is no divergence:
 //   p1 = x >= f<<16, p2 = x >= f<<24  (at most two renorm bytes: x < 2^28)
 //   xr = x >> 8*(p1+p2)
 //   x  = xr + bias + (umulhi(xr, rcp) >> sh) * (4096 - f)
 // with ryg_rans-style exact reciprocals (f == 1: rcp = 2^32-1 gives q = xr-1,
-// folded into bias = cum + 4095).  Renorm bytes go to a 256-byte shared ring
-// (32-bit addressing, one STS each) that the warp flushes to global memory
-// 128 bytes at a time with all 32 lanes.
+// folded into bias = cum + 4095).  It stores each symbol's input state (16-B
+// stores per 4 symbols) and the running byte count every 256 symbols.
+// Pass 2 (k_encode_emit, fully parallel, one thread per 256 symbols) turns the
+// recorded states back into the renormalization bytes at their final stream
+// positions: the byte count at each 256-symbol boundary is known from pass 1.
 constexpr int kEncWarps = 4;
-constexpr uint32_t kEncRing = 256;
+constexpr int kEmitSeg = 256;  // symbols per pass-2 thread (= pass-1 record cadence)
 
 struct __align__(16) EncEnt {
     uint32_t rcp, xm1, xm2, sh;  // xm1 = f << 16; xm2 = f << 24 or 2^32-1 when f >= 16
     uint32_t bias, gmul, pad0, pad1;  // gmul = 4096 - f
 };
 
-struct EncSmem {
-    EncEnt tab[256];
-    uint8_t ring[kEncRing];
-};
-
-__device__ __forceinline__ void enc_step(uint32_t& x, uint32_t& pos, const uint4& a, const uint2& b, uint32_t ring) {
-    // a = (rcp, xm1, xm2, sh), b = (bias, gmul); chain: setp -> selp -> selp -> mul.hi -> shr -> mad
+__device__ __forceinline__ void enc_step(uint32_t& x, uint32_t& pos, const uint4& a, const uint2& b) {
+    // a = (rcp, xm1, xm2, sh), b = (bias, gmul); chain: setp -> selp -> mul.hi -> shr -> mad
     asm volatile(
-        "{\n\t.reg .pred p1, p2;\n\t.reg .u32 x8, x16, xr, q, xb, r1, r2, n;\n\t"
+        "{\n\t.reg .pred p1, p2;\n\t.reg .u32 x8, x16, xr, q, xb, n;\n\t"
         "setp.ge.u32 p1, %0, %3;\n\t"
         "setp.ge.u32 p2, %0, %4;\n\t"
         "shr.u32 x8, %0, 8;\n\t"
         "shr.u32 x16, %0, 16;\n\t"
-        "and.b32 r1, %1, 255;\n\t"
-        "add.u32 r1, r1, %8;\n\t"
-        "add.u32 r2, %1, 1;\n\t"
-        "and.b32 r2, r2, 255;\n\t"
-        "add.u32 r2, r2, %8;\n\t"
-        "@p1 st.shared.u8 [r1], %0;\n\t"
-        "@p2 st.shared.u8 [r2], x8;\n\t"
         "selp.u32 n, 1, 0, p1;\n\t"
         "@p2 add.u32 n, n, 1;\n\t"
         "add.u32 %1, %1, n;\n\t"
@@ -220,104 +210,101 @@ __device__ __forceinline__ void enc_step(uint32_t& x, uint32_t& pos, const uint4
         "shr.u32 q, q, %5;\n\t"
         "mad.lo.u32 %0, q, %7, xb;\n\t}"
         : "+r"(x), "+r"(pos)
-        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(ring)
-        : "memory");
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y));
 }
 
-__device__ __forceinline__ void enc_sym(uint32_t& x, uint32_t& pos, const EncEnt* __restrict__ T, uint32_t s,
-                                        uint8_t* ring) {
-    const uint4 a = *reinterpret_cast<const uint4*>(&T[s].rcp);
-    const uint2 b = *reinterpret_cast<const uint2*>(&T[s].bias);
-    enc_step(x, pos, a, b, (uint32_t)__cvta_generic_to_shared(ring));
-}
-
-// emissions [from, to) of the ring -> global bytes out_end - 1 - k (all lanes)
-__device__ __forceinline__ void enc_flush(const uint8_t* ring, uint8_t* out_end, uint32_t from, uint32_t to,
-                                          int lane) {
-    __syncwarp();
-    for (uint32_t k = from + lane; k < to; k += 32) *(out_end - 1 - k) = ring[k & (kEncRing - 1)];
-    __syncwarp();
+// the encoder's per-symbol table for chunk c (called by one warp)
+__device__ __forceinline__ void build_enc_table(const uint32_t* __restrict__ freq, int64_t c, EncEnt* T, int lane) {
+    uint32_t fs[8], loc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        fs[k] = freq[c * 256 + lane * 8 + k];
+        loc += fs[k];
+    }
+    uint32_t inc = loc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    uint32_t cum = inc - loc;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t f = fs[k];
+        EncEnt e;
+        e.sh = 0;
+        if (f >= 2) {
+            uint32_t shift = 0;
+            while (f > (1u << shift)) ++shift;
+            e.rcp = (uint32_t)(((1ull << (shift + 31)) + f - 1) / f);
+            e.sh = shift - 1;
+        } else {
+            e.rcp = 0xFFFFFFFFu;
+        }
+        e.xm1 = f << 16;
+        e.xm2 = f < 16 ? f << 24 : 0xFFFFFFFFu;
+        e.bias = f >= 2 ? cum : cum + (kProbScale - 1);
+        e.gmul = kProbScale - f;
+        e.pad0 = e.pad1 = 0;
+        T[lane * 8 + k] = e;
+        cum += f;
+    }
 }
 
 __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __restrict__ data, uint64_t total,
                                                             uint64_t chunk_size, int64_t n_chunks,
                                                             const uint8_t* __restrict__ todo,
                                                             const uint32_t* __restrict__ freq,
-                                                            uint8_t* __restrict__ scratch,
                                                             uint32_t* __restrict__ final_state,
                                                             uint64_t* __restrict__ stream_len, uint32_t seg_shift,
                                                             const int64_t* __restrict__ seg_base,
                                                             uint32_t* __restrict__ seg_state,
-                                                            uint32_t* __restrict__ seg_emitted, uint32_t flags) {
-    __shared__ EncSmem sm[kEncWarps];
+                                                            uint32_t* __restrict__ seg_emitted, uint32_t flags,
+                                                            uint32_t* __restrict__ xs, uint32_t* __restrict__ rec,
+                                                            int64_t rec_per_chunk) {
+    __shared__ EncEnt tabs[kEncWarps][256];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t c = (int64_t)blockIdx.x * kEncWarps + warp;
     if (c >= n_chunks || !todo[c]) return;  // whole warp; no block-level sync below
     const uint64_t beg = (uint64_t)c * chunk_size;
     const uint64_t len = total - beg < chunk_size ? total - beg : chunk_size;
-    EncEnt* T = sm[warp].tab;
-    uint8_t* ring = sm[warp].ring;
-    {  // lane owns symbols 8*lane .. 8*lane+7; cum = exclusive warp scan of f
-        uint32_t fs[8], loc = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            fs[k] = freq[c * 256 + lane * 8 + k];
-            loc += fs[k];
-        }
-        uint32_t inc = loc;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc += o;
-        }
-        uint32_t cum = inc - loc;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint32_t f = fs[k];
-            EncEnt e;
-            e.sh = 0;
-            if (f >= 2) {
-                uint32_t shift = 0;
-                while (f > (1u << shift)) ++shift;
-                e.rcp = (uint32_t)(((1ull << (shift + 31)) + f - 1) / f);
-                e.sh = shift - 1;
-            } else {
-                e.rcp = 0xFFFFFFFFu;
-            }
-            e.xm1 = f << 16;
-            e.xm2 = f < 16 ? f << 24 : 0xFFFFFFFFu;
-            e.bias = f >= 2 ? cum : cum + (kProbScale - 1);
-            e.gmul = kProbScale - f;
-            e.pad0 = e.pad1 = 0;
-            T[lane * 8 + k] = e;
-            cum += f;
-        }
-    }
+    EncEnt* T = tabs[warp];
+    build_enc_table(freq, c, T, lane);
     __syncwarp();
 
     const uint8_t* src = data + beg;
-    uint8_t* out_end = scratch + beg + len;  // bytes go backwards from here
+    uint32_t* xsc = xs + beg;             // input state of every symbol
+    uint32_t* rc = rec + c * rec_per_chunk;  // bytes emitted after symbol 256*k
     // emitted >= limit -> the chunk will be stored (container.py:165); a
     // standalone blob (flags & 1) is always completed (ans.py:316-330)
     const uint64_t limit = (flags & 1) ? ~0ull : (len > kHeaderBytes ? len - kHeaderBytes : 0);
     const uint32_t K = 1u << seg_shift;
     const int64_t sb = seg_state ? seg_base[c] : 0;
-    const bool rec = seg_state != nullptr && lane == 0;
-    uint32_t x = kStateLower, pos = 0, flushed = 0;
+    const bool lead = lane == 0;
+    uint32_t x = kStateLower, pos = 0;
     bool stored = (limit == 0);
+    auto record = [&](uint64_t i) {  // after encoding symbol i
+        if (!lead) return;
+        if ((i & (kEmitSeg - 1)) == 0) rc[i / kEmitSeg] = pos;
+        if (seg_state && (i & (K - 1)) == 0) {
+            seg_state[sb + (i >> seg_shift)] = x;
+            seg_emitted[sb + (i >> seg_shift)] = pos;
+        }
+    };
     const uint64_t nblk = len >> 4;  // whole 16-symbol blocks [0, 16*nblk)
     // tail symbols [16*nblk, len), last to first
     for (uint64_t i = len; !stored && i > nblk * 16;) {
         --i;
-        enc_sym(x, pos, T, src[i], ring);
-        if (rec && (i & (K - 1)) == 0) {
-            seg_state[sb + (i >> seg_shift)] = x;
-            seg_emitted[sb + (i >> seg_shift)] = pos;
-        }
+        const uint32_t sy = src[i];
+        const uint4 ea = *reinterpret_cast<const uint4*>(&T[sy].rcp);
+        const uint2 eb = *reinterpret_cast<const uint2*>(&T[sy].bias);
+        if (lead) xsc[i] = x;
+        enc_step(x, pos, ea, eb);
+        record(i);
         if (pos >= limit) stored = true;
     }
-    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
     const bool al16 = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    const bool xal = (reinterpret_cast<uintptr_t>(xsc) & 15) == 0;
     auto load_blk = [&](uint64_t b) -> uint4 {
         if (al16) return __ldg(reinterpret_cast<const uint4*>(src + 16 * b));
         uint32_t w[4];
@@ -342,23 +329,76 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __rest
             ea[k] = *reinterpret_cast<const uint4*>(&T[sy].rcp);
             eb[k] = *reinterpret_cast<const uint2*>(&T[sy].bias);
         }
+        uint32_t xin[16];
 #pragma unroll
-        for (int k = 15; k >= 0; --k) enc_step(x, pos, ea[k], eb[k], ring_s);
-        const uint64_t i = 16 * b;  // split points sit at multiples of K >= 16: only at k == 0
-        if (rec && (i & (K - 1)) == 0) {
-            seg_state[sb + (i >> seg_shift)] = x;
-            seg_emitted[sb + (i >> seg_shift)] = pos;
+        for (int k = 15; k >= 0; --k) {
+            xin[k] = x;
+            enc_step(x, pos, ea[k], eb[k]);
         }
-        if (pos - flushed >= kEncRing / 2) {  // at most 32 bytes per block: the ring never overruns
-            enc_flush(ring, out_end, flushed, flushed + kEncRing / 2, lane);
-            flushed += kEncRing / 2;
+        if (lead) {
+            uint32_t* dst = xsc + 16 * b;
+            if (xal) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    reinterpret_cast<uint4*>(dst)[k] = make_uint4(xin[4 * k], xin[4 * k + 1], xin[4 * k + 2], xin[4 * k + 3]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) dst[k] = xin[k];
+            }
         }
+        record(16 * b);  // split points sit at multiples of K >= 16: only at k == 0
         if (pos >= limit) stored = true;  // could not beat raw storage (container.py:165)
     }
-    if (!stored) enc_flush(ring, out_end, flushed, pos, lane);
-    if (lane == 0) {
+    if (lead) {
         final_state[c] = x;
         stream_len[c] = stored ? ~0ull : pos;
+    }
+}
+
+// Pass 2: one thread per 256 symbols of an encoded chunk.  Replays the
+// renormalization test on the recorded input states and writes the bytes
+// backwards from the chunk's slot end (stream order reversed at assembly).
+__global__ void __launch_bounds__(256) k_encode_emit(const uint8_t* __restrict__ data, uint64_t total,
+                                                     uint64_t chunk_size, int64_t n_chunks,
+                                                     const uint8_t* __restrict__ todo,
+                                                     const uint32_t* __restrict__ freq,
+                                                     const uint64_t* __restrict__ stream_len,
+                                                     const uint32_t* __restrict__ xs, const uint32_t* __restrict__ rec,
+                                                     int64_t rec_per_chunk, uint8_t* __restrict__ scratch) {
+    __shared__ uint32_t xm[256][2];
+    for (int64_t c = blockIdx.y; c < n_chunks; c += gridDim.y) {
+        if (!todo[c] || stream_len[c] == ~0ull) continue;  // uniform per CTA
+        __syncthreads();  // previous chunk's table readers are done
+        for (int s = threadIdx.x; s < 256; s += blockDim.x) {
+            const uint32_t f = freq[c * 256 + s];
+            xm[s][0] = f << 16;
+            xm[s][1] = f < 16 ? f << 24 : 0xFFFFFFFFu;
+        }
+        __syncthreads();
+        const uint64_t beg = (uint64_t)c * chunk_size;
+        const uint64_t len = total - beg < chunk_size ? total - beg : chunk_size;
+        const uint64_t nseg = (len + kEmitSeg - 1) / kEmitSeg;
+        const uint8_t* src = data + beg;
+        const uint32_t* xsc = xs + beg;
+        uint8_t* out_end = scratch + beg + len;
+        for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nseg;
+             g += (uint64_t)gridDim.x * blockDim.x) {
+            const uint64_t lo = g * kEmitSeg, hi = (g + 1) * kEmitSeg < len ? (g + 1) * kEmitSeg : len;
+            uint32_t pos = hi < len ? rec[c * rec_per_chunk + hi / kEmitSeg] : 0u;  // bytes emitted before symbol hi-1
+            for (uint64_t i = hi; i > lo;) {
+                --i;
+                const uint32_t x = xsc[i];
+                const uint32_t sy = src[i];
+                if (x >= xm[sy][0]) {
+                    *(out_end - 1 - pos) = (uint8_t)x;
+                    ++pos;
+                    if (x >= xm[sy][1]) {
+                        *(out_end - 1 - pos) = (uint8_t)(x >> 8);
+                        ++pos;
+                    }
+                }
+            }
+        }
     }
 }
 
@@ -425,17 +465,39 @@ extern "C" int dc_normalize_tables(const uint32_t* hist, int64_t n_chunks, uint3
     return DC_OK;
 }
 
+extern "C" int dc_ans_encode_work_bytes(uint64_t total, uint64_t chunk_size, int64_t n_chunks, uint64_t* out) {
+    if (!out || chunk_size == 0 || n_chunks < 0) return DC_ERR_ARG;
+    const uint64_t per = (chunk_size + kEmitSeg - 1) / kEmitSeg + 1;
+    *out = 4 * total + 16 + 4 * per * (uint64_t)n_chunks + 256;
+    return DC_OK;
+}
+
 extern "C" int dc_ans_encode_chunks(const uint8_t* data, uint64_t total, uint64_t chunk_size, int64_t n_chunks,
                                     const uint8_t* todo, const uint32_t* freq, uint8_t* scratch,
                                     uint32_t* final_state, uint64_t* stream_len, uint32_t seg_shift,
                                     const int64_t* seg_base, uint32_t* seg_state, uint32_t* seg_emitted,
-                                    uint32_t flags, void* stream) {
+                                    uint32_t flags, void* work, uint64_t work_bytes, void* stream) {
     if (n_chunks < 0 || chunk_size == 0 || (seg_state && (seg_shift < 4 || seg_shift > 20))) return DC_ERR_ARG;
     if (n_chunks == 0) return DC_OK;
-    k_encode<<<(unsigned)((n_chunks + kEncWarps - 1) / kEncWarps), kEncWarps * 32, 0, (cudaStream_t)stream>>>(
-        data, total, chunk_size, n_chunks, todo, freq, scratch, final_state, stream_len, seg_shift, seg_base,
-        seg_state, seg_emitted, flags);
+    uint64_t need = 0;
+    dc_ans_encode_work_bytes(total, chunk_size, n_chunks, &need);
+    if (!work || work_bytes < need) return DC_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    uintptr_t w = (reinterpret_cast<uintptr_t>(work) + 15) & ~(uintptr_t)15;
+    uint32_t* xs = reinterpret_cast<uint32_t*>(w);
+    uint32_t* rec = reinterpret_cast<uint32_t*>(w + ((4 * total + 15) & ~(uint64_t)15));
+    const int64_t rec_per = (int64_t)((chunk_size + kEmitSeg - 1) / kEmitSeg + 1);
+    k_encode<<<(unsigned)((n_chunks + kEncWarps - 1) / kEncWarps), kEncWarps * 32, 0, st>>>(
+        data, total, chunk_size, n_chunks, todo, freq, final_state, stream_len, seg_shift, seg_base, seg_state,
+        seg_emitted, flags, xs, rec, rec_per);
     DC_CHECK_LAUNCH("k_encode");
+    if (flags & 2) return DC_OK;  // lengths only: no stream bytes needed
+    const uint64_t nseg = (chunk_size + kEmitSeg - 1) / kEmitSeg;
+    const unsigned gx = (unsigned)((nseg + 255) / 256 < 64 ? (nseg + 255) / 256 : 64);
+    dim3 grid(gx, (unsigned)(n_chunks < 65535 ? n_chunks : 65535));
+    k_encode_emit<<<grid, 256, 0, st>>>(data, total, chunk_size, n_chunks, todo, freq, stream_len, xs, rec, rec_per,
+                                        scratch);
+    DC_CHECK_LAUNCH("k_encode_emit");
     return DC_OK;
 }
 

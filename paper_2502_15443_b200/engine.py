@@ -321,10 +321,13 @@ def encode_payload(payload: torch.Tensor, chunk_size: int, mask: np.ndarray | No
             index = SegmentIndex(seg_shift, base_np, nseg, _t(base_np, torch.int64, dev),
                                  torch.zeros(max(nseg, 1), dtype=torch.int32, device=dev),
                                  torch.zeros(max(nseg, 1), dtype=torch.int32, device=dev))
+        work, wbytes = nv.encode_work(total, chunk_size, n, dev)
         nv.call("dc_ans_encode_chunks", payload.data_ptr(), total, chunk_size, n, todo.data_ptr(),
                 freq.data_ptr(), scratch.data_ptr(), state.data_ptr(), slen.data_ptr(),
                 seg_shift if index else 0, index.d_seg_base.data_ptr() if index else None,
-                index.d_state.data_ptr() if index else None, index.d_off.data_ptr() if index else None, 0, sp)
+                index.d_state.data_ptr() if index else None, index.d_off.data_ptr() if index else None, 0,
+                work.data_ptr(), wbytes, sp)
+        del work  # stream-ordered reuse by the caching allocator
     d_off = torch.from_numpy((np.arange(n, dtype=np.int64) * chunk_size)).to(dev)
     d_len = torch.from_numpy(lens.view(np.int64)).to(dev)
     crc = crc32_ranges(payload, d_off, d_len, min(chunk_size, total)).cpu().numpy().view(np.uint32)

@@ -54,7 +54,8 @@ SIGNATURES: dict[str, list] = {
     "dc_crc32_ranges": [_P, _P, _P, _I64, _U64, _P, _P],
     "dc_hist_chunks": [_P, _U64, _U64, _I64, _P, _P],
     "dc_normalize_tables": [_P, _I64, _P, _P, _P],
-    "dc_ans_encode_chunks": [_P, _U64, _U64, _I64, _P, _P, _P, _P, _P, _U32, _P, _P, _P, _U32, _P],
+    "dc_ans_encode_chunks": [_P, _U64, _U64, _I64, _P, _P, _P, _P, _P, _U32, _P, _P, _P, _U32, _P, _U64, _P],
+    "dc_ans_encode_work_bytes": [_U64, _U64, _I64, _P],
     "dc_assemble_payloads": [_P, _U64, _U64, _I64, _P, _P, _P, _P, _P, _P, _P, _P],
     "dc_quant_absmax": [_P, ctypes.c_int, _P, _I64, _I64, _P, _P, _P],
     "dc_quantize": [_P, ctypes.c_int, _P, _I64, _I64, ctypes.c_double, _P, _P],
@@ -189,3 +190,12 @@ def to_host(t: torch.Tensor) -> "np.ndarray":
 
 def exported_symbols() -> list[str]:
     return list(SIGNATURES)
+
+
+def encode_work(total: int, chunk_size: int, n_chunks: int, device=None):
+    """Device work buffer for dc_ans_encode_chunks (uint8 tensor, size)."""
+    import torch
+    need = ctypes.c_uint64(0)
+    call("dc_ans_encode_work_bytes", int(total), int(chunk_size), int(n_chunks), ctypes.byref(need))
+    buf = torch.empty(int(need.value), dtype=torch.uint8, device=device or require_cuda())
+    return buf, int(need.value)

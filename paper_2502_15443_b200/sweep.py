@@ -52,15 +52,15 @@ def blob_lengths(payloads: list[torch.Tensor], streams: int = 8) -> list[int]:
         st = ss[i % streams]
         st.wait_stream(main)
         with torch.cuda.stream(st):
-            room = 2 * m + 8
-            scratch = nv.device_bytes(room, dev)
-            keep.append(scratch)
+            work, wbytes = nv.encode_work(m, m, 1, dev)
+            keep.append(work)
             sp = st.cuda_stream
             nv.call("dc_hist_chunks", p.data_ptr(), m, m, 1, hist[i].data_ptr(), sp)
             nv.call("dc_normalize_tables", hist[i].data_ptr(), 1, freq[i].data_ptr(), tb[i].data_ptr(), sp)
+            # standalone (bit 0) and lengths only (bit 1): no stream bytes are written
             nv.call("dc_ans_encode_chunks", p.data_ptr(), m, m, 1, todo[i:i + 1].data_ptr(), freq[i].data_ptr(),
-                    scratch.data_ptr() + room - m, state[i:i + 1].data_ptr(), slen[i:i + 1].data_ptr(), 0, None,
-                    None, None, 1, sp)
+                    None, state[i:i + 1].data_ptr(), slen[i:i + 1].data_ptr(), 0, None, None, None, 3,
+                    work.data_ptr(), wbytes, sp)
     for st in ss:
         main.wait_stream(st)
     lens = slen.cpu().numpy()
