@@ -100,6 +100,18 @@ int dc_ans_decode_segments(const uint8_t *base, const uint64_t *blob_off, const 
                            const int32_t *tasks, int64_t n_tasks, uint8_t *out, int32_t *status,
                            void *stream);
 
+/* Small-chunk variant (every chunk <= dc_decode_small_max_chunk() bytes):
+ * warp tasks of <= dc_decode_small_segments() segments, a compact per-warp
+ * table (u8 slot->symbol + per-symbol update), stream read through L1.
+ * Same arguments, task format, outputs and chain checks as
+ * dc_ans_decode_segments.  replaces ans.py:97-200 at small chunk sizes. */
+int dc_decode_small_segments(void);
+int dc_decode_small_max_chunk(void);
+int dc_ans_decode_small(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
+                        const uint64_t *out_off, const uint64_t *out_len, uint32_t seg_shift,
+                        const int64_t *seg_base, const uint32_t *seg_state, const uint32_t *seg_off,
+                        const int32_t *tasks, int64_t n_tasks, uint8_t *out, int32_t *status, void *stream);
+
 /* Raw copy of store chunks (codec 0).  replaces container.py:309-310. */
 int dc_store_copy(const uint8_t *base, const uint64_t *blob_off, const uint64_t *out_off,
                   const uint64_t *out_len, const uint8_t *codec, int64_t n_chunks, uint8_t *out,

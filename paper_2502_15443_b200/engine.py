@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 import struct
 import zlib
 
@@ -153,7 +154,7 @@ class SegmentIndex:
     def tasks(self, jobs: JobTable, ok: np.ndarray, max_segs: int | None = None) -> torch.Tensor:
         """int32 [n_tasks, 4] = (chunk, first segment, count, 0): at most
         ``max_segs`` segments and at most STAGE_CAP staged stream bytes each."""
-        max_segs = max_segs or nv.call("dc_decode_task_segments")
+        max_segs = max_segs or nv.call("dc_decode_small_segments" if small_mode(jobs) else "dc_decode_task_segments")
         K = 1 << self.seg_shift
         sel = np.nonzero((jobs.codec == 1) & ok & (jobs.out_len > 0))[0]
         nseg = (jobs.out_len[sel].astype(np.int64) + K - 1) // K
@@ -214,11 +215,23 @@ def decode_serial(base, jobs: JobTable, ids: np.ndarray, out: torch.Tensor, stat
             status.data_ptr(), nv.stream_ptr())
 
 
+def small_mode(jobs: JobTable) -> bool:
+    """Every chunk small enough for the warp-task decoder (k_decode_small):
+    its tasks are warp-sized, so SegmentIndex.tasks and the kernel choice
+    both follow this one predicate."""
+    lim = int(os.environ.get("DCOMP_SMALL_MAX_CHUNK", "0")) or nv.call("dc_decode_small_max_chunk")
+    return jobs.n > 0 and int(jobs.out_len.max()) <= lim
+
+
+def segment_kernel(jobs: JobTable) -> str:
+    return "dc_ans_decode_small" if small_mode(jobs) else "dc_ans_decode_segments"
+
+
 def decode_segments(base, jobs: JobTable, index: SegmentIndex, tasks: torch.Tensor, out: torch.Tensor,
                     status: torch.Tensor) -> None:
     if tasks.shape[0] == 0:
         return
-    nv.call("dc_ans_decode_segments", base.data_ptr(), jobs.d_blob_off.data_ptr(), jobs.d_blob_len.data_ptr(),
+    nv.call(segment_kernel(jobs), base.data_ptr(), jobs.d_blob_off.data_ptr(), jobs.d_blob_len.data_ptr(),
             jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(), index.seg_shift, index.d_seg_base.data_ptr(),
             index.d_state.data_ptr(), index.d_off.data_ptr(), tasks.data_ptr(), tasks.shape[0], out.data_ptr(),
             status.data_ptr(), nv.stream_ptr())
@@ -435,7 +448,7 @@ class PipelinedDecode:
                     off8(jobs.d_out_len), jobs.d_codec.data_ptr() + g0, k, status.data_ptr() + 4 * g0, sp_comp)
             t0, t1 = np.searchsorted(t_chunk, g0), np.searchsorted(t_chunk, g1)
             if t1 > t0:
-                nv.call("dc_ans_decode_segments", image.data_ptr(), jobs.d_blob_off.data_ptr(),
+                nv.call(segment_kernel(jobs), image.data_ptr(), jobs.d_blob_off.data_ptr(),
                         jobs.d_blob_len.data_ptr(), jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(),
                         index.seg_shift, index.d_seg_base.data_ptr(), index.d_state.data_ptr(),
                         index.d_off.data_ptr(), tasks[t0:t1].data_ptr(), int(t1 - t0), out.data_ptr(),

@@ -80,7 +80,7 @@ class StreamedCompressed:
             nv.call("dc_ans_validate", self.image.data_ptr(), off8(j.d_blob_off), off8(j.d_blob_len),
                     off8(j.d_out_len), j.d_codec.data_ptr() + g0, k, self.status.data_ptr() + 4 * g0, sp)
             if t1 > t0:
-                nv.call("dc_ans_decode_segments", self.image.data_ptr(), j.d_blob_off.data_ptr(),
+                nv.call(engine.segment_kernel(j), self.image.data_ptr(), j.d_blob_off.data_ptr(),
                         j.d_blob_len.data_ptr(), j.d_out_off.data_ptr(), j.d_out_len.data_ptr(), ix.seg_shift,
                         ix.d_seg_base.data_ptr(), ix.d_state.data_ptr(), ix.d_off.data_ptr(),
                         self.tasks[t0:t1].data_ptr(), t1 - t0, self.out.data_ptr(), self.status.data_ptr(), sp)

@@ -81,13 +81,15 @@ def test_split_point_decode_equals_exact(cuda):
         assert np.array_equal(cuda.unpack(data, index=index).tensors[0].qvalues, q)
 
 
-def test_broken_index_falls_back_exactly(cuda):
+@pytest.mark.parametrize("chunk", [16384, 65536])  # warp-task small-chunk kernel / CTA-task kernel
+def test_broken_index_falls_back_exactly(cuda, chunk):
     from paper_2502_15443_b200 import container, engine
     rng = np.random.default_rng(4)
     q = np.clip(np.round(rng.normal(0, 9, (300, 1000))), -127, 127).astype(np.int8)
     t = cuda.QuantizedTensor("w", q, 0.01, cuda.ScaleVector.identity(1000))
     st = {"w": cuda.ActivationStats("w", np.ones(1000))}
-    data, index = container.pack_indexed([t], st, chunk_size=65536, seg_shift=8)
+    data, index = container.pack_indexed([t], st, chunk_size=chunk, seg_shift=8)
+    assert engine.small_mode(container.jobs_for(container._parse(data)[2])) == (chunk <= 32768)
     index.d_state[5] += 1  # corrupt one split point
     index.d_off[17] += 3
     assert np.array_equal(cuda.unpack(data, index=index).tensors[0].qvalues, q)
