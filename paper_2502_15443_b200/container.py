@@ -134,15 +134,25 @@ def _mask_of(plan, n_chunks: int) -> np.ndarray:
 
 
 def _device_payload(tensors) -> torch.Tensor:
+    """Concatenated int8 payload on the GPU: the tensors are gathered into one
+    pinned staging buffer by parallel host copies, then one async H2D."""
     dev = nv.require_cuda()
     total = sum(t.qvalues.size for t in tensors)
     out = nv.device_bytes(total, dev)
-    pos = 0
+    if total == 0:
+        return out
+    stage = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+    sv = stage.numpy()
+    from concurrent.futures import ThreadPoolExecutor
+    jobs, pos = [], 0
     for t in tensors:
         n = t.qvalues.size
         if n:
-            out[pos:pos + n].copy_(torch.from_numpy(np.ascontiguousarray(t.qvalues).reshape(-1).view(np.uint8)))
+            jobs.append((sv[pos:pos + n], np.ascontiguousarray(t.qvalues).reshape(-1).view(np.uint8)))
         pos += n
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+        list(ex.map(lambda j: np.copyto(j[0], j[1]), jobs))
+    out[:total].copy_(stage, non_blocking=True)
     return out
 
 
@@ -190,7 +200,7 @@ def _pack_impl(tensors, stats, chunk_size, plan, seg_shift):
         return data, None
     payload = _device_payload(tensors)
     image, enc, _ = pack_device(payload, header, chunk_size, plan, seg_shift)
-    return image.cpu().numpy().tobytes(), enc.index
+    return nv.to_host(image).tobytes(), enc.index  # pinned D2H, then the one copy `bytes` needs
 
 
 def pack(tensors, stats, chunk_size: int = DEFAULT_CHUNK_SIZE, plan=None) -> bytes:
