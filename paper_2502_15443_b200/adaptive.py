@@ -96,15 +96,17 @@ class MeasuredProfile:
 
 
 def b200_profile(curve, int8_weight_gbs: float, hbm_gbs: float | None = None, h2d_gbs: float | None = None,
-                 storage_gbs: float = 7.0) -> MeasuredProfile:
-    """HardwareProfile from measurements (GB/s with GB = 1e9)."""
+                 storage_gbs: float = 7.0, mem_gpu: float | None = None) -> MeasuredProfile:
+    """HardwareProfile from measurements (GB/s with GB = 1e9); rates not given
+    are measured on the current GPU."""
     pts = [(p["chunk_size"], p["gbs"]) for p in curve]
     d_max, c_sat = fit_speed_curve(pts)
-    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    if mem_gpu is None:
+        mem_gpu = float(torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory)
     import os
     host_mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
     h = HardwareProfile(B_stoc=storage_gbs, B_ctog=h2d_gbs or measure_h2d_gbs(), B_gpu=hbm_gbs or measure_hbm_gbs(),
-                        D_max=d_max, c_sat=c_sat, I_gpu=int8_weight_gbs, mem_gpu=float(props.total_memory),
+                        D_max=d_max, c_sat=c_sat, I_gpu=int8_weight_gbs, mem_gpu=float(mem_gpu),
                         mem_cpu=float(host_mem))
     return MeasuredProfile(h, curve, (d_max, c_sat))
 
