@@ -144,6 +144,56 @@ def _encode_one(u8: np.ndarray) -> tuple[np.ndarray, bytes, int]:
     return freq[0].cpu().numpy().view(np.uint32), stream, int(state.item()) & 0xFFFFFFFF
 
 
+def compress_blobs(pieces: list[np.ndarray], streams: int = 16) -> list[bytes]:
+    """compress_blob() of many byte arrays at once: every blob's serial encode
+    chain runs concurrently (one warp each, side CUDA streams), so the batch
+    costs about one (largest) blob instead of their sum."""
+    dev = nv.require_cuda()
+    n = len(pieces)
+    if n == 0:
+        return []
+    sizes = [int(p.size) for p in pieces]
+    if min(sizes) == 0:
+        raise DcompError("empty input")
+    src = nv.to_device_bytes(np.concatenate([np.asarray(p, dtype=np.uint8).reshape(-1) for p in pieces]), dev)
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    hist = torch.empty((n, 256), dtype=torch.int32, device=dev)
+    freq = torch.empty((n, 256), dtype=torch.int32, device=dev)
+    tb = torch.empty((n, TABLE_BYTES), dtype=torch.uint8, device=dev)
+    state = torch.empty(n, dtype=torch.int32, device=dev)
+    slen = torch.empty(n, dtype=torch.int64, device=dev)
+    todo = torch.ones(n, dtype=torch.uint8, device=dev)
+    main = torch.cuda.current_stream(dev)
+    ss = [torch.cuda.Stream(dev) for _ in range(min(streams, n))]
+    keep = []
+    for i, (m, o) in enumerate(zip(sizes, offs)):
+        st = ss[i % len(ss)]
+        st.wait_stream(main)
+        with torch.cuda.stream(st):
+            room = 2 * m + 8  # worst case: 2 bytes per symbol (+ slop)
+            scratch = nv.device_bytes(room, dev)
+            work, wbytes = nv.encode_work(m, m, 1, dev)
+            keep.append((scratch, work, room))
+            p = src.data_ptr() + int(o)
+            sp = st.cuda_stream
+            nv.call("dc_hist_chunks", p, m, m, 1, hist[i].data_ptr(), sp)
+            nv.call("dc_normalize_tables", hist[i].data_ptr(), 1, freq[i].data_ptr(), tb[i].data_ptr(), sp)
+            nv.call("dc_ans_encode_chunks", p, m, m, 1, todo[i:i + 1].data_ptr(), freq[i].data_ptr(),
+                    scratch.data_ptr() + room - m, state[i:i + 1].data_ptr(), slen[i:i + 1].data_ptr(), 0, None,
+                    None, None, 1, work.data_ptr(), wbytes, sp)
+    for st in ss:
+        main.wait_stream(st)
+    sl = slen.cpu().numpy()
+    x0 = state.cpu().numpy().view(np.uint32)
+    tables = tb.cpu().numpy()
+    out = []
+    for i, (scratch, _, room) in enumerate(keep):
+        k = int(sl[i])
+        stream = scratch[room - k:room].cpu().numpy().tobytes() if k else b""
+        out.append(tables[i].tobytes() + struct.pack("<I", int(x0[i])) + stream)
+    return out
+
+
 def ans_compress(data) -> tuple[AnsTable, bytes]:
     """Compress bytes; returns (table, payload = state u32 LE + stream)."""
     u8 = _as_u8(data)

@@ -555,10 +555,11 @@ def read_container(path) -> ModelBundle:
 
 # --------------------------------------------------------- benchmark helpers
 def chunked_compress(data, chunk_size: int = DEFAULT_CHUNK_SIZE) -> list[bytes]:
-    """Split raw bytes into chunk-sized ANS blobs (every chunk encoded, no store fallback)."""
-    from .ans import compress_blob
+    """Split raw bytes into chunk-sized ANS blobs (every chunk encoded, no store
+    fallback; reference container.py:349-354), all chunks encoded concurrently."""
+    from .ans import compress_blobs
     u8 = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data.reshape(-1).view(np.uint8)
-    return [compress_blob(u8[i:i + chunk_size]) for i in range(0, u8.size, chunk_size)]
+    return compress_blobs([u8[i:i + chunk_size] for i in range(0, u8.size, chunk_size)])
 
 
 def chunked_decompress(blobs: list[bytes], lengths: list[int]) -> np.ndarray:

@@ -68,14 +68,36 @@ __global__ void k_validate(const uint8_t* __restrict__ base, const uint64_t* __r
 }
 
 // ------------------------------------------------------------- serial decode
+// One CTA per chunk: the whole CTA builds the table, then one thread walks
+// the stream exactly as the reference does.  That walk is a serial
+// recurrence, so its speed is its dependency chain: the stream is staged into
+// a 4 x 4 KB shared ring by bulk async copies issued ahead of the reader
+// (no global-memory latency on the chain) and read through the same two-word
+// window and PRMT refills as the segment decoder; output leaves as 16-byte
+// stores.  Bytes past the stream are never consumed by a valid chunk; a
+// corrupt one ends with p != plen whatever it read (verdict unchanged).
 constexpr int kSerialThreads = 128;
+constexpr uint32_t kSerSlot = 4096;
+constexpr uint32_t kSerRing = 4 * kSerSlot;
+
+struct SerialSmem {
+    TableSmem T;
+    alignas(128) uint8_t ring[kSerRing];
+    uint64_t bar[4];
+};
 
 __global__ void __launch_bounds__(kSerialThreads) k_decode_serial(
     const uint8_t* __restrict__ base, const uint64_t* __restrict__ blob_off, const uint64_t* __restrict__ blob_len,
     const uint64_t* __restrict__ out_off, const uint64_t* __restrict__ out_len, const int32_t* __restrict__ ids,
     int64_t n_ids, uint8_t* __restrict__ out, uint32_t seg_shift, const int64_t* __restrict__ seg_base,
     uint32_t* __restrict__ seg_state, uint32_t* __restrict__ seg_off, int32_t* __restrict__ status) {
-    __shared__ TableSmem T;
+    __shared__ SerialSmem S;
+    TableSmem& T = S.T;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(&S.bar[i], 1);
+        fence_mbar_init();
+    }
+    uint32_t ph_base = 0;  // completions per slot so far (same for every slot at a chunk start)
     for (int64_t id = blockIdx.x; id < n_ids; id += gridDim.x) {
         const int c = ids[id];
         const int32_t st0 = status[c];
@@ -83,7 +105,6 @@ __global__ void __launch_bounds__(kSerialThreads) k_decode_serial(
         const uint8_t* blob = base + blob_off[c];
         const uint64_t n = out_len[c];
         if (n == 0) continue;
-        const uint8_t* s = blob + kHeaderBytes;
         const uint64_t plen = blob_len[c] - kHeaderBytes;
         const uint32_t x0 = ld_u32_le_unaligned(blob + kTableBytes);
         uint8_t* o = out + out_off[c];
@@ -103,37 +124,108 @@ __global__ void __launch_bounds__(kSerialThreads) k_decode_serial(
             if (threadIdx.x == 0) status[c] = (x0 == kStateLower && plen == 0) ? DC_CHUNK_OK : DC_CHUNK_CORRUPT;
             continue;
         }
-        if (threadIdx.x == 0) {
-            uint32_t x = x0;
-            uint64_t p = 0;
-            bool bad = false;
-            for (uint64_t i = 0; i < n;) {
-                const uint64_t end = (i + kCheckBlock < n) ? i + kCheckBlock : n;
-                for (uint64_t j = i; j < end; ++j) {
-                    if (seg_state && (j & (K - 1)) == 0) {
-                        seg_state[sb + (j >> seg_shift)] = x;
-                        seg_off[sb + (j >> seg_shift)] = (uint32_t)p;
-                    }
-                    const uint32_t e = T.tab[x & (kProbScale - 1)];
-                    o[j] = (uint8_t)e;
-                    x = (e >> 20) * (x >> 12) + ((e >> 8) & 0xFFF);
-                    if (x < kStateLower) {
-                        x = (x << 8) | (p < plen ? s[p] : 0u);
-                        ++p;
-                        if (x < kStateLower) {
-                            x = (x << 8) | (p < plen ? s[p] : 0u);
-                            ++p;
-                        }
-                    }
+        if (threadIdx.x != 0) continue;
+        // ---- staged stream: bytes [a16, a16 + stage_len) in 4 KB blocks, block b in slot b & 3
+        const uint64_t gs = reinterpret_cast<uint64_t>(blob) + kHeaderBytes;
+        const uint64_t a16 = gs & ~(uint64_t)15;
+        const uint32_t delta = (uint32_t)(gs - a16);
+        const uint64_t stage_len = (delta + plen + 15) & ~(uint64_t)15;
+        const uint64_t nblk = (stage_len + kSerSlot - 1) / kSerSlot;
+        const uint32_t ring = smem_u32(S.ring);
+        uint64_t issued = 0, ready = 0;
+        auto issue_upto = [&](uint64_t lim) {  // blocks < lim, at most 4 in flight
+            for (; issued < lim && issued < nblk; ++issued) {
+                const uint32_t slot = (uint32_t)(issued & 3);
+                const uint64_t off = issued * kSerSlot;
+                const uint32_t bytes = (uint32_t)min((uint64_t)kSerSlot, stage_len - off);
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(&S.bar[slot], bytes);
+                bulk_g2s(S.ring + slot * kSerSlot, reinterpret_cast<const void*>(a16 + off), bytes, &S.bar[slot]);
+            }
+        };
+        auto wait_upto = [&](uint64_t need) {  // blocks <= need are in the ring
+            for (; ready <= need && ready < nblk; ++ready) {
+                const uint32_t slot = (uint32_t)(ready & 3);
+                mbar_wait(&S.bar[slot], (ph_base + (uint32_t)(ready >> 2)) & 1u);
+            }
+        };
+        issue_upto(4);
+        wait_upto((delta + 8) / kSerSlot);
+        auto ldr = [&](uint64_t rel) { return lds_u32(ring + (uint32_t)(rel & (kSerRing - 1))); };
+        // window: w0 holds the next byte at bit offset o, w1 the next word; wrel = rel offset of w1
+        uint64_t wrel = (delta & ~3u) + 4;
+        uint32_t w0 = ldr(wrel - 4), w1 = ldr(wrel), ob = (delta & 3u) * 8u;
+        auto advance = [&](uint32_t sel) {
+            ob += 8u * (sel - kSelBase);
+            if (ob >= 32) {
+                ob -= 32;
+                w0 = w1;
+                wrel += 4;
+                w1 = ldr(wrel);
+            }
+        };
+        auto rpos = [&]() { return wrel - 4 + (ob >> 3); };  // rel offset of the next unread byte
+        const uint32_t tab = smem_u32(T.tab);
+        const FmaK fk = fma_consts(1u);
+        const bool oal = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+        uint32_t x = x0;
+        bool bad = false;
+        uint64_t j = 0;
+        while (j < n) {
+            // refill: a 16-symbol group reads at most 32 bytes (+ the 8-byte window)
+            const uint64_t rp = rpos();
+            wait_upto((rp + 40) / kSerSlot);
+            issue_upto(rp / kSerSlot + 4);
+            if (seg_state && (j & (K - 1)) == 0) {
+                seg_state[sb + (j >> seg_shift)] = x;
+                seg_off[sb + (j >> seg_shift)] = (uint32_t)(rp - delta);
+            }
+            if (j + 16 <= n) {
+                uint32_t w[4];
+#pragma unroll
+                for (int v = 0; v < 16; v += 2) {
+                    uint32_t vb, sel = kSelBase;
+                    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(vb) : "r"(w0), "r"(w1), "r"(ob));
+                    const uint32_t e0 = dec_sym(x, sel, vb, tab, fk);
+                    const uint32_t t = __byte_perm(e0, dec_sym(x, sel, vb, tab, fk), 0x0040);
+                    w[v >> 2] = (v & 2) ? __byte_perm(w[v >> 2], t, 0x5410) : t;
+                    advance(sel);
                 }
-                if (p > plen) {  // ans.py:89-90
+                if (oal) {
+                    *reinterpret_cast<uint4*>(o + j) = make_uint4(w[0], w[1], w[2], w[3]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) o[j + k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+                }
+                j += 16;
+            } else {
+                for (; j < n; ++j) {
+                    uint32_t vb, sel = kSelBase;
+                    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(vb) : "r"(w0), "r"(w1), "r"(ob));
+                    o[j] = (uint8_t)dec_sym(x, sel, vb, tab, fk);
+                    advance(sel);
+                }
+            }
+            if ((j & (kCheckBlock - 1)) == 0 || j == n) {
+                if (rpos() - delta > plen) {  // ans.py:89-90 (memory safety; the verdict is corrupt)
                     bad = true;
                     break;
                 }
-                i = end;
             }
-            if (x != kStateLower || p != plen) bad = true;  // ans.py:92-93
-            status[c] = bad ? DC_CHUNK_CORRUPT : DC_CHUNK_OK;
+        }
+        if (x != kStateLower || rpos() - delta != plen) bad = true;  // ans.py:92-93
+        status[c] = bad ? DC_CHUNK_CORRUPT : DC_CHUNK_OK;
+        // drain: every issued block completes before its slot's barrier is reused
+        wait_upto(issued - 1);
+        if (issued > 0) {
+            // keep all four slots' phases in step for the next chunk
+            const uint64_t rounds = (issued + 3) / 4;
+            for (uint64_t b = issued; b < rounds * 4; ++b) {  // dummy completions for unused slots
+                const uint32_t slot = (uint32_t)(b & 3);
+                mbar_arrive(&S.bar[slot]);
+                mbar_wait(&S.bar[slot], (ph_base + (uint32_t)(b >> 2)) & 1u);
+            }
+            ph_base += (uint32_t)rounds;
         }
     }
 }
