@@ -95,6 +95,31 @@ def test_broken_index_falls_back_exactly(cuda, chunk):
     assert np.array_equal(cuda.unpack(data, index=index).tensors[0].qvalues, q)
 
 
+@pytest.mark.parametrize("chunk", [16384, 1 << 20])
+def test_mixed_codecs_split_point(cuda, chunk):
+    """Single-symbol (all-zero), incompressible (stored) and ordinary chunks in one
+    container through the split-point path, small-chunk and CTA-task kernels."""
+    from paper_2502_15443_b200 import container, engine
+    rng = np.random.default_rng(8)
+    parts = [np.zeros((64, 1024), np.int8), rng.integers(-128, 128, (64, 1024)).astype(np.int8),
+             np.clip(np.round(rng.normal(0, 7, (512, 1024))), -127, 127).astype(np.int8)]
+    ts, st = [], {}
+    for i, q in enumerate(parts):
+        ts.append(cuda.QuantizedTensor(f"m{i}", q, 0.01, cuda.ScaleVector.identity(1024)))
+        st[f"m{i}"] = cuda.ActivationStats(f"m{i}", np.ones(1024))
+    data, index = container.pack_indexed(ts, st, chunk_size=chunk, seg_shift=8)
+    ent = container._parse(data)[2]
+    if chunk == 16384:
+        assert (ent["codec"] == 0).any() and (ent["codec"] == 1).any()
+    base = cuda.native.to_device_bytes(data)
+    jobs = container.jobs_for(ent)
+    assert engine.small_mode(jobs) == (chunk <= 32768)
+    fast = engine.decode_jobs(base, jobs, index=index)
+    assert (fast.status == 0).all()
+    want = np.concatenate([q.reshape(-1).view(np.uint8) for q in parts])
+    assert np.array_equal(fast.out[: want.size].cpu().numpy(), want)
+
+
 def test_unpack_from_pinned_tensors(cuda):
     """unpack() straight from pinned host tensors (container + sidecar) gives the
     bytes-input result; a corrupted pinned payload raises the same error."""
