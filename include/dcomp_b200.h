@@ -249,10 +249,14 @@ int dc_fused_slice_bytes(void);
  * contract as dc_fused_decode_gemm (multiples of 256 instead of 512). */
 int dc_fused_item_rows(void);
 int dc_fused_item_k(void);
+/* `epi` (nullable): per layer {float *y; uint32_t *cnt; float scale; int32 n_slices}
+ * (dc_fused_epi_bytes() each): the fused dequant epilogue y = acc * scale written
+ * by the last K-slice item of each 1024-row block (cnt zeroed before first use). */
+int dc_fused_epi_bytes(void);
 int dc_fused_ring_gemm(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
                        const uint64_t *out_len, const uint8_t *codec, uint64_t chunk_size, const int64_t *seg_base,
                        const uint32_t *seg_state, const uint32_t *seg_off, const void *layers, const int32_t *items,
-                       int64_t n_items, int ntok, int32_t *status, void *stream);
+                       int64_t n_items, int ntok, int32_t *status, const void *epi, void *stream);
 int dc_fused_decode_gemm(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
                          const uint64_t *out_len, const uint8_t *codec, uint64_t chunk_size, const int64_t *seg_base,
                          const uint32_t *seg_state, const uint32_t *seg_off, const void *layers,

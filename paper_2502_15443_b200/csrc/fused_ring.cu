@@ -33,6 +33,17 @@ struct GemmTensorR {  // identical layout to GemmTensor (fused_gemm.cu)
     int32_t k;
 };
 
+// Optional dequant epilogue per layer (W8A8 numerics, scaling.py:127-152):
+// y[t, n] = acc[t, n] * scale with scale = sx * sw.  Accumulation stays exact
+// int32 across K-slices; the LAST item of a 1024-row block (per-block counter)
+// converts that block, so the launch emits fp32 outputs directly.
+struct RingEpi {
+    float* y;          // fp32 [ntok, n_rows] or null (int32 accumulators only)
+    uint32_t* cnt;     // per 1024-row block: items finished (zero between launches)
+    float scale;
+    int32_t n_slices;  // K-slices per row block
+};
+
 constexpr int kRDec = 16;                     // decoder warps
 constexpr int kRThreads = kRDec * 32;
 constexpr int kRTiles = 8;                    // row-tiles per item (1024 rows)
@@ -52,6 +63,7 @@ struct RingSmem {
     uint32_t cnt[kRSlots];
     uint32_t tmem;
     int32_t cur[2];
+    int32_t last;
 };
 
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&w)[4]) {
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
     const uint64_t* __restrict__ out_len, const uint8_t* __restrict__ codec, uint64_t chunk_size,
     const int64_t* __restrict__ seg_base, const uint32_t* __restrict__ seg_state,
     const uint32_t* __restrict__ seg_off, const GemmTensorR* __restrict__ tens, const int4* __restrict__ items,
-    int n_items, int ntok, int32_t* __restrict__ status, uint32_t one) {
+    int n_items, int ntok, int32_t* __restrict__ status, uint32_t one, const RingEpi* __restrict__ epi) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const FmaK fk = fma_consts(one);
     RingSmem& S = *reinterpret_cast<RingSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -441,6 +453,26 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
             }
         }
         tc_fence_before();
+        if (epi != nullptr && epi[it.x].y != nullptr) {  // uniform per item
+            const RingEpi E = epi[it.x];
+            const int blk = m0 / (kRTiles * 128);
+            __syncthreads();  // every thread's accumulator atomics are issued
+            if (threadIdx.x == 0) {
+                __threadfence();
+                S.last = atomicAdd(&E.cnt[blk], 1u) == (uint32_t)E.n_slices - 1;
+            }
+            __syncthreads();
+            if (S.last) {
+                __threadfence();
+                const int rows = min(kRTiles * 128, T.n_rows - m0);
+                for (int i = threadIdx.x; i < rows * ntok; i += kRThreads) {
+                    const int t = i / rows, r = m0 + i % rows;
+                    const int32_t a = __ldcg(&T.acc[(int64_t)t * T.n_rows + r]);
+                    E.y[(int64_t)t * T.n_rows + r] = (float)a * E.scale;
+                }
+                if (threadIdx.x == 0) E.cnt[blk] = 0;  // ready for the next launch
+            }
+        }
     }
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, 512);
@@ -452,6 +484,7 @@ using namespace dc;
 
 extern "C" int dc_fused_item_rows(void) { return kRTiles * 128; }
 extern "C" int dc_fused_item_k(void) { return kFK; }
+extern "C" int dc_fused_epi_bytes(void) { return (int)sizeof(RingEpi); }
 
 // items: int4 (layer, m0, k0, klen): 1024 rows from m0, K-slice [k0, k0+klen),
 // klen a multiple of 256 and <= dc_fused_item_k(); index seg_shift 8;
@@ -460,7 +493,7 @@ extern "C" int dc_fused_ring_gemm(const uint8_t* base, const uint64_t* blob_off,
                                   const uint64_t* out_len, const uint8_t* codec, uint64_t chunk_size,
                                   const int64_t* seg_base, const uint32_t* seg_state, const uint32_t* seg_off,
                                   const void* tens, const int32_t* items, int64_t n_items, int ntok,
-                                  int32_t* status, void* stream) {
+                                  int32_t* status, const void* epi, void* stream) {
     if (n_items <= 0 || ntok <= 0 || ntok > kRNT || chunk_size % 256) return DC_ERR_ARG;
     const size_t smem = sizeof(RingSmem) + 1024;
     static bool attr = false;
@@ -474,7 +507,8 @@ extern "C" int dc_fused_ring_gemm(const uint8_t* base, const uint64_t* blob_off,
     const int64_t grid = n_items < sms ? n_items : sms;
     k_fused_ring<<<(unsigned)grid, kRThreads, smem, (cudaStream_t)stream>>>(
         base, blob_off, blob_len, out_len, codec, chunk_size, seg_base, seg_state, seg_off,
-        reinterpret_cast<const GemmTensorR*>(tens), reinterpret_cast<const int4*>(items), (int)n_items, ntok, status, 1u);
+        reinterpret_cast<const GemmTensorR*>(tens), reinterpret_cast<const int4*>(items), (int)n_items, ntok, status, 1u,
+        reinterpret_cast<const RingEpi*>(epi));
     DC_CHECK_LAUNCH("k_fused_ring");
     return DC_OK;
 }

@@ -190,7 +190,11 @@ class FusedRing(FusedCompressed):
     ``check()``; ``run_checked()`` verifies and, if any chain broke (stale or
     corrupt index), recomputes the outputs exactly from the container."""
 
-    def __init__(self, image: torch.Tensor, jobs, index, chunk_size: int, shapes, t_offs, xs, ntok: int):
+    def __init__(self, image: torch.Tensor, jobs, index, chunk_size: int, shapes, t_offs, xs, ntok: int,
+                 scales=None):
+        """``scales`` (optional, one float per layer = sx * sw): also emit the
+        dequantized fp32 outputs ``ys[i]`` = acc * scale from the same launch
+        (fused dequant epilogue; the int32 accumulation stays exact)."""
         if index is None or index.seg_shift != 8:
             raise ValueError("fused path needs a split-point index with 256-symbol segments")
         rows_per = nv.call("dc_fused_item_rows")
@@ -203,7 +207,7 @@ class FusedRing(FusedCompressed):
         self.image, self.jobs, self.index, self.chunk_size = image, jobs, index, chunk_size
         self.t_offs = [int(t) for t in t_offs]
         self.layers = _LayerSet(shapes, t_offs, xs, ntok)
-        items = []
+        items, kss = [], []
         for li, (r, k) in enumerate(self.layers.shapes):
             # a chain's K-slice must never straddle a chunk boundary: use the
             # largest power of two <= kmax dividing K, the layer offset and the chunk size
@@ -213,17 +217,37 @@ class FusedRing(FusedCompressed):
             for m0 in range(0, r, rows_per):
                 for k0 in range(0, k, ks):
                     items.append((li, m0, k0, min(ks, k - k0)))
+            kss.append(ks)
         self.unit_t = torch.tensor(items, dtype=torch.int32, device=image.device)
         self.status = torch.zeros(max(jobs.n, 1), dtype=torch.int32, device=image.device)
+        self.ys, self.epi = None, None
+        if scales is not None:
+            dev = image.device
+            self.scales = [float(np.float32(x)) for x in scales]
+            self.ys = [torch.zeros((ntok, r), dtype=torch.float32, device=dev) for r, _ in self.layers.shapes]
+            nblk = [-(-r // rows_per) for r, _ in self.layers.shapes]
+            self.counters = torch.zeros(sum(nblk), dtype=torch.int32, device=dev)
+            cnt_off = np.concatenate([[0], np.cumsum(nblk)[:-1]]).astype(np.int64)
+            dt = np.dtype([("y", "<u8"), ("cnt", "<u8"), ("scale", "<f4"), ("n_slices", "<i4")])
+            assert dt.itemsize == nv.call("dc_fused_epi_bytes")
+            e = np.zeros(len(self.layers.shapes), dtype=dt)
+            e["y"] = [y.data_ptr() for y in self.ys]
+            e["cnt"] = [self.counters.data_ptr() + 4 * int(o) for o in cnt_off]
+            e["scale"] = np.asarray(scales, dtype=np.float32)
+            e["n_slices"] = [-(-k // ks) for (_, k), ks in zip(self.layers.shapes, kss)]
+            self.epi = torch.from_numpy(e.view(np.uint8).copy()).to(dev)
 
     def run(self) -> None:
         self.layers.acc_flat.zero_()
         self.status.zero_()
+        if self.epi is not None:
+            self.counters.zero_()
         j, ix = self.jobs, self.index
         nv.call("dc_fused_ring_gemm", self.image.data_ptr(), j.d_blob_off.data_ptr(), j.d_blob_len.data_ptr(),
                 j.d_out_len.data_ptr(), j.d_codec.data_ptr(), self.chunk_size, ix.d_seg_base.data_ptr(),
                 ix.d_state.data_ptr(), ix.d_off.data_ptr(), self.layers.tens.data_ptr(), self.unit_t.data_ptr(),
-                self.unit_t.shape[0], self.layers.ntok, self.status.data_ptr(), nv.stream_ptr())
+                self.unit_t.shape[0], self.layers.ntok, self.status.data_ptr(),
+                self.epi.data_ptr() if self.epi is not None else None, nv.stream_ptr())
 
     def run_checked(self) -> bool:
         """run(), verify every chain (one host sync) and fall back to the exact
@@ -243,4 +267,7 @@ class FusedRing(FusedCompressed):
         gi = GroupedInt8(views, self.layers.xs, self.layers.ntok)
         gi.run()
         self.layers.acc_flat.copy_(gi.layers.acc_flat)
+        if self.ys is not None:
+            for y, acc, sc in zip(self.ys, self.accs, self.scales):
+                y.copy_(acc.to(torch.float32) * sc)
         return False

@@ -76,7 +76,8 @@ SIGNATURES: dict[str, list] = {
     "dc_fused_decode_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P],
     "dc_fused_item_rows": [],
     "dc_fused_item_k": [],
-    "dc_fused_ring_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P],
+    "dc_fused_ring_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P, _P],
+    "dc_fused_epi_bytes": [],
 }
 _RESTYPES = {"dc_last_error": ctypes.c_char_p}
 

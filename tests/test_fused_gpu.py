@@ -140,3 +140,30 @@ def test_fused_ring_checked_fallback(cuda):
     assert not fr.run_checked()
     for w, x, acc in zip(ws, xs, fr.accs):
         assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
+
+
+def test_fused_ring_dequant_epilogue(cuda):
+    """decompress -> dequant -> W8A8 in one launch: fp32 outputs y = acc * (sx*sw)
+    equal the exact int32 product scaled in fp32, and match the f64 W8A8 value
+    within rtol 1e-6 (scaling.py:127-152 numerics)."""
+    from paper_2502_15443_b200 import container
+    from paper_2502_15443_b200.gemm import FusedRing
+    g = torch.Generator().manual_seed(11)
+    shapes = [(2048, 1024), (1024, 4096)]  # several K-slices and row blocks per layer
+    ws = [torch.round(torch.randn(r, k, generator=g) * 20).clamp_(-127, 127).to(torch.int8) for r, k in shapes]
+    xs = [torch.randint(-127, 128, (4, k), generator=g, dtype=torch.int8) for _, k in shapes]
+    scales = [3.1e-4, 7.7e-5]
+    payload = torch.cat([w.reshape(-1).view(torch.uint8) for w in ws]).cuda()
+    t_offs = np.concatenate([[0], np.cumsum([w.numel() for w in ws])[:-1]])
+    chunk = 1 << 23
+    image, enc, entries = container.pack_device(payload, b"\x00" * 8, chunk, None, seg_shift=8)
+    jobs = container.jobs_for(entries, image.device)
+    fr = FusedRing(image, jobs, enc.index, chunk, shapes, t_offs, [x.cuda() for x in xs], 4, scales=scales)
+    for _ in range(2):  # counters reset between launches
+        assert fr.run_checked()
+        for w, x, acc, y, sc in zip(ws, xs, fr.accs, fr.ys, scales):
+            exact = x.long() @ w.long().T
+            assert torch.equal(acc.cpu().long(), exact)
+            assert torch.equal(y.cpu(), exact.to(torch.float32) * np.float32(sc))
+            ref = exact.to(torch.float64) * sc
+            assert torch.allclose(y.cpu().double(), ref, rtol=1e-6, atol=0)
