@@ -334,6 +334,41 @@ def _parse(data: bytes, total: int | None = None):
         raise UnsupportedVersionError(f"unsupported container version {version}")
     (hlen,) = cur.fmt("<I")
     chunk_size, directory = _parse_header(cur.take(hlen))
+    ent, start = _parse_table(data, cur, chunk_size, total)
+    _check_total(ent, directory)
+    return chunk_size, directory, ent, start
+
+
+def _check_total(ent, directory) -> None:
+    total = int(ent["uncomp_len"].sum(dtype=np.uint64)) if len(ent) else 0
+    want = sum(r * c for _, r, c, *_ in directory)
+    if total != want:
+        raise DataFormatError(f"chunks carry {total} bytes, directory declares {want}")
+
+
+def _parse_table_first(data: bytes, total: int):
+    """Chunk table of a container whose header body is parsed later (unpack
+    overlaps the header walk with the GPU pipeline): the same table checks as
+    _parse with chunk_size read from the raw header.  Any error here, or later
+    in the header, is re-raised by a full _parse so the reference's first-error
+    order holds.  Returns (chunk_size, ent, start, header bytes)."""
+    try:
+        if len(data) < 14 or data[:4] != MAGIC or struct.unpack_from("<H", data, 4)[0] != VERSION:
+            raise DataFormatError("prefix")
+        (hlen,) = struct.unpack_from("<I", data, 6)
+        if hlen < 12 or 10 + hlen > len(data):
+            raise DataFormatError("header")
+        (chunk_size,) = struct.unpack_from("<I", data, 10)
+        if chunk_size < 1:
+            raise DataFormatError("chunk size")
+        ent, start = _parse_table(data, _Cursor(data, 10 + hlen), chunk_size, total)
+        return chunk_size, ent, start, data[10:10 + hlen]
+    except DataFormatError:
+        _parse(data, total)  # raises the reference's first error
+        raise
+
+
+def _parse_table(data: bytes, cur: "_Cursor", chunk_size: int, total: int):
     (count,) = cur.fmt("<I")
     avail = (total - cur.pos) // _ENTRY.size
     if avail < count:
@@ -380,11 +415,7 @@ def _parse(data: bytes, total: int | None = None):
         raise TruncatedError(f"chunk payloads extend past end of file ({end} > {total})")
     if end < total:
         raise DataFormatError(f"{total - end} trailing bytes after last chunk")
-    total = int(ent["uncomp_len"].sum(dtype=np.uint64)) if count else 0
-    want = sum(r * c for _, r, c, *_ in directory)
-    if total != want:
-        raise DataFormatError(f"chunks carry {total} bytes, directory declares {want}")
-    return chunk_size, directory, ent, start
+    return ent, start
 
 
 def binding_of(data: bytes) -> int:
@@ -508,27 +539,42 @@ def unpack(data, index=None) -> ModelBundle:
         data = _file_bytes(data)
         head, total = data, len(data)
     LAST_UNPACK_MS.clear()
-    chunk_size, directory, ent, _ = _parse(head, total)
-    if len(ent) == 0:
-        return _bundle(directory, np.empty(0, np.uint8), chunk_size)
-    lap("parse")
     if index is not None:  # split-point path: H2D / decode / D2H pipelined per chunk group
+        # chunk table first: the GPU pipeline starts before the header body
+        # (names, stats, header CRC) is walked on the host
+        chunk_size, ent, _, hdr = _parse_table_first(head, total)
+        lap("table")
         jobs = jobs_for(ent)
-        if isinstance(index, (bytes, bytearray, memoryview, torch.Tensor)):
-            index = engine.SegmentIndex.from_bytes(index, jobs, binding_of(head))
+        if len(ent) and isinstance(index, (bytes, bytearray, memoryview, torch.Tensor)):
+            index = engine.SegmentIndex.from_bytes(index, jobs, binding_of(head), lazy=True)
         lap("index")
-        if index is not None:
+        if len(ent) and index is not None:
             pd = engine.PipelinedDecode(src if src is not None else np.frombuffer(data, np.uint8), jobs, index)
             lap("launch")
+            try:
+                _, directory = _parse_header(hdr)
+                _check_total(ent, directory)
+            except DataFormatError:
+                pd.finish()
+                _parse(head, total)  # the reference's first error
+                raise
+            lap("header")
             out = _bundle(directory, pd.host_out.numpy(), chunk_size)  # views; filled by the pipeline
             lap("bundle")
             _, status, crc = pd.finish()
             lap("pipeline")
+            if pd.marks is not None:
+                LAST_UNPACK_TIMELINE[:] = [("host:" + k, v, float("nan")) for k, v in LAST_UNPACK_MS.items()]
+                LAST_UNPACK_TIMELINE.extend(pd.timeline())
             raise_decode_errors(status)
             bad = np.nonzero(crc != ent["crc32"])[0]
             if len(bad):
                 raise ChecksumError(int(bad[0]))
             return out
+    chunk_size, directory, ent, _ = _parse(head, total)
+    if len(ent) == 0:
+        return _bundle(directory, np.empty(0, np.uint8), chunk_size)
+    lap("parse")
     base = nv.to_device_bytes(data)
     lap("h2d")
     res = decode_and_verify(base, ent, index=index)
@@ -541,6 +587,7 @@ def unpack(data, index=None) -> ModelBundle:
 
 
 LAST_UNPACK_MS: dict[str, float] = {}  # phase timings of the last unpack() (diagnostics)
+LAST_UNPACK_TIMELINE: list = []  # DCOMP_TIMELINE=1: per-stage (name, host ms, device ms)
 _PHASE_SYNC = os.environ.get("DCOMP_PHASE_SYNC") == "1"
 
 

@@ -82,6 +82,9 @@ class SegmentIndex:
     d_state: torch.Tensor      # int32 storage of u32 [n_segs]
     d_off: torch.Tensor        # int32 storage of u32 [n_segs]
     h_off: np.ndarray | None = None  # host copy of the offsets when already on the host
+    # lazy sidecar: pinned host bytes of (state, off) not yet copied; PipelinedDecode
+    # uploads each chunk group's split points just ahead of that group's stream bytes
+    pending: torch.Tensor | None = None
 
     @staticmethod
     def layout(out_len: np.ndarray, codec: np.ndarray, seg_shift: int) -> tuple[np.ndarray, int]:
@@ -104,7 +107,22 @@ class SegmentIndex:
     def nbytes(self) -> int:
         return 8 * self.n_segs
 
+    def upload_segments(self, s0: int, s1: int) -> None:
+        """Copy split points [s0, s1) of a lazy index on the current stream."""
+        if self.pending is None or s1 <= s0:
+            return
+        n = self.n_segs
+        self.d_state.view(torch.uint8)[4 * s0:4 * s1].copy_(self.pending[4 * s0:4 * s1], non_blocking=True)
+        self.d_off.view(torch.uint8)[4 * s0:4 * s1].copy_(self.pending[4 * n + 4 * s0:4 * n + 4 * s1],
+                                                          non_blocking=True)
+
+    def ensure_uploaded(self) -> None:
+        if self.pending is not None:
+            self.upload_segments(0, self.n_segs)
+            self.pending = None
+
     def host_arrays(self) -> tuple[np.ndarray, np.ndarray]:
+        self.ensure_uploaded()
         return (self.d_state[: self.n_segs].cpu().numpy().view(np.uint32),
                 self.d_off[: self.n_segs].cpu().numpy().view(np.uint32))
 
@@ -123,10 +141,11 @@ class SegmentIndex:
         return head + body + struct.pack("<I", zlib.crc32(body))
 
     @classmethod
-    def from_bytes(cls, buf, jobs: JobTable, binding: int, device=None) -> "SegmentIndex | None":
+    def from_bytes(cls, buf, jobs: JobTable, binding: int, device=None, lazy: bool = False) -> "SegmentIndex | None":
         """Load a sidecar (bytes-like, or a pinned CPU uint8 tensor that is
         copied to the device directly); None if it does not belong to this
-        container."""
+        container.  ``lazy`` (pinned tensor only): leave the copy to the
+        consumer (PipelinedDecode uploads it group by group)."""
         src = None
         if isinstance(buf, torch.Tensor):
             src, buf = buf, buf.numpy()
@@ -141,14 +160,18 @@ class SegmentIndex:
         if n != want or len(buf) != 22 + 8 * n + 4:
             return None
         dev = device or _dev()
+        pending = None
         if src is not None and src.is_pinned():
             d = nv.device_bytes(8 * n, dev)
-            d[:8 * n].copy_(src[22:22 + 8 * n], non_blocking=True)
+            if lazy:
+                pending = src[22:22 + 8 * n]
+            else:
+                d[:8 * n].copy_(src[22:22 + 8 * n], non_blocking=True)
         else:
             d = nv.to_device_bytes(np.frombuffer(buf, np.uint8, 8 * n, 22), dev)  # pinned, pipelined upload
         off = np.frombuffer(buf, np.uint32, n, 22 + 4 * n)
         return cls(shift, base, n, _t(base, torch.int64, dev), d[:4 * n].view(torch.int32),
-                   d[4 * n:8 * n].view(torch.int32), h_off=off)
+                   d[4 * n:8 * n].view(torch.int32), h_off=off, pending=pending)
 
     # ---- work decomposition -------------------------------------------------
     def tasks(self, jobs: JobTable, ok: np.ndarray, max_segs: int | None = None) -> torch.Tensor:
@@ -174,10 +197,12 @@ class SegmentIndex:
         # tasks whose staged stream bytes overflow shared memory are halved
         # (vectorized, level by level) until every task fits
         nmax = max(self.n_segs - 1, 0)
+        split = False
         for _ in range(32):
             big = (hi - lo + 15 > STAGE_CAP) & (cnt > 1)
             if not big.any():
                 break
+            split = True
             h = cnt[big] // 2
             k_chunk, k_s0, k_cnt, k_nsg, k_base, k_plen = (chunk[big], s0[big], cnt[big], nsg[big], base[big],
                                                            plen[big])
@@ -191,10 +216,16 @@ class SegmentIndex:
             lo = off[base + s0].astype(np.int64)
             end = s0 + cnt
             hi = np.where(end < nsg, off[np.minimum(base + end, nmax)].astype(np.int64), plen)
-        out = np.stack([chunk, s0, cnt, np.zeros_like(cnt)], axis=1).astype(np.int32)
-        out = out[np.lexsort((out[:, 1], out[:, 0]))]
-        self.last_tasks_host = np.ascontiguousarray(out)
-        return torch.from_numpy(self.last_tasks_host).to(_dev())
+        if split:  # back to (chunk, first segment) order
+            order = np.lexsort((s0, chunk))
+            chunk, s0, cnt = chunk[order], s0[order], cnt[order]
+        # pinned + async: a pageable copy would block the host behind any
+        # large H2D already queued on the copy engine
+        pin = torch.zeros((len(chunk), 4), dtype=torch.int32, pin_memory=True)
+        out = pin.numpy()
+        out[:, 0], out[:, 1], out[:, 2] = chunk, s0, cnt
+        self.last_tasks_host = out
+        return pin.to(_dev(), non_blocking=True)
 
 
 # ------------------------------------------------------------------ decode
@@ -393,6 +424,9 @@ def _streams(dev):
     return _SIDE_STREAMS[dev]
 
 
+_TIMELINE = os.environ.get("DCOMP_TIMELINE") == "1"
+
+
 class PipelinedDecode:
     """Host container bytes -> host decoded bytes: H2D of chunk group g+1,
     validate + split-point decode + CRC of group g and D2H of group g-1
@@ -402,6 +436,8 @@ class PipelinedDecode:
     be wrapped (views) before ``finish()``, which waits, re-decodes chunks
     whose split-point chain broke (exact serial kernel) and returns
     (decoded host bytes, per-chunk status, per-chunk CRC32)."""
+
+    LOOKAHEAD = int(os.environ.get("DCOMP_H2D_LOOKAHEAD", "2"))
 
     def __init__(self, src, jobs: JobTable, index: SegmentIndex, groups: int = 16):
         dev = jobs.d_blob_off.device
@@ -417,20 +453,25 @@ class PipelinedDecode:
         self.host_out = host_out = torch.empty(jobs.total_out, dtype=torch.uint8, pin_memory=True)
         self.status = status = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
         self.crc = crc = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
-        tasks = index.tasks(jobs, np.ones(n, bool))
-        t_host = index.last_tasks_host
-        t_chunk = t_host[:, 0] if len(t_host) else np.zeros(0, np.int32)
-        # contiguous chunk groups of ~equal file bytes
+        self.marks = marks = [] if _TIMELINE else None
+        self._mark("init", s_comp)
+        # contiguous chunk groups: a short ramp (1/128, 1/32, 1/16 of the file)
+        # so the first D2H starts early, then ~equal file bytes
         ends = jobs.blob_off + jobs.blob_len
+        fr = np.array([1 / 128, 1 / 32, 1 / 16]) if groups >= 8 else np.zeros(0)
+        fr = np.concatenate([fr, np.full(groups - len(fr), (1 - fr.sum()) / (groups - len(fr)))])
         cuts = np.searchsorted(np.cumsum(jobs.blob_len.astype(np.float64)),
-                               np.linspace(0, float(jobs.blob_len.sum()), groups + 1)[1:-1]).tolist()
-        bounds = sorted(set([0] + [min(max(c, 0), n) for c in cuts] + [n]))
-        sp_comp = s_comp.cuda_stream
-        self.max_len = max_len = int(jobs.out_len.max()) if n else 0
-        self._keep = [tasks]
-        for g0, g1 in zip(bounds, bounds[1:]):
-            if g1 <= g0:
-                continue
+                               np.cumsum(fr)[:-1] * float(jobs.blob_len.sum())).tolist()
+        bounds = sorted(set([0] + [min(max(c + 1, 1), n) for c in cuts] + [n]))
+        grp = list(zip(bounds, bounds[1:]))
+        lazy = index.pending is not None
+        seg_end = np.append(index.seg_base, index.n_segs)
+        ev_h2d, ev_d2h = {}, {}
+
+        def issue_h2d(i):
+            # H2D runs at most LOOKAHEAD groups ahead of the D2H: the link is
+            # shared by both directions and the (larger) D2H is the long pole
+            g0, g1 = grp[i]
             f0, f1 = int(jobs.blob_off[g0]), int(ends[g1 - 1])
             if pinned:
                 stage = src[f0:f1]
@@ -438,20 +479,36 @@ class PipelinedDecode:
                 stage = torch.empty(f1 - f0, dtype=torch.uint8, pin_memory=True)
                 nv._parallel_copy(stage.numpy(), src[f0:f1], piece=8 << 20)
             with torch.cuda.stream(s_copy):
+                if i - self.LOOKAHEAD in ev_d2h:
+                    s_copy.wait_event(ev_d2h[i - self.LOOKAHEAD])
+                self._mark(f"h2d{g0}", s_copy)
+                if lazy:
+                    index.upload_segments(int(seg_end[g0]), int(seg_end[g1]))
                 image[f0:f1].copy_(stage, non_blocking=True)
-                ev_h2d = torch.cuda.Event()
-                ev_h2d.record(s_copy)
-            s_comp.wait_event(ev_h2d)
+                ev_h2d[i] = torch.cuda.Event()
+                ev_h2d[i].record(s_copy)
+                self._mark(f"h2d{g0}_end", s_copy)
+
+        for i in range(min(self.LOOKAHEAD, len(grp))):
+            issue_h2d(i)
+        sp_comp = s_comp.cuda_stream
+        self.max_len = max_len = int(jobs.out_len.max()) if n else 0
+        self._keep = []
+        for i, (g0, g1) in enumerate(grp):
+            sel = np.zeros(n, bool)
+            sel[g0:g1] = True
+            tasks = index.tasks(jobs, sel)  # per group: the first decode issues early
+            self._keep.append(tasks)
+            s_comp.wait_event(ev_h2d[i])
             k = g1 - g0
             off8 = lambda t: t.data_ptr() + 8 * g0  # noqa: E731
             nv.call("dc_ans_validate", image.data_ptr(), off8(jobs.d_blob_off), off8(jobs.d_blob_len),
                     off8(jobs.d_out_len), jobs.d_codec.data_ptr() + g0, k, status.data_ptr() + 4 * g0, sp_comp)
-            t0, t1 = np.searchsorted(t_chunk, g0), np.searchsorted(t_chunk, g1)
-            if t1 > t0:
+            if tasks.shape[0]:
                 nv.call(segment_kernel(jobs), image.data_ptr(), jobs.d_blob_off.data_ptr(),
                         jobs.d_blob_len.data_ptr(), jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(),
                         index.seg_shift, index.d_seg_base.data_ptr(), index.d_state.data_ptr(),
-                        index.d_off.data_ptr(), tasks[t0:t1].data_ptr(), int(t1 - t0), out.data_ptr(),
+                        index.d_off.data_ptr(), tasks.data_ptr(), tasks.shape[0], out.data_ptr(),
                         status.data_ptr(), sp_comp)
             nv.call("dc_store_copy", image.data_ptr(), off8(jobs.d_blob_off), off8(jobs.d_out_off),
                     off8(jobs.d_out_len), jobs.d_codec.data_ptr() + g0, k, out.data_ptr(), sp_comp)
@@ -462,8 +519,38 @@ class PipelinedDecode:
             s_out.wait_event(ev_dec)
             o0 = int(jobs.out_off[g0])
             o1 = int(jobs.out_off[g1 - 1] + jobs.out_len[g1 - 1])
+            self._mark(f"dec{g0}_end", s_comp)
             with torch.cuda.stream(s_out):
+                self._mark(f"d2h{g0}", s_out)
                 host_out[o0:o1].copy_(out[o0:o1], non_blocking=True)
+                ev_d2h[i] = torch.cuda.Event()
+                ev_d2h[i].record(s_out)
+                self._mark(f"d2h{g0}_end", s_out)
+            if i + self.LOOKAHEAD < len(grp):
+                issue_h2d(i + self.LOOKAHEAD)
+        if lazy:  # every group's split points are in flight on s_copy
+            index.pending = None
+            s_comp.wait_stream(s_copy)
+        self._mark("issued", None)
+
+    def _mark(self, name, stream):
+        """DCOMP_TIMELINE=1: device events (and host issue times) per pipeline stage."""
+        if self.marks is None:
+            return
+        import time
+        ev = None
+        if stream is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+        self.marks.append((name, time.perf_counter(), ev))
+
+    def timeline(self) -> list[tuple[str, float, float]]:
+        """(stage, host issue ms, device ms) relative to construction; after finish()."""
+        if not self.marks:
+            return []
+        h0, e0 = self.marks[0][1], self.marks[0][2]
+        return [(nm, (h - h0) * 1e3, e0.elapsed_time(ev) if ev is not None else float("nan"))
+                for nm, h, ev in self.marks]
 
     def finish(self):
         jobs, n, out, host_out = self.jobs, self.jobs.n, self.out, self.host_out

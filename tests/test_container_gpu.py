@@ -146,6 +146,46 @@ def test_unpack_from_pinned_tensors(cuda):
         container.unpack(pin, index=pside)
 
 
+def test_structural_errors_with_sidecar(cuda):
+    """unpack(data, index=sidecar) starts the GPU pipeline from the chunk table
+    before walking the header body; header / table / length damage must still
+    raise exactly what the index-less path (full ordered parse) raises."""
+    from paper_2502_15443_b200 import container
+    tensors, stats = small_model(cuda, rows=300)
+    data, index = container.pack_indexed(tensors, stats, chunk_size=8192, seg_shift=8)
+    side = index.to_bytes(container.binding_of(data))
+    (hlen,) = struct.unpack_from("<I", data, 6)
+    (count,) = struct.unpack_from("<I", data, 10 + hlen)
+    prefix = 14 + hlen + 29 * count
+    rng = np.random.default_rng(12)
+
+    def outcome(fn):
+        try:
+            fn()
+            return None
+        except cuda.DcompError as e:
+            return type(e).__name__, str(e)
+
+    mutants = []
+    for _ in range(60):
+        b = bytearray(data)
+        pos = int(rng.integers(10, 10 + hlen - 4))  # header body: the sidecar still binds
+        b[pos] ^= 1 << int(rng.integers(0, 8))
+        mutants.append(bytes(b))
+    for _ in range(20):
+        b = bytearray(data)
+        b[int(rng.integers(0, prefix))] ^= 1 << int(rng.integers(0, 8))
+        mutants.append(bytes(b))
+    mutants += [data[:-1], data + b"\x00", data[:prefix + 5]]
+    raised = 0
+    for m in mutants:
+        want = outcome(lambda: container.unpack(m))
+        got = outcome(lambda: container.unpack(m, index=side))
+        assert got == want
+        raised += want is not None
+    assert raised >= 70
+
+
 def test_sidecar_roundtrip(cuda, tmp_path):
     rng = np.random.default_rng(5)
     q = np.clip(np.round(rng.normal(0, 9, (200, 1000))), -127, 127).astype(np.int8)
