@@ -155,10 +155,11 @@ __device__ __forceinline__ uint32_t dec_sym(uint32_t& x, uint32_t& s, uint32_t v
 // saturates; IMAD / IMAD.HI by a constant held in a register (opaque to ptxas,
 // so it cannot turn them back into shifts) run on the FMA pipe instead.
 struct FmaK {
-    uint32_t c4, c2p12, c2p24, c2p20, cm4096, cm16384;
+    uint32_t c4, c2p12, c2p24, c2p20, cm4096, cm16384, c1;
 };
 __device__ __forceinline__ FmaK fma_consts(uint32_t one) {
-    return FmaK{4u * one, 4096u * one, (1u << 24) * one, (1u << 20) * one, 0u - 4096u * one, 0u - 16384u * one};
+    return FmaK{4u * one, 4096u * one, (1u << 24) * one, (1u << 20) * one, 0u - 4096u * one, 0u - 16384u * one,
+                one};
 }
 
 // Slot address without the ALU mask: with t = (x >> 12) - 4096 (needed for the
@@ -222,6 +223,24 @@ __device__ __forceinline__ void win_advance(Win& w, uint32_t s) {
         "and.b32 %3, %3, 31;\n\t}"
         : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
         : "r"(s));
+}
+
+// win_advance with the window moves and the offset wrap on the FMA pipe
+// (IMAD by the opaque 1 / VIADD) instead of SEL + LOP3 on the ALU pipe, which
+// the decode loop saturates.  o stays in [0, 32): o + 8s - 8*kSelBase, minus
+// 32 when a word was crossed.
+__device__ __forceinline__ void win_advance(Win& w, uint32_t s, const FmaK& k) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "mad.lo.u32 %3, %4, 8, %3;\n\t"
+        "setp.ge.u32 q, %3, 0x10840;\n\t"
+        "@q mad.lo.u32 %0, %1, %5, 0;\n\t"
+        "@q mad.lo.u32 %2, %5, 4, %2;\n\t"
+        "@q ld.shared.u32 %1, [%2];\n\t"
+        "@q mad.lo.u32 %3, %5, -32, %3;\n\t"
+        "add.u32 %3, %3, -67616;\n\t}"
+        : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
+        : "r"(s), "r"(k.c1));
 }
 
 // Same inside a 128-byte ring (fused kernel): the word address wraps.

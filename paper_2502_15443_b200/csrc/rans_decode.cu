@@ -311,7 +311,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
                     w[u][v >> 2] = (v & 2) ? __byte_perm(w[u][v >> 2], t, 0x5410) : t;
                 }
 #pragma unroll
-                for (int u = 0; u < NU; ++u) win_advance(W[u], sel[u]);
+                for (int u = 0; u < NU; ++u) win_advance(W[u], sel[u], fk);
             }
         } else {
 #pragma unroll

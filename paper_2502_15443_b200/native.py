@@ -13,7 +13,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdcomp_b200.so")
+LIB_PATH = os.environ.get("DCOMP_LIB") or os.path.join(HERE, "libdcomp_b200.so")  # DCOMP_LIB: A/B builds
 
 READ_SLACK = 16384  # DC_READ_SLACK
 
