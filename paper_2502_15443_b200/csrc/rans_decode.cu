@@ -286,6 +286,20 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
         }
         win_init(W[u], p);
     }
+    // Fast flush when every segment this warp writes is a whole K-byte
+    // segment and the output is 16-B aligned (all but a chunk's last task):
+    // per-line destinations are precomputed 32-bit offsets from the task base.
+    bool ff = out_aligned;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) ff = ff && (warp * 32 + lane + u * kDecThreads < ns) && n[u] == K;
+    const bool fast_flush = __all_sync(0xffffffffu, ff);
+    uint8_t* const tb = obase + ((uint64_t)(uint32_t)s0 << seg_shift);
+    uint32_t dk[NU * 2];
+#pragma unroll
+    for (int k = 0; k < NU * 2; ++k) {
+        const int pc = k * 32 + lane;
+        dk[k] = ((uint32_t)(warp * 32 + ((pc >> 1) & 31) + (pc >> 6) * kDecThreads) << seg_shift) + (pc & 1) * 16;
+    }
     for (int g = 0; g < G; ++g) {
         const uint32_t g0 = (uint32_t)g << 4;
         uint32_t w[NU][4];
@@ -337,6 +351,16 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
         if (slot == 1) {  // G is even (K >= 64)
             __syncwarp();
             const uint32_t line0 = (uint32_t)(g >> 1) * kOutLine;
+            if (fast_flush) {
+#pragma unroll
+                for (int k = 0; k < NU * 2; ++k) {
+                    const int pc = k * 32 + lane;
+                    st_na_v4(tb + dk[k] + line0,
+                             *reinterpret_cast<const uint4*>(ob + swz((pc >> 6) * 32 + ((pc >> 1) & 31), pc & 1)));
+                }
+                __syncwarp();
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < NU * 2; ++k) {
                 const int pc = k * 32 + lane;
