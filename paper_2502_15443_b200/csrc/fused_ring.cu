@@ -183,6 +183,23 @@ __device__ __forceinline__ void fwin_advance(Chain& c, uint32_t s) {
         : "r"(c.rb), "r"(s));
 }
 
+// fwin_advance with the moves and the offset wrap on the FMA pipe (see
+// win_advance(Win&, s, FmaK) in rans_common.cuh)
+__device__ __forceinline__ void fwin_advance(Chain& c, uint32_t s, const FmaK& k) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 a;\n\t"
+        "mad.lo.u32 %3, %5, 8, %3;\n\t"
+        "setp.ge.u32 q, %3, 0x10840;\n\t"
+        "@q mad.lo.u32 %0, %1, %6, 0;\n\t"
+        "@q mad.lo.u32 %2, %6, 4, %2;\n\t"
+        "lop3.b32 a, %2, 127, %4, 0xEA;\n\t"
+        "@q ld.shared.u32 %1, [a];\n\t"
+        "@q mad.lo.u32 %3, %6, -32, %3;\n\t"
+        "add.u32 %3, %3, -67616;\n\t}"
+        : "+r"(c.w0), "+r"(c.w1), "+r"(c.pr), "+r"(c.o)
+        : "r"(c.rb), "r"(s), "r"(k.c1));
+}
+
 __device__ __forceinline__ void ring_refill(Chain& c, uint32_t ring_base) {
     if (c.mode <= 1 && ring_avail(c) < 96u) {
         cp_async16(ring_base + ((uint32_t)c.gfill & 127u), reinterpret_cast<const void*>(c.gfill));
@@ -365,7 +382,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
                             w[u][v >> 2] = (v & 2) ? __byte_perm(w[u][v >> 2], t, 0x5410) : t;
                         }
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) fwin_advance(ch[u], sel[u]);
+                        for (int u = 0; u < 2; ++u) fwin_advance(ch[u], sel[u], fk);
                     }
                 } else if (fast) {
 #pragma unroll
