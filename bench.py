@@ -53,6 +53,7 @@ def parse_args():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-tp-shard", action="store_true", help="skip the single-GPU TP-8 shard measurement")
     return p.parse_args()
 
 
@@ -388,6 +389,20 @@ def main():
             tp = tp_step.measure(tps, iters=10)
             tp.update({"model": "llama-13b", "tp": world, "ntok": 1, "fused_equals_int8": ok,
                        "int8_tok_s": 1e3 / tp["int8_step_ms"], "compressed_tok_s": 1e3 / tp["compressed_fused_step_ms"]})
+            del tps
+            torch.cuda.empty_cache()
+        except Exception as e:  # report, never hide
+            tp = {"error": repr(e)[:300]}
+    elif not args.no_tp_shard:
+        # one GPU: rank 0's shard of the TP-8 split, compute only (the all-reduce
+        # needs the other ranks; its share is measured under torchrun)
+        try:
+            from paper_2502_15443_b200 import tp_step
+            tps = tp_step.TPDecodeStep("llama-13b", 8, 0, ntok=1, device=dev)
+            ok = tp_step.check_local(tps)
+            tp = tp_step.measure_local(tps, iters=10)
+            tp.update({"model": "llama-13b", "tp": 8, "rank": 0, "ntok": 1, "scope": "rank-0 shard compute only",
+                       "fused_equals_int8": ok})
             del tps
             torch.cuda.empty_cache()
         except Exception as e:  # report, never hide

@@ -230,6 +230,11 @@ int dc_w8a8_grouped_maps(const int8_t *const *w_host, const int8_t *const *x_hos
 /* Uncompressed INT8 weights: TMA -> smem -> tcgen05.mma.kind::i8 -> TMEM. */
 int dc_w8a8_grouped(const void *maps, const void *layers, const int32_t *units, int64_t n_units, int ntok,
                     void *stream);
+/* Persistent grouped W8A8: one CTA per SM looping over the unit table (TMA
+ * stream continuous across units, double-buffered TMEM accumulators);
+ * `max_ctas` > 0 caps the grid (= SMs used), 0 = every SM. */
+int dc_w8a8_grouped_persist(const void *maps, const void *tens, const int32_t *units, int64_t n_units, int ntok,
+                            int max_ctas, void *stream);
 
 /* Fused decompress -> W8A8 straight from DCC1 chunks (north-star kernel 3):
  * each thread decodes one 256-symbol segment of one weight row from its
@@ -251,12 +256,15 @@ int dc_fused_item_rows(void);
 int dc_fused_item_k(void);
 /* `epi` (nullable): per layer {float *y; uint32_t *cnt; float scale; int32 n_slices}
  * (dc_fused_epi_bytes() each): the fused dequant epilogue y = acc * scale written
- * by the last K-slice item of each 1024-row block (cnt zeroed before first use). */
+ * by the last K-slice item of each 1024-row block (cnt zeroed before first use).
+ * `max_ctas` > 0 caps the persistent grid (one CTA per SM) so a concurrent INT8
+ * GEMM on another stream gets the remaining SMs; 0 = every SM. */
 int dc_fused_epi_bytes(void);
 int dc_fused_ring_gemm(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
                        const uint64_t *out_len, const uint8_t *codec, uint64_t chunk_size, const int64_t *seg_base,
                        const uint32_t *seg_state, const uint32_t *seg_off, const void *layers, const int32_t *items,
-                       int64_t n_items, int ntok, int32_t *status, const void *epi, void *stream);
+                       int64_t n_items, int ntok, int32_t *status, const void *epi, int max_ctas,
+                       void *stream);
 int dc_fused_decode_gemm(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
                          const uint64_t *out_len, const uint8_t *codec, uint64_t chunk_size, const int64_t *seg_base,
                          const uint32_t *seg_state, const uint32_t *seg_off, const void *layers,

@@ -145,6 +145,119 @@ __global__ void __launch_bounds__(kGrThreads, 1) k_w8a8_grouped(const CUtensorMa
     if (warp == 2) tmem_dealloc(tmem, 32);
 }
 
+// ====================================================== grouped, persistent
+// One CTA per SM (221 KB of smem: 12 TMA stages of W + X), looping over the
+// unit table with stride gridDim.x.  Warp 0 streams W/X tiles with TMA
+// continuously across units, warp 1 issues the MMAs into one of two TMEM
+// accumulators (double-buffered per unit), warps 2-5 drain the other one
+// (tcgen05.ld -> int32 atomics) while the next unit streams.  Because one CTA
+// fills an SM, a capped grid occupies exactly that many SMs: the rest are
+// left to a concurrent fused decode kernel (MixedStep).
+constexpr int kPThreads = 192;
+constexpr int kPStages = 12;
+
+struct PersistSmem {
+    alignas(1024) uint8_t a[kPStages][128 * kGrBK];
+    alignas(1024) uint8_t b[kPStages][kGrNT * kGrBK];
+    uint64_t full[kPStages];
+    uint64_t empty[kPStages];
+    uint64_t accf[2];  // accumulator ub ready (MMA commit)
+    uint64_t acce[2];  // accumulator ub drained (4 epilogue warps)
+    uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(kPThreads, 1) k_w8a8_persist(const CUtensorMap* __restrict__ maps,
+                                                                const GemmTensor* __restrict__ tens,
+                                                                const int4* __restrict__ units, int n_units,
+                                                                int ntok) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    PersistSmem& S = *reinterpret_cast<PersistSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr uint32_t kBytes = 128 * kGrBK + kGrNT * kGrBK;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kPStages; ++s) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&S.accf[b], 1);
+            mbar_init(&S.acce[b], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(&S.tmem, 32);  // two 16-column int32 accumulators
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = S.tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int ui = blockIdx.x; ui < n_units; ui += gridDim.x) {
+                const int4 u = units[ui];
+                const CUtensorMap* tw = maps + 2 * u.x;
+                const CUtensorMap* tx = maps + 2 * u.x + 1;
+                const int nkb = u.w / kGrBK;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const uint32_t s = it % kPStages;
+                    mbar_wait(&S.empty[s], ((it / kPStages) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&S.full[s], kBytes);
+                    tma_load_2d(S.a[s], tw, u.z + kb * kGrBK, u.y, &S.full[s]);
+                    tma_load_2d(S.b[s], tx, u.z + kb * kGrBK, 0, &S.full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_i8(128, kGrNT);
+            uint32_t it = 0, j = 0;
+            for (int ui = blockIdx.x; ui < n_units; ui += gridDim.x, ++j) {
+                const int nkb = units[ui].w / kGrBK;
+                const uint32_t ub = j & 1;
+                mbar_wait(&S.acce[ub], ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+                tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const uint32_t s = it % kPStages;
+                    mbar_wait(&S.full[s], (it / kPStages) & 1);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(S.a[s]), b0 = smem_u32(S.b[s]);
+#pragma unroll
+                    for (int k = 0; k < kGrBK / 32; ++k)
+                        mma_i8(tmem + ub * kGrNT, sw128_kmajor_desc(a0 + 32 * k), sw128_kmajor_desc(b0 + 32 * k),
+                               idesc, (kb | k) != 0);
+                    mma_commit(&S.empty[s]);
+                }
+                mma_commit(&S.accf[ub]);
+            }
+        }
+    } else {
+        const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31 (warps 2,3,4,5 -> 2,3,0,1)
+        uint32_t j = 0;
+        for (int ui = blockIdx.x; ui < n_units; ui += gridDim.x, ++j) {
+            const int4 u = units[ui];
+            const uint32_t ub = j & 1;
+            mbar_wait(&S.accf[ub], (j >> 1) & 1);
+            tc_fence_after();
+            uint32_t v[16];
+            tmem_ld_32x32b_x16(tmem + ((uint32_t)(quarter * 32) << 16) + ub * kGrNT, v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.acce[ub]);
+            const GemmTensor T = tens[u.x];
+            const int row = u.y + quarter * 32 + lane;
+            if (row < T.n_rows) {
+#pragma unroll
+                for (int t = 0; t < kGrNT; ++t)
+                    if (t < ntok) atomicAdd(&T.acc[(int64_t)t * T.n_rows + row], (int32_t)v[t]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 32);
+}
+
 // ================================================================== fused
 constexpr int kFThreads = 256;   // 8 warps: TMEM lane quarter = warp & 3, segment = warp >> 2
 constexpr int kFSlice = 512;     // K bytes per unit (2 segments of 256 per row)
@@ -373,6 +486,29 @@ extern "C" int dc_w8a8_grouped(const void* maps, const void* tens, const int32_t
         reinterpret_cast<const CUtensorMap*>(maps), reinterpret_cast<const GemmTensor*>(tens),
         reinterpret_cast<const int4*>(units), ntok);
     DC_CHECK_LAUNCH("k_w8a8_grouped");
+    return DC_OK;
+}
+
+// Persistent variant of dc_w8a8_grouped: min(n_units, SMs, max_ctas > 0 ?
+// max_ctas : SMs) CTAs, one per SM.
+extern "C" int dc_w8a8_grouped_persist(const void* maps, const void* tens, const int32_t* units, int64_t n_units,
+                                       int ntok, int max_ctas, void* stream) {
+    if (n_units <= 0 || ntok <= 0 || ntok > kGrNT) return DC_ERR_ARG;
+    const size_t smem = sizeof(PersistSmem) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_w8a8_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
+    const int64_t grid = n_units < sms ? n_units : sms;
+    k_w8a8_persist<<<(unsigned)grid, kPThreads, smem, (cudaStream_t)stream>>>(
+        reinterpret_cast<const CUtensorMap*>(maps), reinterpret_cast<const GemmTensor*>(tens),
+        reinterpret_cast<const int4*>(units), (int)n_units, ntok);
+    DC_CHECK_LAUNCH("k_w8a8_persist");
     return DC_OK;
 }
 

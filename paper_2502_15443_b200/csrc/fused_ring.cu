@@ -510,7 +510,7 @@ extern "C" int dc_fused_ring_gemm(const uint8_t* base, const uint64_t* blob_off,
                                   const uint64_t* out_len, const uint8_t* codec, uint64_t chunk_size,
                                   const int64_t* seg_base, const uint32_t* seg_state, const uint32_t* seg_off,
                                   const void* tens, const int32_t* items, int64_t n_items, int ntok,
-                                  int32_t* status, const void* epi, void* stream) {
+                                  int32_t* status, const void* epi, int max_ctas, void* stream) {
     if (n_items <= 0 || ntok <= 0 || ntok > kRNT || chunk_size % 256) return DC_ERR_ARG;
     const size_t smem = sizeof(RingSmem) + 1024;
     static bool attr = false;
@@ -521,6 +521,7 @@ extern "C" int dc_fused_ring_gemm(const uint8_t* base, const uint64_t* blob_off,
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;  // leave SMs to a concurrent INT8 GEMM
     const int64_t grid = n_items < sms ? n_items : sms;
     k_fused_ring<<<(unsigned)grid, kRThreads, smem, (cudaStream_t)stream>>>(
         base, blob_off, blob_len, out_len, codec, chunk_size, seg_base, seg_state, seg_off,

@@ -77,6 +77,17 @@ import numpy as np  # noqa: E402
 _GT_DTYPE = np.dtype([("x", "<u8"), ("acc", "<u8"), ("t_off", "<i8"), ("n_rows", "<i4"), ("k", "<i4")])
 
 
+def _equal_kslice(k: int, target: int) -> int:
+    """Largest multiple of KB dividing k and <= target (k itself if k <= target)."""
+    if k <= target:
+        return k
+    best = KB
+    for ks in range(KB, target + 1, KB):
+        if k % ks == 0:
+            best = ks
+    return best
+
+
 class _LayerSet:
     """Per-layer activations and int32 accumulators shared by the grouped
     INT8 GEMM and the fused decode GEMM (one launch covers every layer)."""
@@ -135,15 +146,24 @@ class GroupedInt8:
             raise nv.NativeError(f"dc_w8a8_grouped_maps failed ({rc})")
         self.maps = torch.from_numpy(maps.copy()).to(self.weights[0].device)
         self.unit_t = self.layers.units(lambda r, k: k)
+        # persistent kernel: round-robin over units, so every unit gets the
+        # same K length (split-K with atomics) to keep the SMs balanced
+        self.unit_p = self.layers.units(lambda r, k: _equal_kslice(k, 4096))
 
     @property
     def accs(self):
         return self.layers.accs
 
-    def run(self) -> None:
+    def run(self, max_ctas: int | None = None) -> None:
+        """One launch over every layer.  ``max_ctas`` selects the persistent
+        kernel (one CTA per SM, grid capped at max_ctas; 0 = every SM)."""
         self.layers.acc_flat.zero_()
-        nv.call("dc_w8a8_grouped", self.maps.data_ptr(), self.layers.tens.data_ptr(), self.unit_t.data_ptr(),
-                self.unit_t.shape[0], self.layers.ntok, nv.stream_ptr())
+        if max_ctas is None:
+            nv.call("dc_w8a8_grouped", self.maps.data_ptr(), self.layers.tens.data_ptr(), self.unit_t.data_ptr(),
+                    self.unit_t.shape[0], self.layers.ntok, nv.stream_ptr())
+        else:
+            nv.call("dc_w8a8_grouped_persist", self.maps.data_ptr(), self.layers.tens.data_ptr(),
+                    self.unit_p.data_ptr(), self.unit_p.shape[0], self.layers.ntok, int(max_ctas), nv.stream_ptr())
 
 
 class FusedCompressed:
@@ -237,7 +257,7 @@ class FusedRing(FusedCompressed):
             e["n_slices"] = [-(-k // ks) for (_, k), ks in zip(self.layers.shapes, kss)]
             self.epi = torch.from_numpy(e.view(np.uint8).copy()).to(dev)
 
-    def run(self) -> None:
+    def run(self, max_ctas: int = 0) -> None:
         self.layers.acc_flat.zero_()
         self.status.zero_()
         if self.epi is not None:
@@ -247,7 +267,7 @@ class FusedRing(FusedCompressed):
                 j.d_out_len.data_ptr(), j.d_codec.data_ptr(), self.chunk_size, ix.d_seg_base.data_ptr(),
                 ix.d_state.data_ptr(), ix.d_off.data_ptr(), self.layers.tens.data_ptr(), self.unit_t.data_ptr(),
                 self.unit_t.shape[0], self.layers.ntok, self.status.data_ptr(),
-                self.epi.data_ptr() if self.epi is not None else None, nv.stream_ptr())
+                self.epi.data_ptr() if self.epi is not None else None, int(max_ctas), nv.stream_ptr())
 
     def run_checked(self) -> bool:
         """run(), verify every chain (one host sync) and fall back to the exact
@@ -271,3 +291,46 @@ class FusedRing(FusedCompressed):
             for y, acc, sc in zip(self.ys, self.accs, self.scales):
                 y.copy_(acc.to(torch.float32) * sc)
         return False
+
+
+class MixedStep:
+    """A partially compressed model's decode step: the compressed
+    layers through the fused decode -> tcgen05 kernel and the plain INT8 layers
+    through the grouped tcgen05 GEMM, run CONCURRENTLY on two streams.  The
+    fused kernel is ALU-bound and the INT8 GEMM HBM-bound, so they overlap
+    well; the persistent fused grid is capped at ``fused_ctas`` SMs (one CTA
+    each), leaving the rest to the INT8 GEMM.  ``tune()`` picks the split from
+    measured step times -- the reference's latency model assumes exactly this
+    overlap (latency.py:144-222: per chunk max(load, decode, compute))."""
+
+    def __init__(self, fused: FusedRing | None, int8: GroupedInt8 | None, fused_ctas: int = 0):
+        self.fused, self.int8, self.fused_ctas = fused, int8, fused_ctas
+        dev = (fused.layers.acc_flat if fused is not None else int8.layers.acc_flat).device
+        self.side = torch.cuda.Stream(dev)
+
+    def run(self) -> None:
+        if self.fused is None or self.int8 is None:
+            (self.fused.run if self.int8 is None else self.int8.run)()
+            return
+        main = torch.cuda.current_stream()
+        sms = _sm_count()
+        fc = self.fused_ctas if 0 < self.fused_ctas < sms else sms
+        self.side.wait_stream(main)  # inputs ready / previous step's readers finished
+        self.fused.run(fc)           # one CTA per SM on fc SMs ...
+        with torch.cuda.stream(self.side):
+            self.int8.run(max_ctas=sms - fc if fc < sms else 0)  # ... the persistent GEMM on the others
+        main.wait_stream(self.side)
+
+    def tune(self, candidates=None, iters: int = 5) -> dict:
+        """Measure the step for each fused-grid size; keep the fastest."""
+        from .adaptive import time_ms
+        if self.fused is None or self.int8 is None:
+            return {}
+        sms = _sm_count()
+        cands = candidates or sorted(set(range(sms // 4, sms, 8)) | {sms})
+        times = {}
+        for c in cands:
+            self.fused_ctas = c
+            times[c] = time_ms(self.run, iters=iters)
+        self.fused_ctas = min(times, key=times.get)
+        return times

@@ -72,11 +72,13 @@ SIGNATURES: dict[str, list] = {
     "dc_tmap_bytes": [],
     "dc_w8a8_grouped_maps": [_P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P],
     "dc_w8a8_grouped": [_P, _P, _P, _I64, ctypes.c_int, _P],
+    "dc_w8a8_grouped_persist": [_P, _P, _P, _I64, ctypes.c_int, ctypes.c_int, _P],
     "dc_fused_slice_bytes": [],
     "dc_fused_decode_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P],
     "dc_fused_item_rows": [],
     "dc_fused_item_k": [],
-    "dc_fused_ring_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P, _P],
+    "dc_fused_ring_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P, ctypes.c_int,
+                           _P],
     "dc_fused_epi_bytes": [],
 }
 _RESTYPES = {"dc_last_error": ctypes.c_char_p}

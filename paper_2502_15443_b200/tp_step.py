@@ -64,6 +64,36 @@ class TPDecodeStep:
         return bool((self.fused.check() == 0).all()) and all(torch.equal(a, b) for a, b in zip(ref, self.fused.accs))
 
 
+def check_local(step: TPDecodeStep) -> bool:
+    """Single-process check of one rank's shard: fused == INT8 partial outputs."""
+    step.compute(False)
+    ref = [a.clone() for a in step.int8.accs]
+    step.compute(True)
+    torch.cuda.synchronize()
+    return bool((step.fused.check() == 0).all()) and all(torch.equal(a, b) for a, b in zip(ref, step.fused.accs))
+
+
+def measure_local(step: TPDecodeStep, iters: int = 10) -> dict:
+    """One rank's compute (no collective) timed alone -- the per-GPU work of a
+    TP step when only one GPU is available; CUDA events."""
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters
+
+    return {"int8_compute_ms": timed(lambda: step.compute(False)),
+            "compressed_fused_compute_ms": timed(lambda: step.compute(True)),
+            "allreduces_per_step": len(step.row_idx), "local_weight_bytes": step.raw_bytes,
+            "local_file_bytes": step.comp_bytes}
+
+
 def measure(step: TPDecodeStep, iters: int = 10) -> dict:
     """Max-over-ranks step times (CUDA events), compute vs all-reduce split."""
     def timed(fn):

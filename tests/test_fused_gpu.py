@@ -30,7 +30,23 @@ def test_grouped_int8_exact(cuda, ntok):
     from paper_2502_15443_b200.gemm import GroupedInt8
     ws, xs = _weights(), _xs(ntok)
     gi = GroupedInt8([w.cuda() for w in ws], [x.cuda() for x in xs], ntok)
-    gi.run()
+    for max_ctas in (None, 0, 1, 3, 64):  # wave kernel, persistent (all SMs / capped grids)
+        gi.run(max_ctas)
+        for w, x, acc in zip(ws, xs, gi.accs):
+            assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
+
+
+def test_persistent_int8_split_k_exact(cuda):
+    """Long-K layers are split into equal K-slices for the persistent kernel's
+    round-robin (atomics accumulate the slices exactly)."""
+    from paper_2502_15443_b200.gemm import GroupedInt8
+    g = torch.Generator().manual_seed(3)
+    shapes = [(512, 16384), (640, 12288), (256, 4096)]
+    ws = [torch.randint(-127, 128, s, generator=g, dtype=torch.int8) for s in shapes]
+    xs = [torch.randint(-127, 128, (2, k), generator=g, dtype=torch.int8) for _, k in shapes]
+    gi = GroupedInt8([w.cuda() for w in ws], [x.cuda() for x in xs], 2)
+    assert int(gi.unit_p[:, 3].max()) == 4096 and gi.unit_p.shape[0] > gi.unit_t.shape[0]
+    gi.run(max_ctas=0)
     for w, x, acc in zip(ws, xs, gi.accs):
         assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
 
@@ -167,3 +183,32 @@ def test_fused_ring_dequant_epilogue(cuda):
             assert torch.equal(y.cpu(), exact.to(torch.float32) * np.float32(sc))
             ref = exact.to(torch.float64) * sc
             assert torch.allclose(y.cpu().double(), ref, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("fused_ctas", [0, 40, 100])
+def test_mixed_step_overlapped_exact(cuda, fused_ctas):
+    """Partially compressed step: fused (compressed) and INT8 (plain) layers on
+    two streams with the fused grid capped -- results equal the exact product."""
+    from paper_2502_15443_b200 import container
+    from paper_2502_15443_b200.gemm import FusedRing, GroupedInt8, MixedStep
+    g = torch.Generator().manual_seed(21)
+    shapes = [(2048, 2048), (4096, 1024), (1024, 4096), (3000, 2048)]
+    ws = [torch.round(torch.randn(r, k, generator=g) * 15).clamp_(-127, 127).to(torch.int8) for r, k in shapes]
+    xs = [torch.randint(-127, 128, (3, k), generator=g, dtype=torch.int8).cuda() for _, k in shapes]
+    comp, plain = [0, 2], [1, 3]
+    payload = torch.cat([ws[i].reshape(-1).view(torch.uint8) for i in comp]).cuda()
+    t_offs = np.concatenate([[0], np.cumsum([ws[i].numel() for i in comp])[:-1]])
+    chunk = 1 << 22
+    image, enc, entries = container.pack_device(payload, b"\x00" * 8, chunk, None, seg_shift=8)
+    jobs = container.jobs_for(entries, image.device)
+    fr = FusedRing(image, jobs, enc.index, chunk, [shapes[i] for i in comp], t_offs, [xs[i] for i in comp], 3)
+    gi = GroupedInt8([ws[i].cuda() for i in plain], [xs[i] for i in plain], 3)
+    mx = MixedStep(fr, gi, fused_ctas)
+    for _ in range(2):
+        mx.run()
+        torch.cuda.synchronize()
+        assert (fr.check() == 0).all()
+        for i, acc in zip(comp + plain, fr.accs + gi.accs):
+            assert torch.equal(acc.cpu().long(), xs[i].cpu().long() @ ws[i].long().T)
+    times = mx.tune(candidates=[30, 148], iters=2)
+    assert set(times) == {30, 148} and mx.fused_ctas in times

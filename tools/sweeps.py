@@ -18,7 +18,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2502_15443_b200 import adaptive, container, synth  # noqa: E402
-from paper_2502_15443_b200.gemm import FusedRing, GroupedInt8  # noqa: E402
+from paper_2502_15443_b200.gemm import FusedRing, GroupedInt8, MixedStep  # noqa: E402
 from paper_2502_15443_b200.latency import CompressionPlan  # noqa: E402
 
 
@@ -66,6 +66,7 @@ def cmd_partial(a):
         mem = int(sizes[plain_idx].sum())
         fns = []
         checks = []
+        gi = fc = None
         if len(plain_idx):
             gi = GroupedInt8([w_views[i] for i in plain_idx], [xs[i] for i in plain_idx], B)
             fns.append(gi.run)
@@ -80,15 +81,26 @@ def cmd_partial(a):
             fns.append(fc.run)
             checks.append(fc)
             mem += int(entries["comp_len"].sum()) + enc.index.nbytes
-        ms = adaptive.time_ms(lambda: [fn() for fn in fns], iters=a.iters)
-        for fc in checks:
-            if (fc.check() != 0).any():
+        ms_seq = adaptive.time_ms(lambda: [fn() for fn in fns], iters=a.iters)
+        for c in checks:
+            if (c.check() != 0).any():
                 raise SystemExit("fused chain check failed")
+        split, ms = None, ms_seq
+        if gi is not None and fc is not None:  # overlapped: fused on part of the SMs, INT8 GEMM on the rest
+            ref = [x.clone() for x in gi.accs + fc.accs]
+            mx = MixedStep(fc, gi)
+            tries = mx.tune(iters=a.iters)
+            split, ms = mx.fused_ctas, min(tries.values())
+            mx.run()
+            torch.cuda.synchronize()
+            if (fc.check() != 0).any() or not all(torch.equal(x, y) for x, y in zip(ref, gi.accs + fc.accs)):
+                raise SystemExit("overlapped step differs from the sequential one")
         if f == 0.0:
             t_int8 = ms
         points.append({"fraction": f, "layers_compressed": int(mask.sum()), "resident_bytes": mem,
                        "memory_vs_int8": mem / int(sizes.sum()), "step_ms": ms, "tokens_per_s": B / (ms / 1e3),
-                       "vs_int8": t_int8 / ms if t_int8 else None})
+                       "vs_int8": t_int8 / ms if t_int8 else None, "sequential_step_ms": ms_seq,
+                       "fused_sms": split})
         print(json.dumps(points[-1]), flush=True)
         fns.clear()
         torch.cuda.empty_cache()
