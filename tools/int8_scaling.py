@@ -22,6 +22,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--model", default="opt-6.7b")
     p.add_argument("--ntok", type=int, default=1)
+    p.add_argument("--out", default=None)
     a = p.parse_args()
     m = synth.build_model(a.model)
     offs = m.offsets()[:-1]
@@ -45,6 +46,9 @@ def main():
         print(json.dumps(rows[-1]), flush=True)
     out["persistent"] = rows
     print(json.dumps(out))
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(out, f, indent=1)
 
 
 if __name__ == "__main__":
