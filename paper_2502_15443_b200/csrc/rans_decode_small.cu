@@ -134,16 +134,24 @@ __device__ void build_compact_table(const uint8_t* __restrict__ tb, SmallWarpSme
         cumend[lane * 8 + k] = cum;
     }
     __syncwarp();
-    // lane fills slots [128 lane, 128 lane + 128): first symbol whose range ends past the slot
+    // lane fills slots [128 lane, 128 lane + 128), word by word, starting at
+    // its own word `lane` and wrapping: at every step the 32 lanes store to 32
+    // different banks (in order, all lanes would hit one bank: 32-way conflict)
     const uint32_t s0 = (uint32_t)lane * 128;
-    int lo = 0, hi = 255;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (cumend[mid] > s0) hi = mid; else lo = mid + 1;
-    }
-    int sy = lo;
+    auto first_sym = [&](uint32_t slot) {  // first symbol whose range ends past the slot
+        int lo = 0, hi = 255;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (cumend[mid] > slot) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    };
+    const int sy_range = first_sym(s0);
+    int sy = first_sym(s0 + 4u * (uint32_t)lane);
     uint32_t* dst = reinterpret_cast<uint32_t*>(W.symtab + s0);
-    for (int wv = 0; wv < 32; ++wv) {
+    for (int i = 0; i < 32; ++i) {
+        const int wv = (lane + i) & 31;
+        if (wv == 0) sy = sy_range;  // wrapped to the start of the lane's range
         uint32_t word = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
