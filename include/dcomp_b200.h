@@ -99,6 +99,17 @@ int dc_ans_decode_segments(const uint8_t *base, const uint64_t *blob_off, const 
                            const int64_t *seg_base, const uint32_t *seg_state, const uint32_t *seg_off,
                            const int32_t *tasks, int64_t n_tasks, uint8_t *out, int32_t *status,
                            void *stream);
+/* Narrow-CTA variant (4 warps, 3 CTAs/SM, 45 KB staging) for chunks of a few
+ * hundred segments (e.g. 64 KiB): tasks of dc_decode_narrow_segments() segments
+ * keep two interleaved chains per lane.  Task stream spans must fit
+ * dc_decode_stage_cap(1) bytes (dc_decode_stage_cap(0) for the wide kernel). */
+int dc_ans_decode_segments_narrow(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
+                                  const uint64_t *out_off, const uint64_t *out_len, uint32_t seg_shift,
+                                  const int64_t *seg_base, const uint32_t *seg_state, const uint32_t *seg_off,
+                                  const int32_t *tasks, int64_t n_tasks, uint8_t *out, int32_t *status,
+                                  void *stream);
+int dc_decode_narrow_segments(void);
+int dc_decode_stage_cap(int narrow);
 
 /* Small-chunk variant (every chunk <= dc_decode_small_max_chunk() bytes):
  * warp tasks of <= dc_decode_small_segments() segments, a compact per-warp

@@ -231,31 +231,44 @@ __global__ void __launch_bounds__(kSerialThreads) k_decode_serial(
 }
 
 // ---------------------------------------------------------- segment decode
-constexpr int kDecThreads = 256;                  // 8 warps
-constexpr int kDecWarps = kDecThreads / 32;
 constexpr int kDecIlp = 2;                        // segments per lane, interleaved
-constexpr int kTaskSegs = kDecThreads * kDecIlp;  // segments per task
-constexpr uint32_t kStageCap = 72 * 1024;         // staged stream bytes per task (2 CTAs/SM fit)
 constexpr uint32_t kStageSlack = 2 * 1024 + 128;  // over-read room (>= 2 * max segment + 1)
 constexpr int kOutLine = 32;                      // bytes per lane-segment per flush
 constexpr int kOutStride = 32;                    // + XOR swizzle of the 16-B halves (see swz)
 constexpr int kOutWarpBytes = kDecIlp * 32 * kOutStride;
-// dynamic smem carve-up (constant offsets keep the shared address space visible)
-constexpr uint32_t kOffTab = 0;
-constexpr uint32_t kOffStage = ((sizeof(TableSmem) + 127) / 128) * 128;
-constexpr uint32_t kOffOut = kOffStage + kStageCap + kStageSlack;
-constexpr uint32_t kOffBar = kOffOut + kDecWarps * kOutWarpBytes;
-constexpr size_t kDecSmem = kOffBar + 16;
-static_assert(kOffStage % 128 == 0 && kOffOut % 16 == 0 && kOffBar % 8 == 0, "smem carve-up alignment");
+
+// Two CTA shapes.  Wide: 8 warps, 512-segment tasks, 72 KB stream staging,
+// 2 CTAs/SM -- the large-chunk configuration.  Narrow: 4 warps, 256-segment
+// tasks, 45 KB staging, 3 CTAs/SM -- a 64 KiB chunk (256 segments) then
+// still gives every lane two interleaved chains instead of one.
+template <int TH, int MINB, uint32_t STAGE>
+struct DecCfg {
+    static constexpr int kThreads = TH;
+    static constexpr int kMinBlocks = MINB;
+    static constexpr int kWarps = TH / 32;
+    static constexpr int kTaskSegs = TH * kDecIlp;
+    static constexpr uint32_t kStageCap = STAGE;
+    // dynamic smem carve-up (constant offsets keep the shared address space visible)
+    static constexpr uint32_t kOffTab = 0;
+    static constexpr uint32_t kOffStage = ((sizeof(TableSmem) + 127) / 128) * 128;
+    static constexpr uint32_t kOffOut = kOffStage + kStageCap + kStageSlack;
+    static constexpr uint32_t kOffBar = kOffOut + kWarps * kOutWarpBytes;
+    static constexpr size_t kSmem = kOffBar + 16;
+    static_assert(kOffStage % 128 == 0 && kOffOut % 16 == 0 && kOffBar % 8 == 0, "smem carve-up alignment");
+};
+using WideCfg = DecCfg<256, 2, 72 * 1024>;
+using NarrowCfg = DecCfg<128, 3, 45 * 1024>;
+static_assert(WideCfg::kSmem * 2 + 2048 <= 228 * 1024 && NarrowCfg::kSmem * 3 + 3072 <= 228 * 1024,
+              "CTAs per SM must fit in shared memory");
 
 // 16-B half `h` of lane-segment `ls` in the output staging buffer.  Halves are
 // swapped when bit 2 of the lane is set, which makes both the per-lane
 // 16-B stores (8 lanes per phase) and the per-line 16-B reads conflict-free.
 __device__ __forceinline__ uint32_t swz(int ls, int h) { return (uint32_t)(ls * kOutStride + ((h ^ ((ls >> 2) & 1)) << 4)); }
 
-// One warp decodes NU segments per lane (segment r = warp*32 + lane + u*256
+// One warp decodes NU segments per lane (segment r = warp*32 + lane + u*TH
 // of the task) and writes them out through its staging buffer `ob`.
-template <int NU>
+template <int NU, int TH>
 __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, int64_t sb, uint32_t lo,
                                             uint32_t delta, uint32_t plen, uint64_t olen, uint32_t nseg_chunk,
                                             const uint32_t* __restrict__ seg_state,
@@ -271,7 +284,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
     Win W[NU];
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
-        const int r = warp * 32 + lane + u * kDecThreads;
+        const int r = warp * 32 + lane + u * TH;
         const uint32_t rel = (uint32_t)(s0 + r);
         uint32_t p;
         if (r < ns) {
@@ -291,14 +304,14 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
     // per-line destinations are precomputed 32-bit offsets from the task base.
     bool ff = out_aligned;
 #pragma unroll
-    for (int u = 0; u < NU; ++u) ff = ff && (warp * 32 + lane + u * kDecThreads < ns) && n[u] == K;
+    for (int u = 0; u < NU; ++u) ff = ff && (warp * 32 + lane + u * TH < ns) && n[u] == K;
     const bool fast_flush = __all_sync(0xffffffffu, ff);
     uint8_t* const tb = obase + ((uint64_t)(uint32_t)s0 << seg_shift);
     uint32_t dk[NU * 2];
 #pragma unroll
     for (int k = 0; k < NU * 2; ++k) {
         const int pc = k * 32 + lane;
-        dk[k] = ((uint32_t)(warp * 32 + ((pc >> 1) & 31) + (pc >> 6) * kDecThreads) << seg_shift) + (pc & 1) * 16;
+        dk[k] = ((uint32_t)(warp * 32 + ((pc >> 1) & 31) + (pc >> 6) * TH) << seg_shift) + (pc & 1) * 16;
     }
     for (int g = 0; g < G; ++g) {
         const uint32_t g0 = (uint32_t)g << 4;
@@ -365,7 +378,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
             for (int k = 0; k < NU * 2; ++k) {
                 const int pc = k * 32 + lane;
                 const int u = pc >> 6, ln = (pc >> 1) & 31, part = pc & 1;
-                const int r = warp * 32 + ln + u * kDecThreads;
+                const int r = warp * 32 + ln + u * TH;
                 if (r >= ns) continue;
                 const uint64_t seg_start = (uint64_t)(s0 + r) << seg_shift;
                 const uint64_t rem = olen - seg_start;
@@ -387,7 +400,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
     // chain checks: every segment must end exactly where the next one starts
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
-        const int r = warp * 32 + lane + u * kDecThreads;
+        const int r = warp * 32 + lane + u * TH;
         if (r >= ns) continue;
         const uint32_t rel = (uint32_t)(s0 + r);
         uint32_t xe, pe;
@@ -402,7 +415,8 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
     }
 }
 
-__global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segments(
     const uint8_t* __restrict__ base, const uint64_t* __restrict__ blob_off, const uint64_t* __restrict__ blob_len,
     const uint64_t* __restrict__ out_off, const uint64_t* __restrict__ out_len, uint32_t seg_shift,
     const int64_t* __restrict__ seg_base, const uint32_t* __restrict__ seg_state,
@@ -410,12 +424,12 @@ __global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
     uint8_t* __restrict__ out, int32_t* __restrict__ status, uint32_t one) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const FmaK fk = fma_consts(one);
-    TableSmem& T = *reinterpret_cast<TableSmem*>(smem + kOffTab);
-    uint8_t* stage = smem + kOffStage;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
+    TableSmem& T = *reinterpret_cast<TableSmem*>(smem + Cfg::kOffTab);
+    uint8_t* stage = smem + Cfg::kOffStage;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::kOffBar);
 
     const int warp = threadIdx.x >> 5;
-    uint8_t* ob = smem + kOffOut + warp * kOutWarpBytes;
+    uint8_t* ob = smem + Cfg::kOffOut + warp * kOutWarpBytes;
     const uint32_t K = 1u << seg_shift;
 
     const int64_t t_begin = (int64_t)blockIdx.x * n_tasks / gridDim.x;
@@ -447,7 +461,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
         const uintptr_t a16 = gsrc & ~(uintptr_t)15;
         const uint32_t delta = (uint32_t)(gsrc - a16);
         const uint32_t bytes = (hi >= lo) ? ((hi - lo + delta + 15u) & ~15u) : 0xFFFFFFFFu;
-        const bool stage_ok = bytes <= kStageCap;
+        const bool stage_ok = bytes <= Cfg::kStageCap;
 
         __syncthreads();  // previous task done with stage[] and T
         if (threadIdx.x == 0) {
@@ -484,12 +498,12 @@ __global__ void __launch_bounds__(kDecThreads, 2) k_decode_segments(
             continue;
         }
         if (warp * 32 >= ns) continue;  // idle warp in a short task
-        if (warp * 32 + kDecThreads < ns)
-            decode_warp<2>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state, seg_off, T.tab,
-                           stage, ob, obase, out_aligned, &status[c], fk);
+        if (warp * 32 + Cfg::kThreads < ns)
+            decode_warp<2, Cfg::kThreads>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state,
+                                          seg_off, T.tab, stage, ob, obase, out_aligned, &status[c], fk);
         else
-            decode_warp<1>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state, seg_off, T.tab,
-                           stage, ob, obase, out_aligned, &status[c], fk);
+            decode_warp<1, Cfg::kThreads>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state,
+                                          seg_off, T.tab, stage, ob, obase, out_aligned, &status[c], fk);
     }
 }
 
@@ -570,27 +584,48 @@ extern "C" int dc_ans_decode_serial(const uint8_t* base, const uint64_t* blob_of
     return DC_OK;
 }
 
-extern "C" int dc_decode_task_segments(void) { return kTaskSegs; }
+extern "C" int dc_decode_task_segments(void) { return WideCfg::kTaskSegs; }
+extern "C" int dc_decode_narrow_segments(void) { return NarrowCfg::kTaskSegs; }
+extern "C" int dc_decode_stage_cap(int narrow) { return (int)(narrow ? NarrowCfg::kStageCap : WideCfg::kStageCap); }
+
+template <class Cfg>
+static int launch_segments(const uint8_t* base, const uint64_t* blob_off, const uint64_t* blob_len,
+                           const uint64_t* out_off, const uint64_t* out_len, uint32_t seg_shift,
+                           const int64_t* seg_base, const uint32_t* seg_state, const uint32_t* seg_off,
+                           const int32_t* tasks, int64_t n_tasks, uint8_t* out, int32_t* status, void* stream) {
+    if (n_tasks < 0 || seg_shift < 6 || seg_shift > 10) return DC_ERR_ARG;
+    if (n_tasks == 0) return DC_OK;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_decode_segments<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+        attr = true;
+    }
+    const int64_t cap = (int64_t)sm_count() * Cfg::kMinBlocks;
+    const int64_t grid = n_tasks < cap ? n_tasks : cap;
+    k_decode_segments<Cfg><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, (cudaStream_t)stream>>>(
+        base, blob_off, blob_len, out_off, out_len, seg_shift, seg_base, seg_state, seg_off,
+        reinterpret_cast<const int4*>(tasks), n_tasks, out, status, 1u);
+    DC_CHECK_LAUNCH("k_decode_segments");
+    return DC_OK;
+}
 
 extern "C" int dc_ans_decode_segments(const uint8_t* base, const uint64_t* blob_off, const uint64_t* blob_len,
                                       const uint64_t* out_off, const uint64_t* out_len, uint32_t seg_shift,
                                       const int64_t* seg_base, const uint32_t* seg_state, const uint32_t* seg_off,
                                       const int32_t* tasks, int64_t n_tasks, uint8_t* out, int32_t* status,
                                       void* stream) {
-    if (n_tasks < 0 || seg_shift < 6 || seg_shift > 10) return DC_ERR_ARG;
-    if (n_tasks == 0) return DC_OK;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_decode_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem);
-        attr = true;
-    }
-    const int64_t cap = (int64_t)sm_count() * 2;
-    const int64_t grid = n_tasks < cap ? n_tasks : cap;
-    k_decode_segments<<<(unsigned)grid, kDecThreads, kDecSmem, (cudaStream_t)stream>>>(
-        base, blob_off, blob_len, out_off, out_len, seg_shift, seg_base, seg_state, seg_off,
-        reinterpret_cast<const int4*>(tasks), n_tasks, out, status, 1u);
-    DC_CHECK_LAUNCH("k_decode_segments");
-    return DC_OK;
+    return launch_segments<WideCfg>(base, blob_off, blob_len, out_off, out_len, seg_shift, seg_base, seg_state,
+                                    seg_off, tasks, n_tasks, out, status, stream);
+}
+
+extern "C" int dc_ans_decode_segments_narrow(const uint8_t* base, const uint64_t* blob_off,
+                                             const uint64_t* blob_len, const uint64_t* out_off,
+                                             const uint64_t* out_len, uint32_t seg_shift, const int64_t* seg_base,
+                                             const uint32_t* seg_state, const uint32_t* seg_off,
+                                             const int32_t* tasks, int64_t n_tasks, uint8_t* out, int32_t* status,
+                                             void* stream) {
+    return launch_segments<NarrowCfg>(base, blob_off, blob_len, out_off, out_len, seg_shift, seg_base, seg_state,
+                                      seg_off, tasks, n_tasks, out, status, stream);
 }
 
 extern "C" int dc_store_copy(const uint8_t* base, const uint64_t* blob_off, const uint64_t* out_off,

@@ -29,7 +29,7 @@ from . import native as nv
 
 HEADER_BYTES = 388
 DEFAULT_SEG_SHIFT = 8          # 256-symbol segments: 8 B of index per 256 B of weights
-STAGE_CAP = 72 * 1024 - 16     # kStageCap in rans_decode.cu minus alignment slop
+STAGE_SLOP = 16  # staged span = stream bytes + up to 15 B of 16-B alignment
 
 
 def _dev():
@@ -176,8 +176,11 @@ class SegmentIndex:
     # ---- work decomposition -------------------------------------------------
     def tasks(self, jobs: JobTable, ok: np.ndarray, max_segs: int | None = None) -> torch.Tensor:
         """int32 [n_tasks, 4] = (chunk, first segment, count, 0): at most
-        ``max_segs`` segments and at most STAGE_CAP staged stream bytes each."""
-        max_segs = max_segs or nv.call("dc_decode_small_segments" if small_mode(jobs) else "dc_decode_task_segments")
+        ``max_segs`` segments and at most the kernel's staging capacity of stream bytes each."""
+        mode = decode_mode(jobs)
+        max_segs = max_segs or nv.call({"small": "dc_decode_small_segments", "narrow": "dc_decode_narrow_segments",
+                                        "wide": "dc_decode_task_segments"}[mode])
+        stage_cap = nv.call("dc_decode_stage_cap", 1 if mode == "narrow" else 0) - STAGE_SLOP
         K = 1 << self.seg_shift
         sel = np.nonzero((jobs.codec == 1) & ok & (jobs.out_len > 0))[0]
         nseg = (jobs.out_len[sel].astype(np.int64) + K - 1) // K
@@ -199,7 +202,7 @@ class SegmentIndex:
         nmax = max(self.n_segs - 1, 0)
         split = False
         for _ in range(32):
-            big = (hi - lo + 15 > STAGE_CAP) & (cnt > 1)
+            big = (hi - lo + 15 > stage_cap) & (cnt > 1)
             if not big.any():
                 break
             split = True
@@ -255,7 +258,22 @@ def small_mode(jobs: JobTable) -> bool:
 
 
 def segment_kernel(jobs: JobTable) -> str:
-    return "dc_ans_decode_small" if small_mode(jobs) else "dc_ans_decode_segments"
+    return {"small": "dc_ans_decode_small", "narrow": "dc_ans_decode_segments_narrow",
+            "wide": "dc_ans_decode_segments"}[decode_mode(jobs)]
+
+
+def decode_mode(jobs: JobTable) -> str:
+    """Which split-point decoder the chunk sizes call for (one predicate shared
+    by SegmentIndex.tasks and segment_kernel): "small" (warp tasks, chunks <=
+    32 KiB), "narrow" (4-warp CTAs, 256-segment tasks, chunks <= 64 KiB by
+    default, DCOMP_NARROW_MAX_CHUNK overrides) or "wide" (8-warp CTAs)."""
+    if small_mode(jobs):
+        return "small"
+    lim = int(os.environ.get("DCOMP_NARROW_MAX_CHUNK", str(NARROW_MAX_CHUNK)))
+    return "narrow" if jobs.n > 0 and int(jobs.out_len.max()) <= lim else "wide"
+
+
+NARROW_MAX_CHUNK = 64 << 10
 
 
 def decode_segments(base, jobs: JobTable, index: SegmentIndex, tasks: torch.Tensor, out: torch.Tensor,

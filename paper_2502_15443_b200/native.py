@@ -50,6 +50,9 @@ SIGNATURES: dict[str, list] = {
     "dc_ans_decode_serial": [_P, _P, _P, _P, _P, _P, _I64, _P, _U32, _P, _P, _P, _P, _P],
     "dc_decode_task_segments": [],
     "dc_ans_decode_segments": [_P, _P, _P, _P, _P, _U32, _P, _P, _P, _P, _I64, _P, _P, _P],
+    "dc_ans_decode_segments_narrow": [_P, _P, _P, _P, _P, _U32, _P, _P, _P, _P, _I64, _P, _P, _P],
+    "dc_decode_narrow_segments": [],
+    "dc_decode_stage_cap": [ctypes.c_int],
     "dc_decode_small_segments": [],
     "dc_decode_small_max_chunk": [],
     "dc_ans_decode_small": [_P, _P, _P, _P, _P, _U32, _P, _P, _P, _P, _I64, _P, _P, _P],

@@ -249,3 +249,30 @@ def test_c1_opt125m_digests(cuda, model_digests):
             assert hashlib.sha256(blob).hexdigest() == meta["sha"]
             back = cuda.unpack(blob)
             assert all(np.array_equal(a.qvalues, b.qvalues) for a, b in zip(qts, back.tensors))
+
+
+@pytest.mark.parametrize("chunk,mode", [(65536, "narrow"), (98304, "wide"), (32768, "small")])
+def test_decoder_mode_selection_exact(cuda, chunk, mode, monkeypatch):
+    """Each split-point decoder (warp-task / 4-warp / 8-warp CTAs) is picked by
+    chunk size and decodes bit-exactly; forcing the narrow kernel onto larger
+    chunks (multi-task chunks) stays exact too."""
+    from paper_2502_15443_b200 import container, engine
+    rng = np.random.default_rng(chunk)
+    ts, st = [], {}
+    for i, (r, c) in enumerate([(700, 1000), (256, 2304)]):
+        q = np.clip(np.round(rng.normal(0, 7, (r, c))), -127, 127).astype(np.int8)
+        ts.append(cuda.QuantizedTensor(f"w{i}", q, 0.01, cuda.ScaleVector.identity(c)))
+        st[f"w{i}"] = cuda.ActivationStats(f"w{i}", np.ones(c))
+    data, index = container.pack_indexed(ts, st, chunk_size=chunk, seg_shift=8)
+    jobs = container.jobs_for(container._parse(data)[2])
+    assert engine.decode_mode(jobs) == mode
+    side = index.to_bytes(container.binding_of(data))
+    out = container.unpack(data, index=side)
+    for x, t in zip(out.tensors, ts):
+        assert np.array_equal(x.qvalues, t.qvalues)
+    monkeypatch.setenv("DCOMP_NARROW_MAX_CHUNK", str(1 << 30))
+    if mode == "wide":
+        assert engine.decode_mode(jobs) == "narrow"
+        out = container.unpack(data, index=side)
+        for x, t in zip(out.tensors, ts):
+            assert np.array_equal(x.qvalues, t.qvalues)
