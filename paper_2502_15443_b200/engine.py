@@ -457,7 +457,10 @@ class PipelinedDecode:
 
     LOOKAHEAD = int(os.environ.get("DCOMP_H2D_LOOKAHEAD", "2"))
 
-    def __init__(self, src, jobs: JobTable, index: SegmentIndex, groups: int = 16):
+    GROUPS = int(os.environ.get("DCOMP_E2E_GROUPS", "16"))
+
+    def __init__(self, src, jobs: JobTable, index: SegmentIndex, groups: int | None = None):
+        groups = groups or self.GROUPS
         dev = jobs.d_blob_off.device
         self.dev, self.jobs = dev, jobs
         s_copy, s_out = _streams(dev)
@@ -587,6 +590,6 @@ class PipelinedDecode:
         return host_out.numpy(), st, self.crc[:n].cpu().numpy().view(np.uint32)
 
 
-def decode_file_pipelined(data, jobs: JobTable, index: SegmentIndex, groups: int = 16):
+def decode_file_pipelined(data, jobs: JobTable, index: SegmentIndex, groups: int | None = None):
     """One-shot PipelinedDecode (see there)."""
     return PipelinedDecode(data, jobs, index, groups).finish()
