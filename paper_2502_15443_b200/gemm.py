@@ -225,8 +225,32 @@ class FusedRing(FusedCompressed):
             if (rows_per - 1) * k + kmax > chunk_size:
                 raise ValueError("chunk too small for the fused path (1024 rows x K must fit in one chunk)")
         self.image, self.jobs, self.index, self.chunk_size = image, jobs, index, chunk_size
-        self.t_offs = [int(t) for t in t_offs]
-        self.layers = _LayerSet(shapes, t_offs, xs, ntok)
+        # Consecutive layers that read the same activations and sit back to back
+        # in the payload (q/k/v, gate/up) become one taller matrix: its row
+        # blocks fill the 1024-row items (a 640-row TP shard alone leaves 3/8
+        # of the chains idle).  accs stay per layer (row-slice views).
+        shapes = [(int(r), int(k)) for r, k in shapes]
+        groups, i = [], 0
+        while i < len(shapes):
+            j = i + 1
+            while (scales is None and j < len(shapes) and shapes[j][1] == shapes[i][1]
+                   and int(t_offs[j]) == int(t_offs[j - 1]) + shapes[j - 1][0] * shapes[j - 1][1]
+                   and xs[j].data_ptr() == xs[i].data_ptr() and xs[j].shape == xs[i].shape):
+                j += 1
+            groups.append((i, j))
+            i = j
+        m_shapes = [(sum(shapes[q][0] for q in range(a, b)), shapes[a][1]) for a, b in groups]
+        m_offs = [int(t_offs[a]) for a, _ in groups]
+        self.t_offs = m_offs
+        self.layers = _LayerSet(m_shapes, m_offs, [xs[a] for a, _ in groups], ntok)
+        self._accs = []
+        for (a, b), acc in zip(groups, self.layers.accs):
+            r0 = 0
+            for q in range(a, b):
+                self._accs.append(acc[:, r0:r0 + shapes[q][0]])
+                r0 += shapes[q][0]
+        self.merged_layers = len(shapes) - len(groups)
+        shapes, t_offs = m_shapes, m_offs
         items, kss = [], []
         for li, (r, k) in enumerate(self.layers.shapes):
             # a chain's K-slice must never straddle a chunk boundary: use the
@@ -256,6 +280,10 @@ class FusedRing(FusedCompressed):
             e["scale"] = np.asarray(scales, dtype=np.float32)
             e["n_slices"] = [-(-k // ks) for (_, k), ks in zip(self.layers.shapes, kss)]
             self.epi = torch.from_numpy(e.view(np.uint8).copy()).to(dev)
+
+    @property
+    def accs(self):
+        return self._accs
 
     def run(self, max_ctas: int = 0) -> None:
         self.layers.acc_flat.zero_()

@@ -34,8 +34,16 @@ class TPDecodeStep:
         self.jobs = container.jobs_for(entries, image.device)
         g = torch.Generator(device=self.dev)
         g.manual_seed(99)
-        self.xs = [torch.randint(-127, 128, (ntok, c), generator=g, device=self.dev, dtype=torch.int8)
-                   for _, c in m.shapes]
+        # one activation per input: q/k/v read the same hidden state, as do gate/up
+        shared = {}
+        self.xs = []
+        for s, (_, c) in zip(self.shards, m.shapes):
+            layer, proj = s.name.rsplit(".", 1)
+            key = (layer, "attn" if proj in ("q_proj", "k_proj", "v_proj") else
+                   "mlp" if proj in ("gate_proj", "up_proj") else proj)
+            if key not in shared:
+                shared[key] = torch.randint(-127, 128, (ntok, c), generator=g, device=self.dev, dtype=torch.int8)
+            self.xs.append(shared[key])
         w_views = [m.payload[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, m.shapes)]
         self.int8 = GroupedInt8(w_views, self.xs, ntok)
         self.fused = FusedRing(image, self.jobs, enc.index, chunk_size, m.shapes, offs, self.xs, ntok)

@@ -212,3 +212,27 @@ def test_mixed_step_overlapped_exact(cuda, fused_ctas):
             assert torch.equal(acc.cpu().long(), xs[i].cpu().long() @ ws[i].long().T)
     times = mx.tune(candidates=[30, 148], iters=2)
     assert set(times) == {30, 148} and mx.fused_ctas in times
+
+
+def test_fused_ring_merges_shared_input_layers(cuda):
+    """q/k/v-style layers (same activations, back to back in the payload) are
+    decoded as one taller matrix; per-layer accumulators stay exact views."""
+    from paper_2502_15443_b200 import container
+    from paper_2502_15443_b200.gemm import FusedRing
+    g = torch.Generator().manual_seed(8)
+    shapes = [(640, 1024), (640, 1024), (640, 1024), (1024, 2048), (384, 2048)]
+    ws = [torch.round(torch.randn(r, k, generator=g) * 12).clamp_(-127, 127).to(torch.int8) for r, k in shapes]
+    x_attn = torch.randint(-127, 128, (2, 1024), generator=g, dtype=torch.int8).cuda()
+    x_other = torch.randint(-127, 128, (2, 2048), generator=g, dtype=torch.int8).cuda()
+    xs = [x_attn, x_attn, x_attn, x_other, x_other.clone()]  # last: equal values, different tensor
+    payload = torch.cat([w.reshape(-1).view(torch.uint8) for w in ws]).cuda()
+    t_offs = np.concatenate([[0], np.cumsum([w.numel() for w in ws])[:-1]])
+    chunk = 1 << 22
+    image, enc, entries = container.pack_device(payload, b"\x00" * 8, chunk, None, seg_shift=8)
+    jobs = container.jobs_for(entries, image.device)
+    fr = FusedRing(image, jobs, enc.index, chunk, shapes, t_offs, xs, 2)
+    assert fr.merged_layers == 2 and len(fr.accs) == len(shapes)
+    assert fr.run_checked()
+    for w, x, acc in zip(ws, xs, fr.accs):
+        assert acc.shape == (2, w.shape[0])
+        assert torch.equal(acc.cpu().long(), x.cpu().long() @ w.long().T)
