@@ -192,23 +192,30 @@ struct __align__(16) EncEnt {
     uint32_t bias, gmul, pad0, pad1;  // gmul = 4096 - f
 };
 
-__device__ __forceinline__ void enc_step(uint32_t& x, uint32_t& pos, const uint4& a, const uint2& b) {
-    // a = (rcp, xm1, xm2, sh), b = (bias, gmul); chain: setp -> selp -> mul.hi -> shr -> mad
+
+// Shorter chain: q = floor(x / (f << 8n)) = mulhi(x, rcp) >> (sh + 8n) -- the
+// same reciprocal for every renorm count n (nested floor division), so the
+// IMAD.HI starts from x itself in parallel with the renorm test instead of
+// after it; x' = (x >> 8n) + cum + q * (4096 - f).  Critical path: max(IMAD.HI,
+// ISETP -> SEL -> IADD) -> SHF -> IMAD.  f == 1: x >= 2^20 > xm1 = 2^16
+// always renormalizes (8n >= 8), so rcp = 2^31 with sh = -1 gives
+// q = (x >> 1) >> (8n - 1) = x >> 8n exactly.
+__device__ __forceinline__ void enc_step_fast(uint32_t& x, uint32_t& pos, const uint4& a, const uint2& b) {
     asm volatile(
-        "{\n\t.reg .pred p1, p2;\n\t.reg .u32 x8, x16, xr, q, xb, n;\n\t"
+        "{\n\t.reg .pred p1, p2;\n\t.reg .u32 q, n1, n2, n8, s, xr;\n\t"
+        "mul.hi.u32 q, %0, %2;\n\t"
         "setp.ge.u32 p1, %0, %3;\n\t"
         "setp.ge.u32 p2, %0, %4;\n\t"
-        "shr.u32 x8, %0, 8;\n\t"
-        "shr.u32 x16, %0, 16;\n\t"
-        "selp.u32 n, 1, 0, p1;\n\t"
-        "@p2 add.u32 n, n, 1;\n\t"
-        "add.u32 %1, %1, n;\n\t"
-        "selp.u32 xr, x8, %0, p1;\n\t"
-        "selp.u32 xr, x16, xr, p2;\n\t"
-        "mul.hi.u32 q, xr, %2;\n\t"
-        "add.u32 xb, xr, %6;\n\t"
-        "shr.u32 q, q, %5;\n\t"
-        "mad.lo.u32 %0, q, %7, xb;\n\t}"
+        "selp.u32 n1, 8, 0, p1;\n\t"
+        "selp.u32 n2, 8, 0, p2;\n\t"
+        "add.u32 n8, n1, n2;\n\t"
+        "add.u32 s, n8, %5;\n\t"
+        "shr.u32 q, q, s;\n\t"
+        "shr.u32 xr, %0, n8;\n\t"
+        "add.u32 xr, xr, %6;\n\t"
+        "shr.u32 n1, n8, 3;\n\t"
+        "add.u32 %1, %1, n1;\n\t"
+        "mad.lo.u32 %0, q, %7, xr;\n\t}"
         : "+r"(x), "+r"(pos)
         : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y));
 }
@@ -238,12 +245,13 @@ __device__ __forceinline__ void build_enc_table(const uint32_t* __restrict__ fre
             while (f > (1u << shift)) ++shift;
             e.rcp = (uint32_t)(((1ull << (shift + 31)) + f - 1) / f);
             e.sh = shift - 1;
-        } else {
-            e.rcp = 0xFFFFFFFFu;
+        } else {  // f == 1 (see enc_step_fast)
+            e.rcp = 0x80000000u;
+            e.sh = 0xFFFFFFFFu;
         }
         e.xm1 = f << 16;
         e.xm2 = f < 16 ? f << 24 : 0xFFFFFFFFu;
-        e.bias = f >= 2 ? cum : cum + (kProbScale - 1);
+        e.bias = cum;
         e.gmul = kProbScale - f;
         e.pad0 = e.pad1 = 0;
         T[lane * 8 + k] = e;
@@ -299,7 +307,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __rest
         const uint4 ea = *reinterpret_cast<const uint4*>(&T[sy].rcp);
         const uint2 eb = *reinterpret_cast<const uint2*>(&T[sy].bias);
         if (lead) xsc[i] = x;
-        enc_step(x, pos, ea, eb);
+        enc_step_fast(x, pos, ea, eb);
         record(i);
         if (pos >= limit) stored = true;
     }
@@ -333,7 +341,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __rest
 #pragma unroll
         for (int k = 15; k >= 0; --k) {
             xin[k] = x;
-            enc_step(x, pos, ea[k], eb[k]);
+            enc_step_fast(x, pos, ea[k], eb[k]);
         }
         if (lead) {
             uint32_t* dst = xsc + 16 * b;

@@ -87,3 +87,21 @@ def test_edge_cases(cuda):
 def test_long_stream(cuda):
     d = np.abs(np.random.default_rng(7).laplace(0, 6, 2**20)).astype(np.uint8)
     assert cuda.decompress_blob(cuda.compress_blob(d), d.size) == d.tobytes()
+
+
+def test_singleton_symbols_f1_bit_exact(cuda, oracle):
+    """Symbols whose normalized frequency is 1 (rare bytes in a long skewed
+    chunk) take the encoder's f == 1 reciprocal form; blobs equal the oracle's
+    and decode back."""
+    rng = np.random.default_rng(17)
+    for n, k in ((1 << 16, 12), (1 << 20, 40), (300_000, 3)):
+        data = np.zeros(n, np.uint8)
+        data[: n // 3] = rng.integers(1, 4, n // 3)
+        pos = rng.choice(n, size=k, replace=False)
+        data[pos] = rng.integers(100, 256, k).astype(np.uint8)  # each appears ~once -> f == 1
+        rng.shuffle(data)
+        blob = cuda.compress_blob(data.tobytes())
+        assert blob == oracle.compress_blob(data.tobytes())
+        table = cuda.AnsTable.from_bytes(blob[:384])
+        assert (table.frequencies == 1).sum() >= 1
+        assert cuda.decompress_blob(blob, n) == data.tobytes()
