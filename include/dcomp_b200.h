@@ -88,13 +88,9 @@ int dc_ans_decode_serial(const uint8_t *base, const uint64_t *blob_off, const ui
 /* Segment-parallel decode (the hot kernel): each lane decodes one segment
  * from its split point; every segment's end state/offset must meet the next
  * split point (or 2^20 / stream end), else the chunk is flagged
- * DC_CHUNK_CHAIN for an exact serial re-decode.  tasks: 8 int32 per task,
- * (chunk, first segment (relative), segment count, 0, span offset lo, span
- * offset hi, span bytes, first split-point index): at most
- * dc_decode_task_segments() segments each, sorted by chunk; the span (the
- * task's 16-B aligned stream bytes as an offset from `base`, and the global
- * index of its first split point) only steers the L2 prefetch of the next
- * task -- 0 bytes disables it, wrong values cost speed, never correctness.
+ * DC_CHUNK_CHAIN for an exact serial re-decode.  tasks: int32 quads
+ * (chunk, first segment (relative), segment count, 0), at most
+ * dc_decode_task_segments() segments each, sorted by chunk.
  * replaces ans.py:97-200 (_dec2/_dec4 multi-lane interleave) with
  * thousands of lanes per chunk. */
 int dc_decode_task_segments(void);
@@ -118,9 +114,8 @@ int dc_decode_stage_cap(int narrow);
 /* Small-chunk variant (every chunk <= dc_decode_small_max_chunk() bytes):
  * warp tasks of <= dc_decode_small_segments() segments, a compact per-warp
  * table (u8 slot->symbol + per-symbol update), stream read through L1.
- * Same arguments, outputs and chain checks as dc_ans_decode_segments; tasks
- * are int32 quads (the first four fields).  replaces ans.py:97-200 at small
- * chunk sizes. */
+ * Same arguments, task format, outputs and chain checks as
+ * dc_ans_decode_segments.  replaces ans.py:97-200 at small chunk sizes. */
 int dc_decode_small_segments(void);
 int dc_decode_small_max_chunk(void);
 int dc_ans_decode_small(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,

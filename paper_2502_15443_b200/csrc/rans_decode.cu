@@ -443,15 +443,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segme
     uint32_t phase = 0;
 
     for (int64_t ti = t_begin; ti < t_end; ++ti) {
-        const int4 task = tasks[2 * ti];  // (chunk, first segment, segments, 0)
+        const int4 task = tasks[ti];
         const int c = task.x, s0 = task.y, ns = task.z;
-        // the next task's record (span, segments), consumed after this task's
-        // copy is issued: loaded now so its latency hides behind the prologue
-        int4 nsp = make_int4(0, 0, 0, 0), ntk = make_int4(0, 0, 0, 0);
-        if (threadIdx.x == 0 && ti + 1 < t_end) {
-            ntk = tasks[2 * ti + 2];
-            nsp = tasks[2 * ti + 3];
-        }
         {  // prologue errors (k_validate, same stream) are never decoded
             const int32_t st0 = status[c];
             if (st0 >= DC_CHUNK_TRUNC_TABLE && st0 <= DC_CHUNK_EMPTY_BAD) continue;
@@ -477,20 +470,6 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segme
             mbar_arrive_expect_tx(bar, nbytes);
             for (uint32_t off = 0; off < nbytes; off += 16384u)
                 bulk_g2s(stage + off, reinterpret_cast<const void*>(a16 + off), min(16384u, nbytes - off), bar);
-            // warm L2 for the next task: its stream span and split points
-            const uint32_t nb = (uint32_t)nsp.z;
-            if (nb && nb <= Cfg::kStageCap) {
-                const uint64_t noff = (uint64_t)(uint32_t)nsp.x | ((uint64_t)(uint32_t)nsp.y << 32);
-                bulk_prefetch_l2(base + noff, nb);
-                const uint32_t si = (uint32_t)nsp.w, nn = (uint32_t)ntk.z;
-                const uintptr_t a = reinterpret_cast<uintptr_t>(seg_state + si) & ~(uintptr_t)15;
-                const uint32_t sz = (uint32_t)((reinterpret_cast<uintptr_t>(seg_state + si + nn) - a) & ~(uintptr_t)15);
-                if (sz) {
-                    bulk_prefetch_l2(reinterpret_cast<const void*>(a), sz);
-                    bulk_prefetch_l2(reinterpret_cast<const void*>(
-                                         reinterpret_cast<uintptr_t>(seg_off + si) & ~(uintptr_t)15), sz);
-                }
-            }
         }
         if (c != cur_chunk) {
             build_decode_table(blob, T);  // overlaps the bulk copy

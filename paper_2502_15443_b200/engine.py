@@ -221,25 +221,12 @@ class SegmentIndex:
             hi = np.where(end < nsg, off[np.minimum(base + end, nmax)].astype(np.int64), plen)
         if split:  # back to (chunk, first segment) order
             order = np.lexsort((s0, chunk))
-            chunk, s0, cnt, base, lo, hi = (chunk[order], s0[order], cnt[order], base[order], lo[order],
-                                            hi[order])
+            chunk, s0, cnt = chunk[order], s0[order], cnt[order]
         # pinned + async: a pageable copy would block the host behind any
-        # large H2D already queued on the copy engine.  CTA-task decoders take
-        # 8 ints per task: (chunk, s0, count, 0) + the task's staged span
-        # (16-B aligned byte offset in the image, lo/hi 32 bits; bytes) and its
-        # first split-point index, so the kernel can warm L2 for the next task.
-        width = 4 if mode == "small" else 8
-        pin = torch.zeros((len(chunk), width), dtype=torch.int32, pin_memory=True)
+        # large H2D already queued on the copy engine
+        pin = torch.zeros((len(chunk), 4), dtype=torch.int32, pin_memory=True)
         out = pin.numpy()
         out[:, 0], out[:, 1], out[:, 2] = chunk, s0, cnt
-        if width == 8 and len(chunk):
-            start = jobs.blob_off[chunk].astype(np.int64) + HEADER_BYTES
-            a16 = (start + lo) & ~np.int64(15)
-            nbytes = np.where(hi >= lo, (start + hi - a16 + 15) & ~np.int64(15), 0)
-            out[:, 4] = (a16 & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
-            out[:, 5] = (a16 >> 32).astype(np.int32)
-            out[:, 6] = 0 if os.environ.get("DCOMP_NO_PREFETCH") == "1" else np.minimum(nbytes, 1 << 30)
-            out[:, 7] = (base + s0).astype(np.uint32).view(np.int32)
         self.last_tasks_host = out
         return pin.to(_dev(), non_blocking=True)
 
