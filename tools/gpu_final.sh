@@ -10,3 +10,5 @@ ncu --set full --import-source on --clock-control none -k regex:k_decode_segment
 ITERS=2 ncu --set full --import-source on --clock-control none -k regex:k_fused_ring -s 1 -c 1 -o gpurun_out/fused_full python tools/profile_fused.py 0 > gpurun_out/ncu_fused.log 2>&1; echo "ncu fused rc=$?"
 python tools/sweeps.py chunks --sizes 16384,32768,65536,262144,1048576,4194304 --out gpurun_out/c3.json > gpurun_out/c3.log 2>&1; echo "c3 rc=$?"
 python tools/sweeps.py partial --curve gpurun_out/c3.json --out gpurun_out/c4.json > gpurun_out/c4.log 2>&1; echo "c4 rc=$?"
+python tools/int8_scaling.py --out gpurun_out/int8_scaling.json > gpurun_out/int8_scaling.log 2>&1; echo "int8 scaling rc=$?"
+DCOMP_TIMELINE=1 python tools/e2e_timeline.py > gpurun_out/e2e_timeline.txt 2>&1; echo "timeline rc=$?"
