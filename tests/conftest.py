@@ -15,6 +15,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs through the CUDA C-ABI library)")
     config.addinivalue_line("markers", "slow: long-running GPU case")
+    config.addinivalue_line("markers", "perf: opt-in timing comparison (DCOMP_PERF=1)")
 
 
 @pytest.fixture(scope="session")
