@@ -151,22 +151,30 @@ __global__ void __launch_bounds__(kSerialThreads) k_decode_serial(
         };
         issue_upto(4);
         wait_upto((delta + 8) / kSerSlot);
-        auto ldr = [&](uint64_t rel) { return lds_u32(ring + (uint32_t)(rel & (kSerRing - 1))); };
+        auto ldr = [&](uint32_t rel) { return lds_u32(ring + (rel & (kSerRing - 1))); };
         // window: w0 holds the next byte at bit offset o, w1 the next word; wrel = rel offset of w1
-        uint64_t wrel = (delta & ~3u) + 4;
+        // (32-bit: a chunk's stream is < 4 GiB).  One chain, so the step is
+        // written for latency: the window moves with a predicated LDS instead
+        // of a branch, and the symbol step uses the shortest (ALU) form.
+        uint32_t wrel = (delta & ~3u) + 4;
         uint32_t w0 = ldr(wrel - 4), w1 = ldr(wrel), ob = (delta & 3u) * 8u;
         auto advance = [&](uint32_t sel) {
-            ob += 8u * (sel - kSelBase);
-            if (ob >= 32) {
-                ob -= 32;
-                w0 = w1;
-                wrel += 4;
-                w1 = ldr(wrel);
-            }
+            asm volatile(
+                "{\n\t.reg .pred q;\n\t.reg .u32 a;\n\t"
+                "mad.lo.u32 %3, %5, 8, %3;\n\t"
+                "setp.ge.u32 q, %3, 0x10840;\n\t"
+                "@q mov.b32 %0, %1;\n\t"
+                "@q add.u32 %2, %2, 4;\n\t"
+                "and.b32 a, %2, 16383;\n\t"
+                "add.u32 a, a, %4;\n\t"
+                "@q ld.shared.u32 %1, [a];\n\t"
+                "and.b32 %3, %3, 31;\n\t}"
+                : "+r"(w0), "+r"(w1), "+r"(wrel), "+r"(ob)
+                : "r"(ring), "r"(sel));
         };
-        auto rpos = [&]() { return wrel - 4 + (ob >> 3); };  // rel offset of the next unread byte
+        static_assert(kSerRing == 16384, "advance() masks ring offsets with 16383");
+        auto rpos = [&]() { return (uint64_t)(wrel - 4 + (ob >> 3)); };  // rel offset of the next unread byte
         const uint32_t tab = smem_u32(T.tab);
-        const FmaK fk = fma_consts(1u);
         const bool oal = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
         uint32_t x = x0;
         bool bad = false;
@@ -186,8 +194,8 @@ __global__ void __launch_bounds__(kSerialThreads) k_decode_serial(
                 for (int v = 0; v < 16; v += 2) {
                     uint32_t vb, sel = kSelBase;
                     asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(vb) : "r"(w0), "r"(w1), "r"(ob));
-                    const uint32_t e0 = dec_sym(x, sel, vb, tab, fk);
-                    const uint32_t t = __byte_perm(e0, dec_sym(x, sel, vb, tab, fk), 0x0040);
+                    const uint32_t e0 = dec_sym(x, sel, vb, tab);
+                    const uint32_t t = __byte_perm(e0, dec_sym(x, sel, vb, tab), 0x0040);
                     w[v >> 2] = (v & 2) ? __byte_perm(w[v >> 2], t, 0x5410) : t;
                     advance(sel);
                 }
@@ -202,7 +210,7 @@ __global__ void __launch_bounds__(kSerialThreads) k_decode_serial(
                 for (; j < n; ++j) {
                     uint32_t vb, sel = kSelBase;
                     asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(vb) : "r"(w0), "r"(w1), "r"(ob));
-                    o[j] = (uint8_t)dec_sym(x, sel, vb, tab, fk);
+                    o[j] = (uint8_t)dec_sym(x, sel, vb, tab);
                     advance(sel);
                 }
             }
