@@ -54,6 +54,7 @@ def parse_args():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-tp-shard", action="store_true", help="skip the single-GPU TP-8 shard measurement")
+    p.add_argument("--no-index-less", action="store_true", help="skip the index-less (serial) unpack step")
     return p.parse_args()
 
 
@@ -434,6 +435,18 @@ def main():
     e2e = {"value": raw / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": len(host_file) + len(side),
            "d2h_bytes_per_step": raw + 8 * pm.jobs.n, "api": "container.unpack(pinned host file, index=pinned sidecar) -> host ModelBundle",
            "phases_ms": {k: statistics.median(p[k] for p in e2e_phases) for k in e2e_phases[0]}}
+    # the reference's exact call, unpack(file) with no sidecar: every chunk is one
+    # serial rANS chain on the GPU (no split points exist yet); one timed step
+    if not args.no_index_less:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        b2 = container.unpack(pin_file)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        same = b2.tensors[-1].qvalues.tobytes() == bundle.tensors[-1].qvalues.tobytes()
+        e2e["index_less"] = {"value": raw / dt / 1e9, "unit": "GB/s", "api": "container.unpack(pinned host file)",
+                             "seconds": dt, "equal": same}
+        del b2
 
     cpu = None
     if rank == 0 and not args.no_cpu:
