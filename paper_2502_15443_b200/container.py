@@ -539,6 +539,13 @@ def unpack(data, index=None) -> ModelBundle:
         data = _file_bytes(data)
         head, total = data, len(data)
     LAST_UNPACK_MS.clear()
+    binding = None
+    if index is None and _INDEX_CACHE_SIZE > 0:  # split points recorded by an earlier index-less unpack
+        try:
+            binding = binding_of(head)
+            index = _INDEX_CACHE.get(binding)
+        except struct.error:
+            binding = None
     if index is not None:  # split-point path: H2D / decode / D2H pipelined per chunk group
         # chunk table first: the GPU pipeline starts before the header body
         # (names, stats, header CRC) is walked on the host
@@ -577,13 +584,30 @@ def unpack(data, index=None) -> ModelBundle:
     lap("parse")
     base = nv.to_device_bytes(data)
     lap("h2d")
-    res = decode_and_verify(base, ent, index=index)
+    record = binding is not None and index is None
+    res = decode_and_verify(base, ent, index=index, build_index=record)
     lap("decode_crc")
+    if record and res.index is not None and res.index.n_segs:  # verified: keep for the next unpack
+        _INDEX_CACHE[binding] = res.index
+        while len(_INDEX_CACHE) > _INDEX_CACHE_SIZE:
+            _INDEX_CACHE.pop(next(iter(_INDEX_CACHE)))
     host = nv.to_host(res.out)
     lap("d2h")
     out = _bundle(directory, host, chunk_size)
     lap("bundle")
     return out
+
+
+# Split-point indexes recorded by index-less unpacks (the serial pass records
+# them for free), keyed by the container's binding: a later unpack of the same
+# container takes the parallel path.  Device memory: 8 B per 256 B of weights
+# per entry; DCOMP_INDEX_CACHE=0 disables, clear_index_cache() frees.
+_INDEX_CACHE: dict = {}
+_INDEX_CACHE_SIZE = int(os.environ.get("DCOMP_INDEX_CACHE", "2"))
+
+
+def clear_index_cache() -> None:
+    _INDEX_CACHE.clear()
 
 
 LAST_UNPACK_MS: dict[str, float] = {}  # phase timings of the last unpack() (diagnostics)

@@ -276,3 +276,27 @@ def test_decoder_mode_selection_exact(cuda, chunk, mode, monkeypatch):
         out = container.unpack(data, index=side)
         for x, t in zip(out.tensors, ts):
             assert np.array_equal(x.qvalues, t.qvalues)
+
+
+def test_index_less_unpack_records_index_for_next_call(cuda):
+    """unpack(file) with no sidecar runs the serial chains and keeps the split
+    points they record; the next unpack of the same container takes the
+    parallel path (same bytes), and a payload-corrupted copy (same binding)
+    still raises the reference's error."""
+    from paper_2502_15443_b200 import container
+    container.clear_index_cache()
+    tensors, stats = small_model(cuda, rows=400, cols=512)
+    data = cuda.pack(tensors, stats, chunk_size=65536)
+    a = container.unpack(data)
+    assert len(container._INDEX_CACHE) == 1
+    assert "table" not in container.LAST_UNPACK_MS
+    b = container.unpack(data)
+    assert "table" in container.LAST_UNPACK_MS  # pipelined split-point path
+    for x, y, t in zip(a.tensors, b.tensors, tensors):
+        assert np.array_equal(x.qvalues, t.qvalues) and np.array_equal(y.qvalues, t.qvalues)
+    info = cuda.inspect(data)
+    bad = bytearray(data)
+    bad[info.chunks[1].file_offset + 100] ^= 0x10
+    with pytest.raises((cuda.CorruptStreamError, cuda.ChecksumError)):
+        container.unpack(bytes(bad))
+    container.clear_index_cache()
