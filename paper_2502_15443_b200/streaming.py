@@ -22,6 +22,8 @@ would bound device memory without changing the timing).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -127,7 +129,7 @@ class StreamedFused:
     def __init__(self, host_image: torch.Tensor, jobs: engine.JobTable, index: engine.SegmentIndex,
                  chunk_size: int, shapes, t_offs, xs, ntok: int, slots: int = 3, group_bytes: int = 32 << 20):
         from .gemm import FusedRing
-        if not host_image.is_pinned():
+        if host_image is not None and not host_image.is_pinned():
             raise ValueError("host_image must be pinned host memory")
         self.host, self.slots = host_image, slots
         dev = index.d_state.device
@@ -187,6 +189,178 @@ class StreamedFused:
 
     def check(self) -> bool:
         return all(not (fr.check() != 0).any() for _, _, _, fr in self.groups)
+
+
+_PAGE = 4096
+
+
+def _open(path: str, direct: bool) -> tuple[int, bool]:
+    """Open for reading, O_DIRECT when asked and supported (tmpfs is not)."""
+    if direct:
+        try:
+            return os.open(path, os.O_RDONLY | os.O_DIRECT), True
+        except OSError:
+            pass
+    return os.open(path, os.O_RDONLY), False
+
+
+def _read_range(fd: int, buf: torch.Tensor, f0: int, f1: int) -> int:
+    """Read file bytes [f0, f1) into the page-aligned pinned ``buf`` starting at
+    a page boundary (O_DIRECT needs aligned offset, size and address); returns
+    the offset of f0 inside ``buf``."""
+    a = f0 & ~(_PAGE - 1)
+    b = (f1 + _PAGE - 1) & ~(_PAGE - 1)
+    mv = memoryview(buf.numpy())[: b - a]
+    got = 0
+    while got < b - a:
+        n = os.preadv(fd, [mv[got:]], a + got)
+        if n <= 0:
+            break
+        got += n
+    if got < f1 - a:
+        raise OSError(f"short read at {a + got} (wanted through {f1})")
+    return f0 - a
+
+
+class StreamedFusedFile(StreamedFused):
+    """GPU_DISK tier (the reference's storage -> CPU -> GPU path, B_stoc /
+    B_ctog, latency.py:33-37): the container file stays on disk; every step
+    reads each layer group's byte range (O_DIRECT by default, so the page
+    cache does not stand in for the disk) into one of ``slots`` pinned host
+    buffers on reader threads, copies it to a device slot and runs the fused
+    decode -> GEMM on it.  Reads, H2D and decode of different groups overlap."""
+
+    def __init__(self, path: str, jobs: engine.JobTable, index: engine.SegmentIndex, chunk_size: int, shapes,
+                 t_offs, xs, ntok: int, slots: int = 4, group_bytes: int = 32 << 20, direct: bool = True,
+                 threads: int = 4):
+        from concurrent.futures import ThreadPoolExecutor
+        super().__init__(None, jobs, index, chunk_size, shapes, t_offs, xs, ntok, slots, group_bytes)
+        self.fd, self.direct = _open(path, direct)
+        self.hslots = [torch.empty(self.slot_bytes + 2 * _PAGE, dtype=torch.uint8, pin_memory=True)
+                       for _ in range(slots)]
+        self.h2d_done = [None] * slots
+        self.pool = ThreadPoolExecutor(max_workers=threads)
+
+    def close(self) -> None:
+        self.pool.shutdown()
+        os.close(self.fd)
+
+    def _read(self, g: int) -> int:
+        slot, f0, f1, _ = self.groups[g]
+        ev = self.h2d_done[slot]
+        if ev is not None:
+            ev.synchronize()  # the slot's previous H2D has read the pinned buffer
+        return _read_range(self.fd, self.hslots[slot], f0, f1)
+
+    def step(self) -> None:
+        s_comp = torch.cuda.current_stream()
+        G, S = len(self.groups), self.slots
+        futs = {g: self.pool.submit(self._read, g) for g in range(min(S, G))}
+        for g, (slot, f0, f1, fr) in enumerate(self.groups):
+            off = futs.pop(g).result()
+            with torch.cuda.stream(self.s_copy):
+                if self.ev_free[slot] is not None:
+                    self.s_copy.wait_event(self.ev_free[slot])
+                fr.image.copy_(self.hslots[slot][off:off + (f1 - f0)], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.s_copy)
+            self.h2d_done[slot] = ev
+            s_comp.wait_event(ev)
+            fr.run()
+            self.ev_free[slot] = torch.cuda.Event()
+            self.ev_free[slot].record(s_comp)
+            if g + S < G:
+                futs[g + S] = self.pool.submit(self._read, g + S)
+
+
+class StreamedRawFile:
+    """Baseline of the disk tier: raw INT8 weights read from a file every step
+    (same reader threads / pinned slots / O_DIRECT), copied to the device
+    weight buffer, then the grouped INT8 GEMM."""
+
+    def __init__(self, path: str, nbytes: int, device, slots: int = 4, group_bytes: int = 64 << 20,
+                 direct: bool = True, threads: int = 4):
+        from concurrent.futures import ThreadPoolExecutor
+        self.fd, self.direct = _open(path, direct)
+        self.out = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        self.groups = [(a, min(nbytes, a + group_bytes)) for a in range(0, nbytes, group_bytes)]
+        self.slots = slots
+        self.hslots = [torch.empty(group_bytes + 2 * _PAGE, dtype=torch.uint8, pin_memory=True)
+                       for _ in range(slots)]
+        self.h2d_done = [None] * slots
+        self.pool = ThreadPoolExecutor(max_workers=threads)
+        self.s_copy = torch.cuda.Stream(device)
+        self.bytes_per_step = nbytes
+
+    def close(self) -> None:
+        self.pool.shutdown()
+        os.close(self.fd)
+
+    def _read(self, g: int) -> int:
+        slot = g % self.slots
+        if self.h2d_done[slot] is not None:
+            self.h2d_done[slot].synchronize()
+        a, b = self.groups[g]
+        return _read_range(self.fd, self.hslots[slot], a, b)
+
+    def step(self) -> None:
+        G, S = len(self.groups), self.slots
+        futs = {g: self.pool.submit(self._read, g) for g in range(min(S, G))}
+        for g, (a, b) in enumerate(self.groups):
+            off = futs.pop(g).result()
+            slot = g % S
+            with torch.cuda.stream(self.s_copy):
+                self.out[a:b].copy_(self.hslots[slot][off:off + (b - a)], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.s_copy)
+            self.h2d_done[slot] = ev
+            if g + S < G:
+                futs[g + S] = self.pool.submit(self._read, g + S)
+        torch.cuda.current_stream().wait_stream(self.s_copy)
+
+
+def measure_disk(model_payload: torch.Tensor, shapes, offs, image: torch.Tensor, jobs, index, ntok: int = 1,
+                 iters: int = 3, workdir: str | None = None, direct: bool = True) -> dict:
+    """Per-step time of the disk tier: raw INT8 file vs compressed DCC1 image
+    file, each read every step (O_DIRECT), fused decode -> GEMM vs INT8 GEMM."""
+    import tempfile
+    from .adaptive import time_ms
+    dev = model_payload.device
+    workdir = workdir or tempfile.gettempdir()
+    raw_path = os.path.join(workdir, "dcomp_disk_raw.bin")
+    img_path = os.path.join(workdir, "dcomp_disk_img.dcc")
+    model_payload.cpu().numpy().tofile(raw_path)
+    image.cpu().numpy().tofile(img_path)
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    xs = [torch.randint(-127, 128, (ntok, c), generator=g, device=dev, dtype=torch.int8) for _, c in shapes]
+    out = {"direct_io": direct}
+    raw = StreamedRawFile(raw_path, model_payload.numel(), dev, direct=direct)
+    gemm_raw = GroupedInt8(layer_views(raw.out, shapes, offs), xs, ntok)
+    chunk = int(jobs.out_len.max())
+    comp = StreamedFusedFile(img_path, jobs, index, chunk, shapes, offs, xs, ntok, direct=direct)
+    try:
+        raw.step()
+        gemm_raw.run()
+        comp.step()
+        torch.cuda.synchronize()
+        ok = comp.check() and all(torch.equal(a, b) for a, b in zip(gemm_raw.accs, comp.accs))
+        t_raw = time_ms(lambda: (raw.step(), gemm_raw.run()), iters, warmup=1)
+        t_comp = time_ms(comp.step, iters, warmup=1)
+        out["direct_io"] = raw.direct and comp.direct
+        out.update({"raw_step_ms": t_raw, "compressed_step_ms": t_comp, "speedup": t_raw / t_comp,
+                    "raw_read_bytes": raw.bytes_per_step, "compressed_read_bytes": comp.bytes_per_step,
+                    "raw_read_gbs": raw.bytes_per_step / t_raw / 1e6, "outputs_equal": ok,
+                    "device_bytes_compressed": comp.device_bytes})
+    finally:
+        raw.close()
+        comp.close()
+        for p in (raw_path, img_path):
+            try:
+                os.remove(p)
+            except OSError:
+                pass
+    return out
 
 
 def layer_views(buf: torch.Tensor, shapes, offs) -> list[torch.Tensor]:

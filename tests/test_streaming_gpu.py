@@ -43,3 +43,15 @@ def test_streamed_fused_bounded_ring(cuda):
             w = m.payload[o:o + r * c].view(torch.int8).view(r, c).cpu().long()
             assert torch.equal(acc.cpu().long(), x.cpu().long() @ w.T)
     assert isinstance(sf.bytes_per_step, int) and np.isfinite(sf.device_bytes)
+
+
+def test_disk_tier_fused_equals_int8(cuda, tmp_path):
+    """GPU_DISK tier: raw INT8 file and DCC1 image file read every step
+    (O_DIRECT where the filesystem allows) -- fused outputs equal the INT8 GEMM's."""
+    from paper_2502_15443_b200 import streaming, synth
+    m = synth.build_model("opt-125m", layers=2)
+    pm = synth.pack_model(m, 4 << 20, seg_shift=8)
+    r = streaming.measure_disk(m.payload, m.shapes, m.offsets()[:-1], pm.image, pm.jobs, pm.index, ntok=2,
+                               iters=1, workdir=str(tmp_path))
+    assert r["outputs_equal"]
+    assert r["compressed_read_bytes"] < r["raw_read_bytes"]
