@@ -55,6 +55,7 @@ def parse_args():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-tp-shard", action="store_true", help="skip the single-GPU TP-8 shard measurement")
     p.add_argument("--no-index-less", action="store_true", help="skip the index-less (serial) unpack step")
+    p.add_argument("--no-disk", action="store_true", help="skip the disk-tier streaming measurement")
     return p.parse_args()
 
 
@@ -379,6 +380,17 @@ def main():
     except Exception as e:  # report, never hide
         streaming_tier = {"skipped" if world > 1 else "error": repr(e)[:300]}
 
+    # GPU_DISK tier (B_stoc): raw INT8 file vs DCC1 file read from disk every
+    # step (O_DIRECT), fused decode -> GEMM vs INT8 GEMM; N=1 only
+    disk_tier = None
+    if world == 1 and not args.no_disk:
+        try:
+            from paper_2502_15443_b200 import streaming
+            disk_tier = streaming.measure_disk(m.payload, m.shapes, offs, pm.image, pm.jobs, pm.index, ntok=1,
+                                               iters=3, workdir=os.path.join(ROOT, "gpurun_out"))
+        except Exception as e:  # report, never hide
+            disk_tier = {"error": repr(e)[:300]}
+
     # config C5 under torchrun: LLaMA-13B-shaped tensor parallelism across
     # the ranks (fused compressed vs INT8 per rank + NCCL int32 all-reduce)
     tp = None
@@ -478,6 +490,7 @@ def main():
             "decode_step_tokens": tokens,
             "tp_decode": tp,
             "streaming_tier": streaming_tier,
+            "disk_tier": disk_tier,
             "gpu_launches": args.steps * (1 + int(has_store)),
             "clocks": clocks.summary(),
         }
