@@ -380,6 +380,10 @@ def main():
     except Exception as e:  # report, never hide
         streaming_tier = {"skipped" if world > 1 else "error": repr(e)[:300]}
 
+    def adaptive_h2d():
+        from paper_2502_15443_b200 import adaptive
+        return adaptive.measure_h2d_gbs(1 << 28)
+
     # GPU_DISK tier (B_stoc): raw INT8 file vs DCC1 file read from disk every
     # step (O_DIRECT), fused decode -> GEMM vs INT8 GEMM; N=1 only
     disk_tier = None
@@ -388,6 +392,21 @@ def main():
             from paper_2502_15443_b200 import streaming
             disk_tier = streaming.measure_disk(m.payload, m.shapes, offs, pm.image, pm.jobs, pm.index, ntok=1,
                                                iters=3, workdir=os.path.join(ROOT, "gpurun_out"))
+            # the reference's latency model for its STORAGE architecture, B_stoc =
+            # the measured raw read rate of this disk
+            import importlib
+            latency = importlib.import_module("paper_2502_15443_b200.latency")
+            stoc = disk_tier["raw_read_gbs"]
+            dprof = latency.HardwareProfile(B_stoc=stoc, B_ctog=adaptive_h2d(), B_gpu=hbm, D_max=value, c_sat=1.0,
+                                            I_gpu=tokens["B1"]["int8_weight_gbs"], mem_gpu=1e12, mem_cpu=1e12)
+            n_ch = int(pm.jobs.n)
+            arch = latency.Architecture.STORAGE
+            none = latency.CompressionPlan.block_plan(args.chunk_size, n_ch, 0)
+            full = latency.CompressionPlan.block_plan(args.chunk_size, n_ch, 1)
+            disk_tier.update({
+                "B_stoc_gbs": stoc,
+                "predicted_raw_ms": latency.latency(dprof, none, arch).per_sample_latency * 1e3,
+                "predicted_compressed_ms": latency.latency(dprof, full, arch, raw / comp).per_sample_latency * 1e3})
         except Exception as e:  # report, never hide
             disk_tier = {"error": repr(e)[:300]}
 
