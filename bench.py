@@ -76,10 +76,11 @@ def ncu_traffic(kernel: str, config: dict):
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             e = json.load(f)[kernel]
         if all(config.get(k) == v for k, v in e["config"].items()):
-            return e["dram_bytes_per_launch"], e["report"]
+            pipes = {k: e[k] for k in ("alu_pipe_pct", "fma_pipe_pct", "issue_active_pct", "l1tex_pct") if k in e}
+            return e["dram_bytes_per_launch"], e["report"], pipes
     except Exception:
         pass
-    return None, None
+    return None, None, {}
 
 
 class ClockSampler:
@@ -487,8 +488,9 @@ def main():
         except Exception as e:  # report, never fake
             cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
 
-    traffic, traffic_src = ncu_traffic("k_decode_segments", {"model": args.model, "chunk_size": args.chunk_size,
-                                                            "seg_shift": args.seg_shift, "layers": args.layers})
+    traffic, traffic_src, pipes = ncu_traffic("k_decode_segments", {"model": args.model,
+                                                                   "chunk_size": args.chunk_size,
+                                                                   "seg_shift": args.seg_shift, "layers": args.layers})
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -503,7 +505,10 @@ def main():
                        "build_s": t_build},
             "roofline": {"bound": "hbm", "kernel": "k_decode_segments", "achieved": achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                         "traffic_src": traffic_src, "alg_bytes_per_launch": alg_bytes, "launch_ms": kms},
+                         "traffic_src": traffic_src, "alg_bytes_per_launch": alg_bytes, "launch_ms": kms,
+                         # the decode is bound by instruction issue on the ALU pipe, not HBM
+                         # (same ncu capture): see DESIGN.md "Why the decode is not at the HBM roofline"
+                         "ncu_pipes": pipes},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "decode_step_tokens": tokens,

@@ -49,6 +49,13 @@ def main():
     name = re.sub(r"\W", "", a.kernel.split(":")[-1])
     doc[name] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr, "duration_us": dur,
                  "config": json.loads(a.config), "report": os.path.basename(a.report)}
+    # what actually bounds the kernel: issue and the busiest pipes (ALU for rANS)
+    for key, metric in (("alu_pipe_pct", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                        ("fma_pipe_pct", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                        ("issue_active_pct", "sm__inst_issued.avg.pct_of_peak_sustained_active"),
+                        ("l1tex_pct", "l1tex__throughput.avg.pct_of_peak_sustained_active")):
+        if metric in col:
+            doc[name][key] = float(d[col[metric]].replace(",", ""))
     with open(a.out, "w") as f:
         json.dump(doc, f, indent=1)
     print(json.dumps(doc[name]))
