@@ -207,7 +207,7 @@ int dc_dequantize(const int8_t *q, double w_scale, const double *s, int64_t rows
 int dc_scale_weights(const double *w, const double *s, int64_t rows, int64_t cols, double *out, void *stream);
 
 /* ------------------------------------------------------ pruning (kernel 1)
- * Zero the k lowest scores cm[c]*|q| (f64), ties by row-major index.
+ * Zero the k lowest scores cm[c]*|q| (f64), ties by row-major index (rows*cols < 2^32).
  * replaces pruning.py:37-64 (prune_scores, _lowest_k, prune). */
 int dc_prune_scratch_bytes(int64_t rows, int64_t cols, uint64_t *out_host);
 int dc_prune_tensor(const int8_t *q, const double *cm, int64_t rows, int64_t cols, int64_t k, int8_t *out,

@@ -54,12 +54,24 @@ __global__ void k_select_hist(const uint32_t* __restrict__ counts, const double*
     const int64_t n = cols * kBins;
     const unsigned long long prefix = st->prefix;
     const int top = shift + 16;  // bits above this pass's digit
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t cnt = counts[i];
-        if (!cnt) continue;
-        const unsigned long long key = key_of(cm[i / kBins], (int)(i % kBins));
-        if (top < 64 && (key >> top) != prefix) continue;
-        atomicAdd(&hist[(key >> shift) & 0xFFFF], (unsigned long long)cnt);
+    // whole warps iterate together so equal digits can be combined: the first
+    // pass (top 16 key bits) sends nearly every entry to a handful of bins
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        uint32_t cnt = 0, bin = 0xFFFFFFFFu;
+        if (i < n) {
+            cnt = counts[i];
+            if (cnt) {
+                const uint32_t col = (uint32_t)i / (uint32_t)kBins;  // n < 2^32: 32-bit magic division
+                const unsigned long long key = key_of(cm[col], (int)((uint32_t)i - col * (uint32_t)kBins));
+                if (top >= 64 || (key >> top) == prefix) bin = (uint32_t)((key >> shift) & 0xFFFF);
+            }
+        }
+        const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+        const uint32_t sum = __reduce_add_sync(peers, bin == 0xFFFFFFFFu ? 0u : cnt);
+        if (bin != 0xFFFFFFFFu && (threadIdx.x & 31) == __ffs(peers) - 1)
+            atomicAdd(&hist[bin], (unsigned long long)sum);
     }
 }
 
@@ -109,23 +121,45 @@ __global__ void __launch_bounds__(1024) k_excl_scan(uint32_t* __restrict__ v, in
     const int t = threadIdx.x;
     const int64_t per = (n + 1023) / 1024;
     unsigned long long s = 0;
+#pragma unroll 8
     for (int64_t i = t * per; i < min(n, (t + 1) * per); ++i) s += v[i];
-    part[t] = s;
+    // block-wide exclusive scan of the 1024 thread sums (warp scans + a scan of
+    // the 32 warp totals; counts < 2^32, see dc_prune_tensor)
+    const int lane = t & 31, w = t >> 5;
+    uint32_t inc = (uint32_t)s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    __shared__ uint32_t wtot[32];
+    if (lane == 31) wtot[w] = inc;
     __syncthreads();
-    if (t == 0) {
-        unsigned long long acc = 0;
-        for (int i = 0; i < 1024; ++i) {
-            const unsigned long long x = part[i];
-            part[i] = acc;
-            acc += x;
+    if (w == 0) {
+        const uint32_t x0 = wtot[lane];
+        uint32_t x = x0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += o;
         }
+        wtot[lane] = x - x0;
     }
     __syncthreads();
+    part[t] = wtot[w] + inc - (uint32_t)s;
+    __syncthreads();
     unsigned long long acc = part[t];
-    for (int64_t i = t * per; i < min(n, (t + 1) * per); ++i) {
-        const uint32_t x = v[i];
-        v[i] = (uint32_t)acc;
-        acc += x;
+    const int64_t e = min(n, (t + 1) * per);
+    for (int64_t i0 = t * per; i0 < e; i0 += 8) {  // 8 loads in flight, then the stores
+        uint32_t x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = i0 + j < e ? v[i0 + j] : 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (i0 + j < e) {
+                v[i0 + j] = (uint32_t)acc;
+                acc += x[j];
+            }
     }
 }
 
@@ -213,11 +247,18 @@ __global__ void __launch_bounds__(1024) k_select_pick2(const unsigned long long*
     __shared__ int s_part;
     __shared__ unsigned long long s_base;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    for (int i = 0; i < 64; ++i) {
-        unsigned long long v = hist[i * 1024 + t];
+    // partial p = bins [32p, 32p + 32): warp w, round i reduces partial 32i + w
+    // from one coalesced 256-B load with one REDUX (the host caps a tensor at
+    // 2^32 - 1 elements, so every partial fits 32 bits); 16 loads in flight
+    for (int i0 = 0; i0 < 64; i0 += 16) {
+        unsigned long long v[16];
 #pragma unroll
-        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-        if (lane == 0) part[i * 32 + w] = v;
+        for (int j = 0; j < 16; ++j) v[j] = hist[(i0 + j) * 1024 + t];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t sum = __reduce_add_sync(0xffffffffu, (uint32_t)v[j]);
+            if (lane == 0) part[(i0 + j) * 32 + w] = sum;
+        }
     }
     __syncthreads();
     const unsigned long long a = part[2 * t], b = part[2 * t + 1], s = a + b;
@@ -556,6 +597,10 @@ extern "C" int dc_prune_scratch_bytes(int64_t rows, int64_t cols, uint64_t* out)
 extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, int64_t cols, int64_t k,
                                int8_t* out, uint8_t* scratch, void* stream) {
     if (rows < 0 || cols < 0 || k < 0 || k > rows * cols) return DC_ERR_ARG;
+    if (rows * cols > 0xFFFFFFFFll) {  // selection partials are summed in 32 bits
+        set_error_msg("dc_prune_tensor: at most 2^32 - 1 elements per tensor");
+        return DC_ERR_ARG;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = rows * cols;
     if (n == 0) return DC_OK;
