@@ -422,6 +422,17 @@ __global__ void __launch_bounds__(kPrThreads) k_apply2(const int8_t* __restrict_
     }
 }
 
+static int sm_count_pr() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
 // ---------------------------------------------------------------- per row
 // Register path (cols <= 4096): a CTA per row, 16 columns per thread, keys
 // computed once; 8 x 8-bit radix passes over a shared 256-bin histogram with a
@@ -448,6 +459,7 @@ __device__ __forceinline__ void block_pick256(const uint32_t* hist, unsigned lon
     if (lo < kk && kk <= (unsigned long long)inc) {
         *s_prefix = (prefix << 8) | (unsigned long long)t;
         *s_k = kk - lo;
+        s_k[1] = v;  // the chosen bucket's population
     }
     __syncthreads();
     prefix = *s_prefix;
@@ -455,63 +467,121 @@ __device__ __forceinline__ void block_pick256(const uint32_t* hist, unsigned lon
 }
 
 __global__ void __launch_bounds__(kPrThreads) k_prune_rows2(const int8_t* __restrict__ q, const double* __restrict__ cm,
-                                                             int64_t cols, int64_t k, int8_t* __restrict__ out) {
+                                                             int64_t rows, int64_t cols, int64_t k,
+                                                             int8_t* __restrict__ out) {
+    // persistent over rows: thread t owns columns [16t, 16t + 16) of every row,
+    // their channel maxima stay in registers (one load per CTA, not per row)
     __shared__ uint32_t hist[256];
     __shared__ uint32_t wsum[kPrThreads / 32];
-    __shared__ unsigned long long s_prefix, s_k;
-    const int t = threadIdx.x;
-    const int8_t* qr = q + (int64_t)blockIdx.x * cols;
-    int8_t* orow = out + (int64_t)blockIdx.x * cols;
+    __shared__ unsigned long long s_prefix, s_k[2], s_min[kPrThreads / 32], s_max[kPrThreads / 32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int c0 = t * 16;
-    int8_t v[16];
-    unsigned long long key[16];
+    double cmr[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const int c = c0 + j;
-        v[j] = c < cols ? qr[c] : 0;
-        key[j] = c < cols ? key_of(cm[c], absq(v[j])) : ~0ull;
-    }
-    unsigned long long prefix = 0, kk = (unsigned long long)k;
-    for (int pass = 0; pass < 8; ++pass) {
-        const int shift = 56 - 8 * pass;
-        hist[t] = 0;
+    for (int j = 0; j < 16; ++j) cmr[j] = c0 + j < cols ? cm[c0 + j] : 0.0;
+    const bool vec = (cols & 15) == 0 && ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        const int8_t* qr = q + row * cols;
+        int8_t* orow = out + row * cols;
+        int8_t v[16];
+        if (vec) {
+            uint4 qv = make_uint4(0, 0, 0, 0);
+            if (c0 < cols) qv = *reinterpret_cast<const uint4*>(qr + c0);
+            memcpy(v, &qv, 16);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = c0 + j < cols ? qr[c0 + j] : 0;
+        }
+        unsigned long long key[16];
+        unsigned long long kmin = ~0ull, kmax = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            key[j] = c0 + j < cols ? key_of(cmr[j], absq(v[j])) : ~0ull;
+            if (c0 + j < cols) {
+                kmin = min(kmin, key[j]);
+                kmax = max(kmax, key[j]);
+            }
+        }
+        // the row's keys share their leading bytes (scores span a few binades):
+        // start the radix passes at the first byte where min and max differ
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, d));
+            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, d));
+        }
+        __syncthreads();  // previous row done with the shared scratch
+        if (lane == 0) {
+            s_min[w] = kmin;
+            s_max[w] = kmax;
+        }
         __syncthreads();
+        for (int i = 0; i < kPrThreads / 32; ++i) {
+            kmin = min(kmin, s_min[i]);
+            kmax = max(kmax, s_max[i]);
+        }
+        const int p0 = kmin == kmax ? 8 : __clzll(kmin ^ kmax) / 8;
+        unsigned long long prefix = p0 == 0 ? 0ull : p0 == 8 ? kmin : kmin >> (64 - 8 * p0);
+        unsigned long long kk = (unsigned long long)k;
+        for (int pass = p0; pass < 8; ++pass) {
+            const int shift = 56 - 8 * pass;
+            hist[t] = 0;
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < cols && (pass == 0 || (key[j] >> (shift + 8)) == prefix))
+                    atomicAdd(&hist[(key[j] >> shift) & 0xFF], 1u);
+            __syncthreads();
+            block_pick256(hist, prefix, kk, &s_prefix, s_k, wsum);
+            if (s_k[1] == 1 && shift > 0) {  // one key in the bucket: it is the threshold
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < cols && (key[j] >> shift) == prefix) s_prefix = key[j];
+                __syncthreads();
+                prefix = s_prefix;
+                break;
+            }
+        }
+        // ordered ties: zero key < T, and the first kk entries with key == T
+        const unsigned long long T = prefix;
+        uint32_t eqm = 0, ltm = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            eqm |= (uint32_t)(c0 + j < cols && key[j] == T) << j;
+            ltm |= (uint32_t)(key[j] < T) << j;
+        }
+        const uint32_t cnt = __popc(eqm);
+        uint32_t inc = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        __syncthreads();
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        uint32_t before = 0;
+        for (int i = 0; i < w; ++i) before += wsum[i];
+        unsigned long long rank = before + inc - cnt;
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-            if (c0 + j < cols && (pass == 0 || (key[j] >> (shift + 8)) == prefix))
-                atomicAdd(&hist[(key[j] >> shift) & 0xFF], 1u);
-        __syncthreads();
-        block_pick256(hist, prefix, kk, &s_prefix, &s_k, wsum);
-    }
-    // ordered ties: zero key < T, and the first kk entries with key == T
-    const unsigned long long T = prefix;
-    uint32_t eqm = 0, ltm = 0;
+            if ((eqm >> j) & 1) {
+                if (rank < kk) ltm |= 1u << j;
+                ++rank;
+            }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        eqm |= (uint32_t)(c0 + j < cols && key[j] == T) << j;
-        ltm |= (uint32_t)(key[j] < T) << j;
-    }
-    const uint32_t cnt = __popc(eqm);
-    const int lane = t & 31, w = t >> 5;
-    uint32_t inc = cnt;
+        for (int j = 0; j < 16; ++j)
+            if ((ltm >> j) & 1) v[j] = 0;
+        if (vec) {
+            if (c0 < cols) {
+                uint4 o;
+                memcpy(&o, v, 16);
+                *reinterpret_cast<uint4*>(orow + c0) = o;
+            }
+        } else {
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += o;
-    }
-    __syncthreads();
-    if (lane == 31) wsum[w] = inc;
-    __syncthreads();
-    uint32_t before = 0;
-    for (int i = 0; i < w; ++i) before += wsum[i];
-    unsigned long long rank = before + inc - cnt;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if ((eqm >> j) & 1) {
-            if (rank < kk) ltm |= 1u << j;
-            ++rank;
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < cols) orow[c0 + j] = v[j];
         }
-        if (c0 + j < cols) orow[c0 + j] = ((ltm >> j) & 1) ? (int8_t)0 : v[j];
     }
 }
 
@@ -670,7 +740,9 @@ extern "C" int dc_prune_rows(const int8_t* q, const double* cm, int64_t rows, in
     if (rows < 0 || cols < 0 || k < 0 || k > cols) return DC_ERR_ARG;
     if (rows == 0 || cols == 0) return DC_OK;
     if (k > 0 && cols <= kRowMax) {
-        k_prune_rows2<<<(unsigned)rows, kPrThreads, 0, (cudaStream_t)stream>>>(q, cm, cols, k, out);
+        const int64_t cap = (int64_t)sm_count_pr() * 2;  // resident CTAs (123 regs x 256 threads)
+        k_prune_rows2<<<(unsigned)(rows < cap ? rows : cap), kPrThreads, 0, (cudaStream_t)stream>>>(q, cm, rows,
+                                                                                                  cols, k, out);
         DC_CHECK_LAUNCH("k_prune_rows2");
         return DC_OK;
     }

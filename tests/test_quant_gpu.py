@@ -95,6 +95,26 @@ def test_prune_matches_oracle_random(cuda, oracle):
             assert (q == 0).sum() + newly.sum() >= int(np.floor(sp * q.size))
 
 
+def test_prune_per_row_wide_rows_match_oracle(cuda, oracle):
+    """Per-row selection on wide rows (the register path, up to 4096 columns):
+    rows whose keys are all equal, rows dominated by ties, rows of distinct
+    scores (the early exit when a bucket holds one key) -- zero sets equal the
+    reference's stable-argsort result."""
+    rng = np.random.default_rng(55)
+    for cols, sp in ((4096, 0.2), (4000, 0.5), (3000, 0.01), (4096, 0.999)):
+        rows = 24
+        q = np.clip(np.round(rng.normal(0, 25, (rows, cols))), -127, 127).astype(np.int8)
+        q[0, :] = 7                       # with constant cm: every key equal
+        q[1, :] = rng.choice([-3, 3, 5], cols)  # heavy ties
+        cm = rng.lognormal(-1, 1.5, cols)
+        cm_const = np.full(cols, 0.75)
+        for c_vec in (cm, cm_const):
+            qt = cuda.QuantizedTensor("r", q, 0.1, cuda.ScaleVector.identity(cols))
+            st = cuda.ActivationStats("r", c_vec)
+            got = cuda.prune(qt, st, cuda.PruneConfig(sp, cuda.PruneScope.PER_ROW)).qvalues
+            assert np.array_equal(got, oracle.prune(q, c_vec, sp, True)), (cols, sp)
+
+
 def test_prune_properties(cuda):
     rng = np.random.default_rng(44)
     q = np.clip(np.round(rng.normal(0, 20, (256, 512))), -127, 127).astype(np.int8)
