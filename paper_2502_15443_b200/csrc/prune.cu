@@ -328,23 +328,26 @@ __device__ __forceinline__ void flags16(const int8_t* __restrict__ q, const uint
                                         bool vec, int8_t (&v)[16], uint32_t& ltm, uint32_t& eqm) {
     ltm = eqm = 0;
     if (vec && i0 + 16 <= n) {  // cols % 16 == 0: one row, 16-B aligned
-        const int64_t c0 = i0 % cols;
+        const int64_t c0 = (uint32_t)i0 % (uint32_t)cols;  // n < 2^32 (dc_prune_tensor): 32-bit division
         const uint4 qv = *reinterpret_cast<const uint4*>(q + i0);
         const uint4 lv = *reinterpret_cast<const uint4*>(lo + c0);
         const uint4 hv = *reinterpret_cast<const uint4*>(hi + c0);
         memcpy(v, &qv, 16);
-        uint8_t l8[16], h8[16];
-        memcpy(l8, &lv, 16);
-        memcpy(h8, &hv, 16);
+        // four bytes per SIMD op: |q| (0x80 -> 128, unsigned), byte compares
+        // against the column bounds, byte masks folded to 4 bits each
+        const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w},
+                       hw[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const int a = absq(v[k]);
-            ltm |= (uint32_t)(a < l8[k]) << k;
-            eqm |= (uint32_t)(a >= l8[k] && a < h8[k]) << k;
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t a = __vabs4(qw[k]);
+            const uint32_t lt = __vcmpltu4(a, lw[k]);
+            const uint32_t eq = __vcmpltu4(a, hw[k]) & ~lt;
+            ltm |= (((lt & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
+            eqm |= (((eq & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
         }
         return;
     }
-    int64_t c = i0 % cols;
+    int64_t c = (uint32_t)i0 % (uint32_t)cols;
     for (int k = 0; k < 16; ++k) {
         const int64_t i = i0 + k;
         v[k] = 0;
@@ -358,13 +361,24 @@ __device__ __forceinline__ void flags16(const int8_t* __restrict__ q, const uint
     }
 }
 
+// Fast per-element passes: a block covers kEqSub sub-tiles of kEqBlock
+// elements (thread t: 16 elements at sub-tile r, offset 16t); all kEqSub
+// 16-B loads are issued before any use, so each thread keeps 4 in flight.
+constexpr int kEqSub = 4;
+constexpr int64_t kEqBlock2 = (int64_t)kEqSub * kEqBlock;
+
 __global__ void __launch_bounds__(kPrThreads) k_eq_count2(const int8_t* __restrict__ q, const uint8_t* __restrict__ lo,
                                                            const uint8_t* __restrict__ hi, int64_t n, int64_t cols,
                                                            bool vec, uint32_t* __restrict__ blk_cnt) {
-    int8_t v[16];
-    uint32_t ltm, eqm;
-    flags16(q, lo, hi, n, cols, (int64_t)blockIdx.x * kEqBlock + threadIdx.x * 16, vec, v, ltm, eqm);
-    uint32_t cnt = __popc(eqm);
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int r = 0; r < kEqSub; ++r) {
+        int8_t v[16];
+        uint32_t ltm, eqm;
+        flags16(q, lo, hi, n, cols, (int64_t)blockIdx.x * kEqBlock2 + r * kEqBlock + threadIdx.x * 16, vec, v, ltm,
+                eqm);
+        cnt += __popc(eqm);
+    }
     __shared__ uint32_t red[kPrThreads / 32];
 #pragma unroll
     for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
@@ -382,43 +396,59 @@ __global__ void __launch_bounds__(kPrThreads) k_apply2(const int8_t* __restrict_
                                                         bool vec, const SelectState* __restrict__ st,
                                                         const uint32_t* __restrict__ blk_prefix,
                                                         int8_t* __restrict__ out) {
-    const unsigned long long r = st->k;
-    const int64_t i0 = (int64_t)blockIdx.x * kEqBlock + threadIdx.x * 16;
-    int8_t v[16];
-    uint32_t ltm, eqm;
-    flags16(q, lo, hi, n, cols, i0, vec, v, ltm, eqm);
-    // block-exclusive scan of per-thread tie counts (row-major order)
-    const uint32_t cnt = __popc(eqm);
+    const unsigned long long r_keep = st->k;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t inc = cnt;
+    int8_t v[kEqSub][16];
+    uint32_t ltm[kEqSub], eqm[kEqSub];
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += o;
+    for (int r = 0; r < kEqSub; ++r)
+        flags16(q, lo, hi, n, cols, (int64_t)blockIdx.x * kEqBlock2 + r * kEqBlock + threadIdx.x * 16, vec, v[r],
+                ltm[r], eqm[r]);
+    __shared__ uint32_t ws[kEqSub][kPrThreads / 32];
+    // tie ranks in row-major order: sub-tile r before r + 1, thread t before t + 1
+    uint32_t inc[kEqSub];
+#pragma unroll
+    for (int r = 0; r < kEqSub; ++r) {
+        inc[r] = __popc(eqm[r]);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc[r], d);
+            if (lane >= d) inc[r] += o;
+        }
+        if (lane == 31) ws[r][w] = inc[r];
     }
-    __shared__ uint32_t ws[kPrThreads / 32];
-    if (lane == 31) ws[w] = inc;
     __syncthreads();
-    uint32_t before = 0;
-    for (int k = 0; k < w; ++k) before += ws[k];
-    unsigned long long rank = (unsigned long long)blk_prefix[blockIdx.x] + before + inc - cnt;
-    uint32_t zero = ltm;
+    unsigned long long base = blk_prefix[blockIdx.x];
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-        if ((eqm >> k) & 1) {
-            if (rank < r) zero |= 1u << k;
+    for (int r = 0; r < kEqSub; ++r) {
+        uint32_t before = 0, total = 0;
+        for (int k = 0; k < kPrThreads / 32; ++k) {
+            const uint32_t x = ws[r][k];
+            before += k < w ? x : 0u;
+            total += x;
+        }
+        unsigned long long rank = base + before + inc[r] - __popc(eqm[r]);
+        base += total;
+        uint32_t zero = ltm[r];
+        for (uint32_t e = eqm[r]; e; e &= e - 1) {  // ties (few): the first r_keep in row-major order
+            if (rank < r_keep) zero |= e & (0u - e);
             ++rank;
         }
+        const int64_t i0 = (int64_t)blockIdx.x * kEqBlock2 + r * kEqBlock + threadIdx.x * 16;
+        if (vec && i0 + 16 <= n) {
+            uint32_t o[4];
+            memcpy(o, v[r], 16);
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-        if ((zero >> k) & 1) v[k] = 0;
-    if (vec && i0 + 16 <= n) {
-        uint4 o;
-        memcpy(&o, v, 16);
-        *reinterpret_cast<uint4*>(out + i0) = o;
-    } else {
-        for (int k = 0; k < 16; ++k)
-            if (i0 + k < n) out[i0 + k] = v[k];
+            for (int k = 0; k < 4; ++k)  // 4 zero bits -> 4 byte masks
+                o[k] &= ~((((zero >> (4 * k)) & 15u) * 0x00204081u & 0x01010101u) * 0xFFu);
+            *reinterpret_cast<uint4*>(out + i0) = make_uint4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if ((zero >> k) & 1) v[r][k] = 0;
+            for (int k = 0; k < 16; ++k)
+                if (i0 + k < n) out[i0 + k] = v[r][k];
+        }
     }
 }
 
@@ -726,11 +756,12 @@ extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, 
     DC_CHECK_LAUNCH("k_col_bounds");
     const bool vec = cols % 16 == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
                      (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    k_eq_count2<<<(unsigned)nblk, kPrThreads, 0, st>>>(q, lo, hi, n, cols, vec, blk);
+    const int64_t nblk2 = (n + kEqBlock2 - 1) / kEqBlock2;  // <= nblk: fits the scratch
+    k_eq_count2<<<(unsigned)nblk2, kPrThreads, 0, st>>>(q, lo, hi, n, cols, vec, blk);
     DC_CHECK_LAUNCH("k_eq_count2");
-    k_excl_scan<<<1, 1024, 0, st>>>(blk, nblk);
+    k_excl_scan<<<1, 1024, 0, st>>>(blk, nblk2);
     DC_CHECK_LAUNCH("k_excl_scan");
-    k_apply2<<<(unsigned)nblk, kPrThreads, 0, st>>>(q, lo, hi, n, cols, vec, sel, blk, out);
+    k_apply2<<<(unsigned)nblk2, kPrThreads, 0, st>>>(q, lo, hi, n, cols, vec, sel, blk, out);
     DC_CHECK_LAUNCH("k_apply2");
     return DC_OK;
 }
