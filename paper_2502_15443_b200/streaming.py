@@ -242,8 +242,22 @@ class StreamedFusedFile(StreamedFused):
         self.pool = ThreadPoolExecutor(max_workers=threads)
 
     def close(self) -> None:
-        self.pool.shutdown()
-        os.close(self.fd)
+        if getattr(self, "fd", None) is not None:
+            self.pool.shutdown()
+            os.close(self.fd)
+            self.fd = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def _read(self, g: int) -> int:
         slot, f0, f1, _ = self.groups[g]
@@ -293,8 +307,22 @@ class StreamedRawFile:
         self.bytes_per_step = nbytes
 
     def close(self) -> None:
-        self.pool.shutdown()
-        os.close(self.fd)
+        if getattr(self, "fd", None) is not None:
+            self.pool.shutdown()
+            os.close(self.fd)
+            self.fd = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def _read(self, g: int) -> int:
         slot = g % self.slots
