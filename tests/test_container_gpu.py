@@ -300,3 +300,23 @@ def test_index_less_unpack_records_index_for_next_call(cuda):
     with pytest.raises((cuda.CorruptStreamError, cuda.ChecksumError)):
         container.unpack(bytes(bad))
     container.clear_index_cache()
+
+
+@pytest.mark.parametrize("chunk", [4096, 5000, 12345, 65537, 100003, 300001])
+def test_odd_chunk_sizes_split_point_exact(cuda, oracle, chunk):
+    """Chunk sizes that are not multiples of the 256-symbol segment (ragged last
+    segments everywhere), every decoder mode: file bytes equal the oracle's pack,
+    the sidecar-driven decode equals the tensors."""
+    from paper_2502_15443_b200 import container
+    rng = np.random.default_rng(chunk)
+    ts, st, ents = [], {}, []
+    for i, (r, c) in enumerate([(333, 700), (129, 1001)]):
+        q = np.clip(np.round(rng.normal(0, 11, (r, c))), -127, 127).astype(np.int8)
+        ts.append(cuda.QuantizedTensor(f"t{i}", q, 0.02, cuda.ScaleVector.identity(c)))
+        st[f"t{i}"] = cuda.ActivationStats(f"t{i}", np.ones(c))
+        ents.append((f"t{i}", q, 0.02, 0.0, np.ones(c), np.ones(c)))
+    data, index = container.pack_indexed(ts, st, chunk_size=chunk, seg_shift=8)
+    assert data == oracle.pack(ents, chunk)
+    out = container.unpack(data, index=index.to_bytes(container.binding_of(data)))
+    for x, t in zip(out.tensors, ts):
+        assert np.array_equal(x.qvalues, t.qvalues)
