@@ -105,3 +105,35 @@ def test_singleton_symbols_f1_bit_exact(cuda, oracle):
         table = cuda.AnsTable.from_bytes(blob[:384])
         assert (table.frequencies == 1).sum() >= 1
         assert cuda.decompress_blob(blob, n) == data.tobytes()
+
+
+def _shannon_bits(d):
+    p = np.bincount(d, minlength=256).astype(np.float64) / d.size
+    p = p[p > 0]
+    return float(-(p * np.log2(p)).sum())
+
+
+def test_entropy_window_and_distributions(cuda, oracle):
+    """The reference's size bounds (test_ans.py TestSizeBounds, test_acceptance.py
+    codec optimality): every GPU blob within [0.99 H - 16, 1.03 H + 400] bytes of
+    the Shannon bound, and byte-identical to the oracle, on ten distributions."""
+    rng = np.random.default_rng(2024)
+    n = 100_000
+    streams = {
+        "uniform256": rng.integers(0, 256, n, dtype=np.uint8),
+        "uniform16": rng.integers(0, 16, n).astype(np.uint8),
+        "uniform2": rng.integers(0, 2, n).astype(np.uint8),
+        "constant": np.full(n, 7, dtype=np.uint8),
+        "bernoulli": rng.choice([0, 1], n, p=[0.97, 0.03]).astype(np.uint8),
+        "geometric": np.minimum(rng.geometric(0.2, n) - 1, 255).astype(np.uint8),
+        "zipf": np.minimum(rng.zipf(1.4, n) - 1, 255).astype(np.uint8),
+        "binomial": rng.binomial(255, 0.5, n).astype(np.uint8),
+        "poisson": np.minimum(rng.poisson(30, n), 255).astype(np.uint8),
+        "gauss_int8": np.clip(np.rint(rng.normal(0, 9, n)), -127, 127).astype(np.int8).view(np.uint8),
+    }
+    for name, data in streams.items():
+        ideal = n * _shannon_bits(data) / 8
+        blob = cuda.compress_blob(data)
+        assert 0.99 * ideal - 16 <= len(blob) <= 1.03 * ideal + 400, name
+        assert blob == oracle.compress_blob(data), name
+        assert cuda.decompress_blob(blob, n) == data.tobytes(), name
