@@ -355,6 +355,7 @@ def measure_disk(model_payload: torch.Tensor, shapes, offs, image: torch.Tensor,
     from .adaptive import time_ms
     dev = model_payload.device
     workdir = workdir or tempfile.gettempdir()
+    os.makedirs(workdir, exist_ok=True)
     raw_path = os.path.join(workdir, "dcomp_disk_raw.bin")
     img_path = os.path.join(workdir, "dcomp_disk_img.dcc")
     model_payload.cpu().numpy().tofile(raw_path)
