@@ -31,48 +31,6 @@ ALPHA_GRID = tuple(round(0.1 * i, 1) for i in range(11))
 _DTYPE_CODE = {torch.float64: 0, torch.float32: 1, torch.bfloat16: 2, torch.float16: 3}
 
 
-@dataclasses.dataclass(frozen=True)
-class ScaleVector:
-    alpha: float
-    s: np.ndarray  # (cols,) float64, > 0
-
-    def __post_init__(self):
-        s = np.asarray(self.s, dtype=np.float64)
-        if (s <= 0).any() or not np.isfinite(s).all():
-            raise ValueError("scale factors must be positive and finite")
-        object.__setattr__(self, "s", s)
-
-    @classmethod
-    def identity(cls, cols: int) -> "ScaleVector":
-        return cls(0.0, np.ones(cols))
-
-
-@dataclasses.dataclass(frozen=True)
-class QuantizedTensor:
-    name: str
-    qvalues: np.ndarray  # (rows, cols) int8 in [-127, 127]
-    w_scale: float
-    scale_vec: ScaleVector
-
-    def __post_init__(self):
-        q = np.asarray(self.qvalues, dtype=np.int8)
-        if q.ndim != 2:
-            raise ValueError(f"{self.name}: expected 2-D qvalues")
-        object.__setattr__(self, "qvalues", q)
-        if self.w_scale <= 0:
-            raise ValueError(f"{self.name}: w_scale must be positive")
-        if len(self.scale_vec.s) != q.shape[1]:
-            raise ValueError(f"{self.name}: scale_vec length != cols")
-
-    @property
-    def rows(self) -> int:
-        return self.qvalues.shape[0]
-
-    @property
-    def cols(self) -> int:
-        return self.qvalues.shape[1]
-
-
 def compute_scale(stats: ActivationStats, alpha: float) -> ScaleVector:
     """s_i = max(channel_max_i, 1e-8) ** alpha; alpha = 0 is the identity."""
     if not 0.0 <= alpha <= 1.0:
@@ -168,13 +126,6 @@ def dequantize(q: QuantizedTensor) -> WeightTensor:
     return WeightTensor(q.name, out.cpu().numpy())
 
 
-@dataclasses.dataclass(frozen=True)
-class LayerErrorReport:
-    alpha: float
-    fp_identity_error: float  # (X/s)(sW) vs XW, no quantization
-    quantized_error: float    # full INT8 path vs the f64 reference
-
-
 def simulate_layer(x: np.ndarray, w: WeightTensor, stats: ActivationStats, alpha: float) -> LayerErrorReport:
     """Relative Frobenius errors of the scaled W8A8 path on one layer.
 
@@ -203,3 +154,49 @@ def simulate_layer(x: np.ndarray, w: WeightTensor, stats: ActivationStats, alpha
     y_hat = acc.to(torch.float64) * (sx * sw)
     q_err = float(torch.linalg.norm(y_hat - y_ref)) / ref_norm
     return LayerErrorReport(alpha=alpha, fp_identity_error=fp_err, quantized_error=q_err)
+
+
+# ---- value types of the API (defined after the functions; annotations are strings)
+
+@dataclasses.dataclass(frozen=True)
+class ScaleVector:
+    alpha: float
+    s: np.ndarray  # (cols,) float64, > 0
+
+    def __post_init__(self):
+        s = np.asarray(self.s, dtype=np.float64)
+        if (s <= 0).any() or not np.isfinite(s).all():
+            raise ValueError("scale factors must be positive and finite")
+        object.__setattr__(self, "s", s)
+
+    @classmethod
+    def identity(cls, cols: int) -> "ScaleVector":
+        return cls(0.0, np.ones(cols))
+
+
+@dataclasses.dataclass(frozen=True)
+class QuantizedTensor:
+    name: str
+    qvalues: np.ndarray  # (rows, cols) int8 in [-127, 127]
+    w_scale: float
+    scale_vec: ScaleVector
+
+    def __post_init__(self):
+        q = np.asarray(self.qvalues, dtype=np.int8)
+        if q.ndim != 2:
+            raise ValueError(f"{self.name}: expected 2-D qvalues")
+        object.__setattr__(self, "qvalues", q)
+        if self.w_scale <= 0:
+            raise ValueError(f"{self.name}: w_scale must be positive")
+        if len(self.scale_vec.s) != q.shape[1]:
+            raise ValueError(f"{self.name}: scale_vec length != cols")
+
+    rows = property(lambda self: self.qvalues.shape[0])
+    cols = property(lambda self: self.qvalues.shape[1])
+
+
+@dataclasses.dataclass(frozen=True)
+class LayerErrorReport:
+    alpha: float
+    fp_identity_error: float  # (X/s)(sW) vs XW, no quantization
+    quantized_error: float    # full INT8 path vs the f64 reference
