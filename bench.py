@@ -223,7 +223,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": f"{args.model}-shaped W8A8 fully compressed (alpha {args.alpha}), DCC1 unpack "
                                f"(decode + CRC verify + tensor slicing) of the whole container on host cores",
-                   "model": args.model, "chunk_size": chunk, "n_chunks": n_chunks, "raw_bytes": raw,
+                   "weights_shape": args.model, "chunk_size": chunk, "n_chunks": n_chunks, "raw_bytes": raw,
                    "file_bytes": len(data), "cr": raw / len(data)},
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": f"{raw / 1e6:.1f} MB decompressed per step ({n_layers} layers, one layer's "
@@ -497,7 +497,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"{args.model}-shaped W8A8 fully compressed (alpha {args.alpha}), decompress all "
-                                   f"chunks of the resident DCC1 container", "model": args.model,
+                                   f"chunks of the resident DCC1 container", "weights_shape": args.model,
                        "chunk_size": args.chunk_size, "seg_len": 1 << args.seg_shift, "n_chunks": int(pm.jobs.n),
                        "raw_bytes": raw, "file_bytes": pm.file_bytes, "cr": cr_file,
                        "cr_resident": raw / (pm.file_bytes + pm.index.nbytes), "index_bytes": pm.index.nbytes,
