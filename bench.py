@@ -1,25 +1,32 @@
 #!/usr/bin/env python
 """Benchmark driver (contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1]): OPT-1.3B-shaped W8A8 weights, random
-init on the GPU, compression-aware quantized (alpha 0.5), packed FULLY
-compressed into DCC1 at the reference's default 16 MiB chunks by the GPU
-encoder.  One step = decompress every chunk of the resident container to
-its int8 weights (split-point parallel rANS decode + raw copy of stored
-chunks), i.e. the work a compressed-weight inference pass repeats.
+Workload: the north star's target configuration (BASELINE.json north_star,
+config C4's shape): OPT-6.7B-shaped W8A8 weights from a deterministic
+integer-hash generator (~N(0, 0.2); channel maxima as SynthSpec),
+compression-aware quantized (alpha 0.5) and packed FULLY compressed into
+DCC1 at the reference's default 16 MiB chunks by the GPU encoder.  One step
+= the reference's unpack work on the container resident in HBM: validate
+every chunk, split-point parallel rANS decode, raw copy of stored chunks,
+CRC32 of every decoded chunk checked against the chunk table
+(container.py:296-331).
 
-  value     decompressed GB/s with the container resident in HBM
+  value     decompressed GB/s of that step (container resident in HBM)
   e2e       same metric through the public API ``container.unpack`` from
-            HOST bytes (H2D copy, decode, CRC verification, D2H weights)
+            pinned HOST bytes (H2D, decode, CRC verify, D2H of every weight);
+            ``e2e.index_less`` = the reference's exact call (no sidecar)
   roofline  dominant kernel (k_decode_segments): algorithmic bytes
             N * (1 + 1/CR) per launch / its CUDA-event time vs measured HBM
+  decode_step_tokens  fused decode -> tcgen05 W8A8 vs INT8 at B = 1, 16
+  extra     the same measurements on OPT-1.3B (config C2)
   cpu_baseline  the C oracle (a restatement of the reference's numba
             kernels) decoding a bounded sample on this box's host cores
 
-``--impl reference`` times the CPU reference path (the oracle port, all host
-threads) on the same metric; under torchrun only rank 0 runs it.
-Multi-GPU: one process per GPU, each decodes its own model copy (weak
-scaling, no collective on the data path); time = max over ranks.
+``--impl reference`` times the reference's unpack (the oracle port, all host
+threads) on whole-layer samples of the SAME container (identical bytes; both
+lines carry the digest of its header + chunk table); under torchrun only
+rank 0 runs it.  Multi-GPU: one process per GPU, each decodes its own copy
+(weak scaling, no collective on the data path); time = max over ranks.
 """
 
 from __future__ import annotations
@@ -33,6 +40,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -45,7 +54,9 @@ def parse_args():
     p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--model", default="opt-1.3b")
+    p.add_argument("--model", default="opt-6.7b")
+    p.add_argument("--extra-model", default="opt-1.3b", help="second workload reported as an extra key ('none')")
+    p.add_argument("--seed", type=int, default=1234)
     p.add_argument("--chunk-size", type=int, default=16 * 2**20)
     p.add_argument("--alpha", type=float, default=0.5)
     p.add_argument("--seg-shift", type=int, default=8)
@@ -177,60 +188,246 @@ def cpu_sample_decode(image_bytes: bytes, entries, budget_s: float, threads: int
     return nbytes * reps / dt / 1e9, f"{len(sample)} ANS chunks x {reps} reps ({nbytes / 1e6:.1f} MB each rep)", threads
 
 
+def synth_spec(model: str, seed: int, layers: int | None = None):
+    """The bench workload, shared by both arms: (name, rows, cols) per linear
+    (exporter order), a uint32 hash key per tensor for the integer-hash
+    weights (synth.hash_weights on the GPU arm, oracle or_gen_weights on the
+    reference arm: the same f64 values) and host-drawn channel maxima
+    (log-normal(-1, 1), 2 % outlier channels x20, as SynthSpec)."""
+    import numpy as np
+    from paper_2502_15443_b200.tensors import model_layout  # the shape table only
+    layout = model_layout(model)
+    if layers is not None:
+        per = sum(1 for n, _, _ in layout if n.startswith("layers.0."))
+        layout = layout[: per * layers]
+    keys, cms = [], []
+    for i, (_, _, c) in enumerate(layout):
+        keys.append((seed * 0x9E3779B1 + i * 0x7F4A7C15 + 0x632BE5AB) & 0xFFFFFFFF)
+        rng = np.random.default_rng([seed, i])
+        cm = rng.lognormal(-1.0, 1.0, c)
+        k = int(round(0.02 * c))
+        if k:
+            cm[rng.choice(c, k, replace=False)] *= 20.0
+        cms.append(cm)
+    return layout, keys, cms
+
+
+def container_digest(head: bytes) -> str:
+    """sha256 of a DCC1 file's header + chunk table (every chunk's codec,
+    offsets, lengths and CRC32 of its decompressed bytes): equal digests =
+    the same container bytes in both arms."""
+    import hashlib
+    import struct
+    (hlen,) = struct.unpack_from("<I", head, 6)
+    (count,) = struct.unpack_from("<I", head, 10 + hlen)
+    return hashlib.sha256(bytes(head[:14 + hlen + 4 + 29 * count])).hexdigest()[:32]
+
+
+REF_SAMPLE_BYTES = 1 << 30  # bytes of weights one reference-arm step unpacks (whole layers)
+
+
 def run_reference(args):
-    """--impl reference: the reference algorithm on host cores (C oracle port,
-    all threads), on a bounded sample of the same workload."""
+    """--impl reference: the reference's unpack algorithm on host cores (the
+    oracle/ C port of its numba kernels + zlib CRC + tensor slicing, all host
+    threads), on the SAME container our arm decodes (identical bytes: the
+    digest of header + chunk table is printed), each step one bounded
+    sample: a DCC1 container of whole consecutive layers (~1 GiB of weights)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle import oracle as O
     O.lib()
-    sys.path.insert(0, ROOT)
-    from paper_2502_15443_b200.tensors import SynthSpec, model_layout, synth_ensemble
     threads = os.cpu_count() or 1
-    # one transformer layer of the model shape, tiled over every layer of the
-    # model: the same chunk count / container size as our arm (the reference's
-    # unpack hands chunks to threads in fours, so a small sample would leave
-    # host cores idle)
-    full = model_layout(args.model)
-    layer = full[:6]
-    made = []
-    for i, (name, r, c) in enumerate(layer):
-        w, st = synth_ensemble(SynthSpec(rows=r, cols=c, name=name), 1000 + i)
-        s = O.compute_scale(st.channel_max, args.alpha)
-        q, ws = O.quantize(w.values, s)
-        made.append((q, ws, s, st.channel_max))
-    n_layers = len(full) // len(layer) if args.layers is None else args.layers
-    entries = [(f"layers.{L}.{name.split('.')[-1]}", q, ws, args.alpha, s, cm)
-               for L in range(n_layers) for (name, _, _), (q, ws, s, cm) in zip(layer, made)]
+    t0 = time.perf_counter()
+    layout, keys, cms = synth_spec(args.model, args.seed, args.layers)
+
+    def make(i):
+        name, r, c = layout[i]
+        s = O.compute_scale(cms[i], args.alpha)
+        q, ws = O.gen_quantize(keys[i], r, c, s)
+        return (name, q, ws, args.alpha, s, cms[i])
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        entries = list(ex.map(make, range(len(layout))))
     chunk = args.chunk_size
     data = O.pack(entries, chunk, threads=threads)
-    raw = sum(e[1].size for e in entries)
-    n_chunks = -(-raw // chunk)
+    digest = container_digest(data)
+    raw_total = sum(e[1].size for e in entries)
+    file_total = len(data)
+    del data
+    # the sample: whole layers from the front, about REF_SAMPLE_BYTES of weights
+    per = sum(1 for n, _, _ in layout if n.startswith("layers.0.")) or len(layout)
+    layer_bytes = sum(r * c for _, r, c in layout[:per])
+    n_layers = max(1, min(len(layout) // per, REF_SAMPLE_BYTES // max(layer_bytes, 1)))
+    sample = O.pack(entries[: per * n_layers], chunk, threads=threads)
+    raw = sum(e[1].size for e in entries[: per * n_layers])
+    del entries
+    t_build = time.perf_counter() - t0
     for _ in range(args.warmup):
-        O.unpack(data, threads=threads)
+        O.unpack(sample, threads=threads)
     times = []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.unpack(data, threads=threads)
-        times.append(time.perf_counter() - t0)
+        t1 = time.perf_counter()
+        O.unpack(sample, threads=threads)
+        times.append(time.perf_counter() - t1)
     dt = sum(times)
     v = raw * args.steps / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{args.model}-shaped W8A8 fully compressed (alpha {args.alpha}), DCC1 unpack "
-                               f"(decode + CRC verify + tensor slicing) of the whole container on host cores",
-                   "weights_shape": args.model, "chunk_size": chunk, "n_chunks": n_chunks, "raw_bytes": raw,
-                   "file_bytes": len(data), "cr": raw / len(data)},
+        "config": workload_config(args, raw_total, file_total, digest),
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{raw / 1e6:.1f} MB decompressed per step ({n_layers} layers, one layer's "
-                                   f"synthetic weights tiled), oracle/ C port of the reference's numba decode"},
+                         "sample": f"unpack (decode on {threads} threads in the reference's groups of four "
+                                   f"chunks + serial zlib CRC of every chunk + tensor slicing) of a DCC1 "
+                                   f"container of layers 0-{n_layers - 1} ({raw / 1e6:.0f} MB of weights, "
+                                   f"{-(-raw // chunk)} chunks) per step, cut from the same weights "
+                                   f"as the full container (digest {digest})"},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "build_s": t_build,
     }
     print(json.dumps(line), flush=True)
+
+
+def workload_config(args, raw: int, file_bytes: int, digest: str) -> dict:
+    return {"workload": f"{args.model}-shaped W8A8 weights (hash-generated ~N(0, 0.2), SynthSpec channel maxima, "
+                        f"compression-aware quantized at alpha {args.alpha}), fully compressed DCC1 at "
+                        f"{args.chunk_size >> 20} MiB chunks; one step = unpack the container (validate + rANS "
+                        f"decode + CRC32 verify of every chunk)",
+            "weights_shape": args.model, "chunk_size": args.chunk_size, "raw_bytes": raw, "file_bytes": file_bytes,
+            "cr": raw / file_bytes, "container_digest": digest, "seed": args.seed}
+
+
+class DeviceUnpack:
+    """One bench step: the reference's unpack work on a container resident in
+    HBM (container.py:296-331) -- prologue validation, split-point rANS decode
+    of every ANS chunk, raw copy of stored chunks, CRC32 of every decoded chunk
+    compared with the chunk table -- with no host synchronisation (verdicts
+    accumulate on the device and are checked after the timed region)."""
+
+    def __init__(self, pm, dev):
+        import torch
+        from paper_2502_15443_b200 import native as nv
+        self.pm, self.nv = pm, nv
+        self.out = nv.device_bytes(pm.raw_bytes, dev)
+        self.status = torch.zeros(max(pm.jobs.n, 1), dtype=torch.int32, device=dev)
+        self.crc = torch.zeros(max(pm.jobs.n, 1), dtype=torch.int32, device=dev)
+        self.want = torch.from_numpy(pm.entries["crc32"].astype(np.uint32).view(np.int32).copy()).to(dev)
+        self.bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.has_store = bool((pm.entries["codec"] == 0).any())
+        self.max_len = int(pm.jobs.out_len.max())
+        self.events = []
+        self.launches = 4 + int(self.has_store)  # validate, decode, [store], crc pieces + finalize
+
+    def __call__(self, record: bool = False):
+        import torch
+        from paper_2502_15443_b200 import engine
+        pm, j, nv = self.pm, self.pm.jobs, self.nv
+        sp = nv.stream_ptr()
+        engine.validate(pm.image, j, self.status)
+        if record:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+        engine.decode_segments(pm.image, j, pm.index, pm.tasks, self.out, self.status)
+        if record:
+            ev[1].record()
+            self.events.append(ev)
+        if self.has_store:
+            engine.store_copy(pm.image, j, self.out)
+        nv.call("dc_crc32_ranges", self.out.data_ptr(), self.out.numel(), j.d_out_off.data_ptr(), j.d_out_len.data_ptr(), j.n,
+                self.max_len, self.crc.data_ptr(), sp)
+        self.bad |= (self.crc[: j.n] != self.want).any().to(torch.int32) | (self.status[: j.n] != 0).any().to(
+            torch.int32)
+
+    def kernel_ms(self) -> float:
+        return sum(a.elapsed_time(b) for a, b in self.events) / max(len(self.events), 1)
+
+
+def time_steps(fn, steps: int, world: int, dev):
+    """K steps between barriers + device syncs; CUDA-event time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    return float(ms.item())
+
+
+def time_ms(fn, iters):
+    import torch
+    for _ in range(2):
+        fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def build_packed(args, model: str, dev):
+    import torch
+    from paper_2502_15443_b200 import synth
+    t0 = time.perf_counter()
+    layout, keys, cms = synth_spec(model, args.seed, args.layers)
+    m = synth.build_hash_model(model, layout, keys, cms, alpha=args.alpha, device=dev)
+    pm = synth.pack_model(m, args.chunk_size, seg_shift=args.seg_shift)
+    torch.cuda.synchronize()
+    head = pm.image[:14].cpu().numpy().tobytes()
+    hlen = int.from_bytes(head[6:10], "little")
+    digest = container_digest(pm.image[:14 + hlen + 4 + 29 * pm.jobs.n].cpu().numpy().tobytes())
+    return m, pm, digest, time.perf_counter() - t0
+
+
+def decode_step_tokens(m, pm, out, dev, iters, batches=(1, 16), unfused_step=None):
+    """Decode-step tokens/s: every linear of the model once for B tokens --
+    INT8 weights vs fused compressed (decode -> TMEM -> tcgen05) [vs decode
+    to HBM then INT8 GEMM].  Exactness is checked before timing."""
+    import torch
+    from paper_2502_15443_b200.gemm import FusedRing, GroupedInt8
+    offs = m.offsets()[:-1]
+    raw = m.nbytes
+    w_int8 = [m.payload[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, m.shapes)]
+    w_dec = [out[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, m.shapes)]
+    tokens = {}
+    for B in batches:
+        gx = torch.Generator(device=dev)
+        gx.manual_seed(7 + B)
+        xs = [torch.randint(-127, 128, (B, c), generator=gx, device=dev, dtype=torch.int8) for _, c in m.shapes]
+        gi = GroupedInt8(w_int8, xs, B)
+        fc = FusedRing(pm.image, pm.jobs, pm.index, pm.chunk_size, m.shapes, offs, xs, B)
+        gi.run()
+        fc.run()
+        torch.cuda.synchronize()
+        if (fc.check() != 0).any() or not all(torch.equal(a, b) for a, b in zip(gi.accs, fc.accs)):
+            raise SystemExit("fused decode-GEMM mismatch vs INT8 GEMM")
+        t_i8 = time_ms(gi.run, iters)
+        t_fu = time_ms(fc.run, iters)
+        row = {"int8_tok_s": B / (t_i8 / 1e3), "compressed_fused_tok_s": B / (t_fu / 1e3), "int8_ms": t_i8,
+               "fused_ms": t_fu, "fused_vs_int8": t_i8 / t_fu, "int8_weight_gbs": raw / (t_i8 / 1e3) / 1e9}
+        if unfused_step is not None:
+            gd = GroupedInt8(w_dec, xs, B)
+            t_un = time_ms(lambda: (unfused_step(), gd.run()), iters)
+            row.update({"compressed_unfused_tok_s": B / (t_un / 1e3), "unfused_ms": t_un})
+            del gd
+        tokens[f"B{B}"] = row
+        del gi, fc
+    return tokens
 
 
 def main():
@@ -238,7 +435,6 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -250,62 +446,30 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    from paper_2502_15443_b200 import container, engine, native, synth
+    from paper_2502_15443_b200 import container, engine, native
     native.require_cuda()
 
-    t_build = time.perf_counter()
-    m = synth.build_model(args.model, alpha=args.alpha, seed=1234 + rank, device=dev, layers=args.layers)
-    pm = synth.pack_model(m, args.chunk_size, seg_shift=args.seg_shift)
-    torch.cuda.synchronize()
-    t_build = time.perf_counter() - t_build
+    m, pm, digest, t_build = build_packed(args, args.model, dev)
     raw = pm.raw_bytes
     comp = pm.comp_bytes
     cr_file = raw / pm.file_bytes
-    out = native.device_bytes(raw, dev)
-    status = torch.zeros(pm.jobs.n, dtype=torch.int32, device=dev)
-    has_store = bool((pm.entries["codec"] == 0).any())
-
-    kernel_events = []  # (start, end) around the decode launch of every timed step
-
-    def step(record: bool = False):
-        if record:
-            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            ev[0].record()
-        engine.decode_segments(pm.image, pm.jobs, pm.index, pm.tasks, out, status)
-        if record:
-            ev[1].record()
-            kernel_events.append(ev)
-        if has_store:
-            engine.store_copy(pm.image, pm.jobs, out)
+    unp = DeviceUnpack(pm, dev)
+    out = unp.out
 
     clocks = ClockSampler(local).__enter__()
     time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
     for _ in range(args.warmup):
-        step()
+        unp()
     torch.cuda.synchronize()
-    if int(status.abs().sum().item()) != 0 or not torch.equal(out, m.payload):
-        raise SystemExit("decode mismatch: GPU output != encoder input")
-
+    if int(unp.bad.item()) != 0 or not torch.equal(out, m.payload):
+        raise SystemExit("unpack mismatch: status / CRC verdicts or GPU output != encoder input")
     # the timed region; the dominant kernel's own duration is taken from events
     # around its launch inside every timed step (same stream)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record()
-    for _ in range(args.steps):
-        step(record=True)
-    end.record()
-    torch.cuda.synchronize()
+    ms = time_steps(lambda: unp(record=True), args.steps, world, dev)
     clocks.__exit__(None, None, None)
-    if world > 1:
-        dist.barrier()
-    ms = start.elapsed_time(end)
-    kms = sum(a.elapsed_time(b) for a, b in kernel_events) / len(kernel_events)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    if int(unp.bad.item()) != 0:
+        raise SystemExit("unpack verdicts changed inside the timed region")
+    kms = unp.kernel_ms()
     value = raw * world * args.steps / (ms / 1e3) / 1e9
     hbm, peak_kind = peaks()
     ans_raw = int(pm.entries["uncomp_len"][pm.entries["codec"] == 1].sum())
@@ -313,48 +477,13 @@ def main():
     alg_bytes = ans_raw + ans_comp  # decompressed bytes written + compressed bytes read
     achieved = alg_bytes / (kms / 1e3) / 1e9
 
-    # decode-step tokens/s: every linear of the model once for B tokens,
-    # INT8 weights vs fused compressed (decode -> TMEM -> tcgen05) vs
-    # decode-to-HBM then INT8 GEMM.  Exactness is checked before timing.
-    from paper_2502_15443_b200.gemm import FusedRing, GroupedInt8
+    def decode_only():
+        engine.decode_segments(pm.image, pm.jobs, pm.index, pm.tasks, out, unp.status)
+        if unp.has_store:
+            engine.store_copy(pm.image, pm.jobs, out)
+
+    tokens = decode_step_tokens(m, pm, out, dev, max(5, min(args.steps // 5, 20)), unfused_step=decode_only)
     offs = m.offsets()[:-1]
-    w_int8 = [m.payload[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, m.shapes)]
-    w_dec = [out[o:o + r * c].view(torch.int8).view(r, c) for o, (r, c) in zip(offs, m.shapes)]
-
-    def time_ms(fn, iters):
-        for _ in range(2):
-            fn()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(iters):
-            fn()
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / iters
-
-    tokens = {}
-    for B in (1, 16):
-        gx = torch.Generator(device=dev)
-        gx.manual_seed(7 + B)
-        xs = [torch.randint(-127, 128, (B, c), generator=gx, device=dev, dtype=torch.int8) for _, c in m.shapes]
-        gi = GroupedInt8(w_int8, xs, B)
-        gd = GroupedInt8(w_dec, xs, B)
-        fc = FusedRing(pm.image, pm.jobs, pm.index, pm.chunk_size, m.shapes, offs, xs, B)
-        gi.run()
-        fc.run()
-        torch.cuda.synchronize()
-        if (fc.check() != 0).any() or not all(torch.equal(a, b) for a, b in zip(gi.accs, fc.accs)):
-            raise SystemExit("fused decode-GEMM mismatch vs INT8 GEMM")
-        iters = max(5, args.steps // 5)
-        t_i8 = time_ms(gi.run, iters)
-        t_fu = time_ms(fc.run, iters)
-        t_un = time_ms(lambda: (step(), gd.run()), iters)
-        tokens[f"B{B}"] = {"int8_tok_s": B / (t_i8 / 1e3), "compressed_fused_tok_s": B / (t_fu / 1e3),
-                           "compressed_unfused_tok_s": B / (t_un / 1e3), "int8_ms": t_i8, "fused_ms": t_fu,
-                           "unfused_ms": t_un, "fused_vs_int8": t_i8 / t_fu,
-                           "int8_weight_gbs": raw / (t_i8 / 1e3) / 1e9}
-        del gi, gd, fc
 
     # GPU_CPU tier: weights in pinned host memory streamed over
     # PCIe every step, raw INT8 vs the compressed container + on-GPU decode,
@@ -369,7 +498,7 @@ def main():
         streaming_tier = streaming.measure(m.payload, m.shapes, offs, pm.image, pm.jobs, pm.index, ntok=1,
                                            iters=5, groups=16)
         h2d = adaptive.measure_h2d_gbs(1 << 28)
-        prof = latency.HardwareProfile(B_stoc=7.0, B_ctog=h2d, B_gpu=hbm, D_max=value, c_sat=1.0,
+        prof = latency.HardwareProfile(B_stoc=7.0, B_ctog=h2d, B_gpu=hbm, D_max=raw / (kms / 1e3) / 1e9, c_sat=1.0,
                                        I_gpu=tokens["B1"]["int8_weight_gbs"], mem_gpu=1e12, mem_cpu=1e12)
         n_ch = int(pm.jobs.n)
         arch = latency.Architecture.GPU_CPU
@@ -382,24 +511,21 @@ def main():
     except Exception as e:  # report, never hide
         streaming_tier = {"skipped" if world > 1 else "error": repr(e)[:300]}
 
-    def adaptive_h2d():
-        from paper_2502_15443_b200 import adaptive
-        return adaptive.measure_h2d_gbs(1 << 28)
-
     # GPU_DISK tier (B_stoc): raw INT8 file vs DCC1 file read from disk every
     # step (O_DIRECT), fused decode -> GEMM vs INT8 GEMM; N=1 only
     disk_tier = None
     if world == 1 and not args.no_disk:
         try:
-            from paper_2502_15443_b200 import streaming
+            import importlib
+            from paper_2502_15443_b200 import adaptive, streaming
             disk_tier = streaming.measure_disk(m.payload, m.shapes, offs, pm.image, pm.jobs, pm.index, ntok=1,
                                                iters=3, workdir=os.path.join(ROOT, "gpurun_out"))
             # the reference's latency model for its STORAGE architecture, B_stoc =
             # the measured raw read rate of this disk
-            import importlib
             latency = importlib.import_module("paper_2502_15443_b200.latency")
             stoc = disk_tier["raw_read_gbs"]
-            dprof = latency.HardwareProfile(B_stoc=stoc, B_ctog=adaptive_h2d(), B_gpu=hbm, D_max=value, c_sat=1.0,
+            dprof = latency.HardwareProfile(B_stoc=stoc, B_ctog=adaptive.measure_h2d_gbs(1 << 28), B_gpu=hbm,
+                                            D_max=raw / (kms / 1e3) / 1e9, c_sat=1.0,
                                             I_gpu=tokens["B1"]["int8_weight_gbs"], mem_gpu=1e12, mem_cpu=1e12)
             n_ch = int(pm.jobs.n)
             arch = latency.Architecture.STORAGE
@@ -466,57 +592,96 @@ def main():
         raise SystemExit("e2e mismatch")
     e2e_s = statistics.median(e2e_times)
     e2e = {"value": raw / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": len(host_file) + len(side),
-           "d2h_bytes_per_step": raw + 8 * pm.jobs.n, "api": "container.unpack(pinned host file, index=pinned sidecar) -> host ModelBundle",
+           "d2h_bytes_per_step": raw + 8 * pm.jobs.n,
+           "api": "container.unpack(pinned host file, index=pinned sidecar) -> host ModelBundle",
            "phases_ms": {k: statistics.median(p[k] for p in e2e_phases) for k in e2e_phases[0]}}
+    del bundle
     # the reference's exact call, unpack(file) with no sidecar: every chunk is one
     # serial rANS chain on the GPU (no split points exist yet); one timed step
     if not args.no_index_less:
+        container.clear_index_cache()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         b2 = container.unpack(pin_file)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        same = b2.tensors[-1].qvalues.tobytes() == bundle.tensors[-1].qvalues.tobytes()
-        e2e["index_less"] = {"value": raw / dt / 1e9, "unit": "GB/s", "api": "container.unpack(pinned host file)",
-                             "seconds": dt, "equal": same}
+        same = b2.tensors[-1].qvalues.tobytes() == m.payload[-m.shapes[-1][0] * m.shapes[-1][1]:].cpu().numpy().tobytes()
+        e2e["index_less"] = {"value": raw / dt / 1e9, "unit": "GB/s",
+                             "api": "container.unpack(pinned host file) -- no sidecar, first call", "seconds": dt,
+                             "equal": same}
         del b2
+        container.clear_index_cache()
 
     cpu = None
     if rank == 0 and not args.no_cpu:
         try:
             v, sample, cores = cpu_sample_decode(host_file, pm.entries, args.cpu_seconds, os.cpu_count() or 1)
-            cpu = {"value": v, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample}
+            cpu = {"value": v, "unit": "GB/s", "cores": cores, "kind": "port",
+                   "sample": "decode only (no CRC): " + sample}
         except Exception as e:  # report, never fake
             cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
+    del host_file, pin_file, pin_side
 
     traffic, traffic_src, pipes = ncu_traffic("k_decode_segments", {"model": args.model,
                                                                    "chunk_size": args.chunk_size,
                                                                    "seg_shift": args.seg_shift, "layers": args.layers})
+    n_tasks = int(pm.tasks.shape[0])
+    n_chunks = int(pm.jobs.n)
+    index_bytes = pm.index.nbytes
+    file_bytes = pm.file_bytes
+    launches_per_step = unp.launches
+    del unp, out, m, pm
+    torch.cuda.empty_cache()
+
+    extra = None
+    if args.extra_model != "none":
+        try:
+            m2, pm2, digest2, _ = build_packed(args, args.extra_model, dev)
+            u2 = DeviceUnpack(pm2, dev)
+            for _ in range(3):
+                u2()
+            torch.cuda.synchronize()
+            if int(u2.bad.item()) != 0 or not torch.equal(u2.out, m2.payload):
+                raise RuntimeError("extra-model unpack mismatch")
+            ms2 = time_ms(lambda: u2(record=True), 20)
+            extra = {"model": args.extra_model, "value": pm2.raw_bytes / (ms2 / 1e3) / 1e9, "unit": "GB/s",
+                     "ms_per_step": ms2, "decode_kernel_ms": u2.kernel_ms(),
+                     "decode_kernel_gbs": pm2.raw_bytes / (u2.kernel_ms() / 1e3) / 1e9,
+                     "cr": pm2.raw_bytes / pm2.file_bytes, "container_digest": digest2,
+                     "decode_step_tokens": decode_step_tokens(m2, pm2, u2.out, dev, 20)}
+            del u2, m2, pm2
+            torch.cuda.empty_cache()
+        except Exception as e:  # report, never hide
+            extra = {"model": args.extra_model, "error": repr(e)[:300]}
+
     if rank == 0:
+        cfg = workload_config(args, raw, file_bytes, digest)
+        cfg.update({"seg_len": 1 << args.seg_shift, "n_chunks": n_chunks, "n_tasks": n_tasks,
+                    "cr_resident": raw / (file_bytes + index_bytes), "index_bytes": index_bytes,
+                    "l2": "inputs (compressed) and outputs exceed the 126 MB L2",
+                    "parallelism": f"dp{world} (replicas)", "build_s": t_build,
+                    "reference_arm": "bench.py --impl reference builds the same container from the same spec "
+                                     "(same container_digest) and unpacks whole-layer samples of it"})
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{args.model}-shaped W8A8 fully compressed (alpha {args.alpha}), decompress all "
-                                   f"chunks of the resident DCC1 container", "weights_shape": args.model,
-                       "chunk_size": args.chunk_size, "seg_len": 1 << args.seg_shift, "n_chunks": int(pm.jobs.n),
-                       "raw_bytes": raw, "file_bytes": pm.file_bytes, "cr": cr_file,
-                       "cr_resident": raw / (pm.file_bytes + pm.index.nbytes), "index_bytes": pm.index.nbytes,
-                       "l2": "inputs (compressed) and outputs exceed the 126 MB L2", "parallelism": f"dp{world} (replicas)",
-                       "build_s": t_build},
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": cfg,
+            "decode_kernel_gbs": raw / (kms / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "kernel": "k_decode_segments", "achieved": achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "traffic_src": traffic_src, "alg_bytes_per_launch": alg_bytes, "launch_ms": kms,
+                         "frac_decompressed": raw / (kms / 1e3) / 1e9 / hbm,
                          # the decode is bound by instruction issue on the ALU pipe, not HBM
                          # (same ncu capture): see DESIGN.md "Why the decode is not at the HBM roofline"
                          "ncu_pipes": pipes},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "decode_step_tokens": tokens,
+            "extra": extra,
             "tp_decode": tp,
             "streaming_tier": streaming_tier,
             "disk_tier": disk_tier,
-            "gpu_launches": args.steps * (1 + int(has_store)),
+            "gpu_launches": args.steps * launches_per_step,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -130,9 +130,11 @@ int dc_store_copy(const uint8_t *base, const uint64_t *blob_off, const uint64_t 
 
 /* --------------------------------------------------------------- CRC32
  * CRC-32/ISO-HDLC (zlib.crc32) of n byte ranges data[off[i] .. off[i]+len[i]);
- * max_len >= every len[i] (sizes the grid).
+ * max_len >= every len[i] (sizes the grid); data_bytes = the size of the
+ * buffer at `data` (enables the TMA lane kernel for whole 64 KB spans of
+ * ranges whose end is 128-byte aligned; 0 = piece kernel only).
  * replaces container.py:169 and :327-331 (zlib.crc32 per chunk). */
-int dc_crc32_ranges(const uint8_t *data, const uint64_t *off, const uint64_t *len, int64_t n,
+int dc_crc32_ranges(const uint8_t *data, uint64_t data_bytes, const uint64_t *off, const uint64_t *len, int64_t n,
                     uint64_t max_len, uint32_t *crc_out, void *stream);
 
 /* ------------------------------------------------------- rANS encoding
@@ -248,21 +250,15 @@ int dc_w8a8_grouped_persist(const void *maps, const void *tens, const int32_t *u
                             int max_ctas, void *stream);
 
 /* Fused decompress -> W8A8 straight from DCC1 chunks (north-star kernel 3):
- * each thread decodes one 256-symbol segment of one weight row from its
- * split point into registers and tcgen05.st's it into the row's TMEM lane;
- * tcgen05.mma takes A from TMEM (decoded weights never reach HBM).  Index
- * with seg_shift 8; chunk_size, layer offsets and k multiples of
- * dc_fused_slice_bytes(); a unit's rows span <= 2 chunks.  Broken chains
- * set status[chunk] = DC_CHUNK_CHAIN (caller falls back to decode + GEMM).
- * replaces scaling.py:148-151 on weights decoded by ans.py:71-94. */
-int dc_fused_slice_bytes(void);
-
-/* TMEM-ring variant (the fast one): one persistent 16-warp CTA per SM; items
- * (layer, m0, k0, klen) of dc_fused_item_rows() rows x klen <= dc_fused_item_k()
- * bytes; 1024 decode chains write 16-byte groups into a 6-deep TMEM ring of
- * 32-byte K-steps; the last warp to finish a K-step issues its tcgen05.mma
- * (A from TMEM) for all 8 row tiles.  Same layer table, index and status
- * contract as dc_fused_decode_gemm (multiples of 256 instead of 512). */
+ * one persistent 16-warp CTA per SM; items (layer, m0, k0, klen) of
+ * dc_fused_item_rows() rows x klen <= dc_fused_item_k() bytes; 1024 decode
+ * chains (each from its split point, seg_shift 8) write 16-byte groups into a
+ * 6-deep TMEM ring of 32-byte K-steps; the last warp to finish a K-step issues
+ * its tcgen05.mma (A from TMEM) for all 8 row tiles -- decoded weights never
+ * reach HBM.  chunk_size, layer offsets and k multiples of 256.  Broken chains
+ * (or split points outside the stream) set status[chunk] = DC_CHUNK_CHAIN
+ * (caller falls back to decode + GEMM).  Replaces scaling.py:148-151 on
+ * weights decoded by ans.py:71-94. */
 int dc_fused_item_rows(void);
 int dc_fused_item_k(void);
 /* `epi` (nullable): per layer {float *y; uint32_t *cnt; float scale; int32 n_slices}
@@ -276,10 +272,6 @@ int dc_fused_ring_gemm(const uint8_t *base, const uint64_t *blob_off, const uint
                        const uint32_t *seg_state, const uint32_t *seg_off, const void *layers, const int32_t *items,
                        int64_t n_items, int ntok, int32_t *status, const void *epi, int max_ctas,
                        void *stream);
-int dc_fused_decode_gemm(const uint8_t *base, const uint64_t *blob_off, const uint64_t *blob_len,
-                         const uint64_t *out_len, const uint8_t *codec, uint64_t chunk_size, const int64_t *seg_base,
-                         const uint32_t *seg_state, const uint32_t *seg_off, const void *layers,
-                         const int32_t *units, int64_t n_units, int ntok, int32_t *status, void *stream);
 
 #ifdef __cplusplus
 }

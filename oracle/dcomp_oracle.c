@@ -323,3 +323,62 @@ int or_prune(const int8_t *q, const double *cm, uint64_t rows, uint64_t cols, do
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------ */
+/* Benchmark synthetic weights (bench.py; not a reference function).   */
+/* Both bench arms must pack byte-identical containers, so the weights */
+/* come from an integer hash that the CUDA arm restates with torch ops */
+/* (paper_2502_15443_b200/synth.py hash_weights_device):              */
+/*   h_t = fmix32(key + 3j + t), t = 0..2 (uint32 arithmetic)          */
+/*   u   = sum of the six 16-bit halves of h_0..h_2                    */
+/*   w_j = (double)(u - 196605) * GEN_SCALE      (Irwin-Hall(6) ~ N(0,0.2)) */
+/* followed by scale_weights + quantize exactly as or_quantize.         */
+/* ------------------------------------------------------------------ */
+#define GEN_SCALE 4.315837287515549e-06 /* 0.2 / (65536 * sqrt(6 / 12)) */
+
+static inline uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h;
+}
+
+static inline double gen_w(uint32_t key, uint64_t j) {
+    uint32_t u = 0;
+    for (uint32_t t = 0; t < 3; t++) {
+        uint32_t h = fmix32(key + 3u * (uint32_t)j + t);
+        u += (h & 0xFFFFu) + (h >> 16);
+    }
+    return (double)((int32_t)u - 196605) * GEN_SCALE;
+}
+
+void or_gen_weights(uint32_t key, uint64_t start, uint64_t n, double *out) {
+    for (uint64_t i = 0; i < n; i++) out[i] = gen_w(key, start + i);
+}
+
+int or_gen_quantize(uint32_t key, const double *s, uint64_t rows, uint64_t cols, int8_t *q,
+                    double *w_scale_out) {
+    uint64_t n = rows * cols;
+    if (n == 0) return 1;
+    double m = 0.0;
+    for (uint64_t r = 0; r < rows; r++)
+        for (uint64_t c = 0; c < cols; c++) {
+            double v = fabs(gen_w(key, r * cols + c) * s[c]); /* scaling.py:81, :99 */
+            if (v > m) m = v;
+        }
+    if (m == 0.0) return 2;
+    double ws = m / 127.0; /* scaling.py:102 */
+    for (uint64_t r = 0; r < rows; r++)
+        for (uint64_t c = 0; c < cols; c++) {
+            double x = (gen_w(key, r * cols + c) * s[c]) / ws; /* scaling.py:103 */
+            double a = floor(fabs(x) + 0.5);                    /* scaling.py:84-86 */
+            double v = x < 0 ? -a : (x > 0 ? a : 0.0);
+            if (v > 127.0) v = 127.0;
+            if (v < -127.0) v = -127.0;
+            q[r * cols + c] = (int8_t)v;
+        }
+    *w_scale_out = ws;
+    return 0;
+}

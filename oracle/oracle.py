@@ -81,6 +81,10 @@ def lib():
         L.or_prune.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                ctypes.c_double, ctypes.c_int, ctypes.c_void_p]
         L.or_prune.restype = ctypes.c_int
+        L.or_gen_weights.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p]
+        L.or_gen_quantize.argtypes = [ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.c_void_p, ctypes.c_void_p]
+        L.or_gen_quantize.restype = ctypes.c_int
         del u8p
         _lib = L
     return _lib
@@ -230,6 +234,26 @@ def quantize(w: np.ndarray, s: np.ndarray | None = None) -> tuple[np.ndarray, fl
         raise OracleError("DcompError", "empty input")
     if rc == 2:
         raise OracleError("DcompError", "zero dynamic range")
+    return q, ws.value
+
+
+def gen_weights(key: int, n: int, start: int = 0) -> np.ndarray:
+    """bench.py's hash weights (dcomp_oracle.c or_gen_weights), flat f64."""
+    out = np.empty(n, dtype=np.float64)
+    if n:
+        lib().or_gen_weights(key & 0xFFFFFFFF, start, n, _ptr(out))
+    return out
+
+
+def gen_quantize(key: int, rows: int, cols: int, s: np.ndarray) -> tuple[np.ndarray, float]:
+    """Hash weights -> scale_weights + quantize (scaling.py:78-105), fused so
+    no f64 tensor is materialized.  Releases the GIL (ctypes)."""
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    q = np.empty((rows, cols), dtype=np.int8)
+    ws = ctypes.c_double(0.0)
+    rc = lib().or_gen_quantize(key & 0xFFFFFFFF, _ptr(s), rows, cols, _ptr(q), ctypes.addressof(ws))
+    if rc:
+        raise OracleError("DcompError", "empty input" if rc == 1 else "zero dynamic range")
     return q, ws.value
 
 

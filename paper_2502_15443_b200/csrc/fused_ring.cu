@@ -25,7 +25,7 @@
 
 namespace dc {
 
-struct GemmTensorR {  // identical layout to GemmTensor (fused_gemm.cu)
+struct GemmTensorR {  // identical layout to GemmTensor (gemm_grouped.cu)
     const int8_t* x;
     int32_t* acc;
     int64_t t_off;
@@ -328,11 +328,19 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
                 const int64_t j = seg_base[c.chunk] + (o >> 8);
                 const int64_t je = j + (klen >> 8);
                 const uint64_t sbase = reinterpret_cast<uint64_t>(blob) + kHeaderBytes;
-                c.x = seg_state[j];
-                c.gstart = sbase + seg_off[j];
+                const uint32_t plen = (uint32_t)(blob_len[c.chunk] - kHeaderBytes);
                 const bool tail = (uint64_t)(o >> 8) + (klen >> 8) >= nseg;
+                const uint32_t so = seg_off[j], se = tail ? plen : seg_off[je];
+                c.x = seg_state[j];
                 c.xe = tail ? kStateLower : seg_state[je];
-                c.gend = sbase + (tail ? (uint64_t)(blob_len[c.chunk] - kHeaderBytes) : (uint64_t)seg_off[je]);
+                if (so > se || se > plen) {  // damaged index: an empty span and an
+                    c.x = kStateLower;       // unreachable end state flag the chain
+                    c.xe = 0xFFFFFFFFu;
+                    c.gstart = c.gend = sbase;
+                } else {
+                    c.gstart = sbase + so;
+                    c.gend = sbase + se;
+                }
                 c.mode = TB.single >= 0 ? 2 : 0;
                 c.sym = TB.single >= 0 ? (uint32_t)TB.single : 0u;
             }

@@ -258,193 +258,6 @@ __global__ void __launch_bounds__(kPThreads, 1) k_w8a8_persist(const CUtensorMap
     if (warp == 1) tmem_dealloc(tmem, 32);
 }
 
-// ================================================================== fused
-constexpr int kFThreads = 256;   // 8 warps: TMEM lane quarter = warp & 3, segment = warp >> 2
-constexpr int kFSlice = 512;     // K bytes per unit (2 segments of 256 per row)
-constexpr int kFSeg = 256;       // symbols per chain; index seg_shift must be 8
-constexpr int kFSlot = 256;      // staged stream bytes per chain (larger -> read from global)
-constexpr int kFNT = 16;
-constexpr uint32_t kFCols = 256; // TMEM: A in cols [0,128), accumulator at col 128
-
-struct FusedSmem {
-    TableSmem tab[2];
-    alignas(1024) uint8_t x[kFSlice / 128][kFNT * 128];  // X slice, SW128 atoms (2 KB per 128 B of K)
-    alignas(16) uint8_t slot[kFThreads][kFSlot + 16];
-    uint64_t sbar;
-    uint64_t done;
-    uint32_t tmem;
-    int32_t cur[2];
-};
-
-// one 16-symbol group of a chain read from a generic (global) stream pointer
-__device__ __forceinline__ uint32_t gen_step(uint32_t& x, const uint8_t*& p, const uint8_t* pend, uint32_t tab) {
-    const uint32_t e = lds_u32(tab + ((x & (kProbScale - 1)) << 2));
-    x = (e >> 20) * ((x >> 12) - kProbScale) + (e >> 8);
-    for (int k = 0; k < 2; ++k)
-        if (x < kStateLower) {
-            x = (x << 8) | (p < pend ? (uint32_t)*p : 0u);
-            ++p;
-        }
-    return e;
-}
-
-__global__ void __launch_bounds__(kFThreads, 2) k_fused_decode(
-    const uint8_t* __restrict__ base, const uint64_t* __restrict__ blob_off, const uint64_t* __restrict__ blob_len,
-    const uint64_t* __restrict__ out_len, const uint8_t* __restrict__ codec, uint64_t chunk_size,
-    const int64_t* __restrict__ seg_base, const uint32_t* __restrict__ seg_state,
-    const uint32_t* __restrict__ seg_off, const GemmTensor* __restrict__ tens, const int4* __restrict__ units,
-    int n_units, int ntok, int32_t* __restrict__ status) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    FusedSmem& S = *reinterpret_cast<FusedSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q = warp & 3, part = warp >> 2;
-    if (threadIdx.x == 0) {
-        mbar_init(&S.sbar, kFThreads);
-        mbar_init(&S.done, 1);
-        fence_mbar_init();
-        S.cur[0] = S.cur[1] = -1;
-    }
-    if (warp == 0) tmem_alloc(&S.tmem, kFCols);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = S.tmem;
-    const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16);
-    uint32_t sphase = 0, dphase = 0;
-
-    for (int ui = blockIdx.x; ui < n_units; ui += gridDim.x) {
-        const int4 u = units[ui];
-        const GemmTensor T = tens[u.x];
-        const int m0 = u.y, k0 = u.z;
-        const int row = m0 + q * 32 + lane;
-        const bool valid = row < T.n_rows;
-        const int last_row = min(m0 + 127, T.n_rows - 1);
-        const uint64_t g0 = (uint64_t)T.t_off + (uint64_t)m0 * T.k + k0;
-        const uint64_t g1 = (uint64_t)T.t_off + (uint64_t)last_row * T.k + k0 + kFSlice - 1;
-        const int c_lo = (int)(g0 / chunk_size), c_hi = (int)(g1 / chunk_size);
-        if (c_hi - c_lo > 1) {  // the host never builds such units; refuse rather than mis-decode
-            if (threadIdx.x == 0) atomicExch(&status[c_lo], DC_CHUNK_CHAIN);
-            continue;
-        }
-        const uint64_t g =(uint64_t)T.t_off + (uint64_t)(valid ? row : m0) * T.k + k0 + part * kFSeg;
-        const int c = (int)(g / chunk_size);
-        const uint32_t o = (uint32_t)(g - (uint64_t)c * chunk_size);
-        const bool ans = codec[c] == 1;
-        const uint8_t* blob = base + blob_off[c];
-
-        // ---- chain setup and stream staging (one bulk copy per chain)
-        uint32_t x0 = kStateLower, xe = kStateLower, s_lo = 0, s_hi = 0;
-        const uint8_t* src;
-        if (ans) {
-            const uint64_t nseg = (out_len[c] + kFSeg - 1) / kFSeg;
-            const int64_t j = seg_base[c] + (o / kFSeg);
-            x0 = seg_state[j];
-            s_lo = seg_off[j];
-            const bool lastseg = (o / kFSeg) + 1 >= nseg;
-            s_hi = lastseg ? (uint32_t)(blob_len[c] - kHeaderBytes) : seg_off[j + 1];
-            xe = lastseg ? kStateLower : seg_state[j + 1];
-            src = blob + kHeaderBytes + s_lo;
-        } else {
-            s_hi = kFSeg;
-            src = blob + o;  // stored chunk: raw bytes
-        }
-        const uintptr_t a16 = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
-        const uint32_t delta = (uint32_t)(reinterpret_cast<uintptr_t>(src) - a16);
-        const uint32_t span = (s_hi >= s_lo) ? s_hi - s_lo : 0xFFFFFFFFu;
-        const uint32_t nbytes = (span + delta + 15u) & ~15u;
-        const bool staged = valid && span != 0xFFFFFFFFu && nbytes <= kFSlot + 16 && nbytes > 0;
-        __syncthreads();  // previous unit done with slots, tables and X
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&S.sbar, staged ? nbytes : 0u);
-        if (staged) bulk_g2s(S.slot[threadIdx.x], reinterpret_cast<const void*>(a16), nbytes, &S.sbar);
-        // ---- decode tables for the (at most two) chunks of this unit
-        const bool two = c_hi > c_lo;
-        for (int t = 0; t < 1 + (int)two; ++t) {
-            const int ct = c_lo + t;
-            if (S.cur[t] != ct) {  // uniform: every thread reads the same S.cur
-                __syncthreads();
-                if (codec[ct] == 1) build_decode_table(base + blob_off[ct], S.tab[t]);
-                __syncthreads();
-                if (threadIdx.x == 0) S.cur[t] = ct;
-            }
-        }
-        load_x_sw128<kFNT>(&S.x[0][0], T.x, ntok, T.k, k0, kFSlice);
-        mbar_wait(&S.sbar, sphase);
-        sphase ^= 1u;
-        __syncthreads();  // S.cur / tables visible
-
-        // ---- decode 256 symbols of this row into TMEM columns [part*64, part*64+64)
-        const TableSmem& TB = S.tab[c - c_lo];
-        const uint32_t tab = smem_u32(TB.tab);
-        const int mode = !valid ? 3 : (!ans ? 1 : (TB.single >= 0 ? 2 : (staged ? 0 : 4)));
-        const bool fast = __all_sync(0xffffffffu, mode == 0);
-        uint32_t x = x0;
-        uint32_t p = smem_u32(S.slot[threadIdx.x]) + delta;
-        const uint32_t pbase = p;
-        uint32_t nb = staged ? lds_u8(p) : 0u;
-        const uint8_t* gp = src;
-        const uint8_t* gend = blob + kHeaderBytes + s_hi;
-        const uint32_t col0 = tlane + (uint32_t)part * (kFSeg / 4);
-        for (int grp = 0; grp < kFSeg / 16; ++grp) {
-            uint32_t w[4];
-            if (fast) {
-#pragma unroll
-                for (int v = 0; v < 16; ++v) w[v >> 2] = put_byte(w[v >> 2], dec_step<true>(x, p, nb, tab), v & 3);
-            } else {
-#pragma unroll 1
-                for (int v = 0; v < 16; ++v) {
-                    uint32_t e;
-                    if (mode == 0) e = dec_step<false>(x, p, nb, tab);
-                    else if (mode == 4) e = gen_step(x, gp, gend, tab);
-                    else if (mode == 1) e = lds_u8(p + grp * 16 + v);
-                    else if (mode == 2) e = (uint32_t)TB.single;
-                    else e = 0u;
-                    w[v >> 2] = put_byte(w[v >> 2], e, v & 3);
-                }
-            }
-            tmem_st_32x32b_x4(col0 + grp * 4, w[0], w[1], w[2], w[3]);
-        }
-        // chain check: the segment must end on the next split point
-        if (mode == 0 || mode == 4) {
-            const uint32_t pend = (mode == 0) ? (p - pbase) : (uint32_t)(gp - src);
-            if (x != xe || pend != span) atomicExch(&status[c], DC_CHUNK_CHAIN);
-        } else if (mode == 2 && (x0 != kStateLower || s_hi != s_lo)) {
-            atomicExch(&status[c], DC_CHUNK_CORRUPT);
-        }
-        tmem_wait_st();
-        fence_proxy_async_smem();  // X tile written with generic stores
-        tc_fence_before();
-        __syncthreads();
-
-        // ---- MMA: 16 x (128 x 16 x 32), A from TMEM, X from smem
-        if (threadIdx.x == 0) {
-            tc_fence_after();
-            constexpr uint32_t idesc = idesc_i8(128, kFNT);
-#pragma unroll
-            for (int ks = 0; ks < kFSlice / 32; ++ks)
-                mma_i8_ts(tmem + 128, tmem + ks * 8, sw128_kmajor_desc(smem_u32(S.x[ks >> 2]) + 32 * (ks & 3)), idesc,
-                          ks > 0);
-            mma_commit(&S.done);
-        }
-        __syncwarp();
-        mbar_wait(&S.done, dphase);
-        dphase ^= 1u;
-        tc_fence_after();
-        if (part == 0) {  // warps 0-3 read the accumulator quarter they own
-            uint32_t acc[16];
-            tmem_ld_32x32b_x16(tlane + 128, acc);
-            if (valid) {
-#pragma unroll
-                for (int t = 0; t < kFNT; ++t)
-                    if (t < ntok) atomicAdd(&T.acc[(int64_t)t * T.n_rows + row], (int32_t)acc[t]);
-            }
-        }
-        tc_fence_before();
-    }
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, kFCols);
-}
-
 int make_tmap_i8(CUtensorMap* m, const void* base, uint64_t rows, uint64_t k, uint32_t box_rows);  // gemm_w8a8.cu
 
 static int make_maps(CUtensorMap* maps_host, const int8_t* const* w, const int8_t* const* x, const int64_t* rows,
@@ -509,34 +322,5 @@ extern "C" int dc_w8a8_grouped_persist(const void* maps, const void* tens, const
         reinterpret_cast<const CUtensorMap*>(maps), reinterpret_cast<const GemmTensor*>(tens),
         reinterpret_cast<const int4*>(units), (int)n_units, ntok);
     DC_CHECK_LAUNCH("k_w8a8_persist");
-    return DC_OK;
-}
-
-extern "C" int dc_fused_slice_bytes(void) { return kFSlice; }
-
-// Fused decompress -> W8A8 over DCC1 chunks.  units: int4 (layer, m0, k0, 0)
-// with k0 % 512 == 0; the index must use 256-symbol segments (seg_shift 8);
-// chunk_size, every layer's t_off and k must be multiples of 512 and a unit's
-// 128 rows must span at most two chunks.
-extern "C" int dc_fused_decode_gemm(const uint8_t* base, const uint64_t* blob_off, const uint64_t* blob_len,
-                                    const uint64_t* out_len, const uint8_t* codec, uint64_t chunk_size,
-                                    const int64_t* seg_base, const uint32_t* seg_state, const uint32_t* seg_off,
-                                    const void* tens, const int32_t* units, int64_t n_units, int ntok,
-                                    int32_t* status, void* stream) {
-    if (n_units <= 0 || ntok <= 0 || ntok > kFNT || chunk_size % kFSlice) return DC_ERR_ARG;
-    const size_t smem = sizeof(FusedSmem) + 1024;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_fused_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t grid = n_units < 2LL * sms ? n_units : 2LL * sms;
-    k_fused_decode<<<(unsigned)grid, kFThreads, smem, (cudaStream_t)stream>>>(
-        base, blob_off, blob_len, out_len, codec, chunk_size, seg_base, seg_state, seg_off,
-        reinterpret_cast<const GemmTensor*>(tens), reinterpret_cast<const int4*>(units), (int)n_units, ntok, status);
-    DC_CHECK_LAUNCH("k_fused_decode");
     return DC_OK;
 }

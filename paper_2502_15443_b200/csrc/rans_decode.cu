@@ -278,7 +278,7 @@ __device__ __forceinline__ uint32_t swz(int ls, int h) { return (uint32_t)(ls * 
 // of the task) and writes them out through its staging buffer `ob`.
 template <int NU, int TH>
 __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, int64_t sb, uint32_t lo,
-                                            uint32_t delta, uint32_t plen, uint64_t olen, uint32_t nseg_chunk,
+                                            uint32_t hi, uint32_t delta, uint32_t plen, uint64_t olen, uint32_t nseg_chunk,
                                             const uint32_t* __restrict__ seg_state,
                                             const uint32_t* __restrict__ seg_off, const uint32_t* tab_ptr,
                                             const uint8_t* stage_ptr, uint8_t* ob, uint8_t* __restrict__ obase,
@@ -290,6 +290,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
     const int G = (int)(K >> 4);
     uint32_t x[NU], n[NU];
     Win W[NU];
+    bool wild = false;  // a split point outside the staged span: never used as an address
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
         const int r = warp * 32 + lane + u * TH;
@@ -297,7 +298,9 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
         uint32_t p;
         if (r < ns) {
             x[u] = seg_state[sb + rel];
-            p = stage + seg_off[sb + rel] - lo + delta;
+            const uint32_t so = seg_off[sb + rel];
+            wild = wild || so < lo || so > hi;
+            p = (so < lo || so > hi) ? stage : stage + so - lo + delta;
             const uint64_t rem = olen - ((uint64_t)rel << seg_shift);
             n[u] = rem < K ? (uint32_t)rem : K;
         } else {  // decodes harmless garbage from stage[0..2K), never written
@@ -405,6 +408,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
             __syncwarp();
         }
     }
+    if (wild) atomicExch(st, DC_CHUNK_CHAIN);
     // chain checks: every segment must end exactly where the next one starts
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
@@ -468,7 +472,9 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segme
         const uintptr_t gsrc = reinterpret_cast<uintptr_t>(gstream) + lo;
         const uintptr_t a16 = gsrc & ~(uintptr_t)15;
         const uint32_t delta = (uint32_t)(gsrc - a16);
-        const uint32_t bytes = (hi >= lo) ? ((hi - lo + delta + 15u) & ~15u) : 0xFFFFFFFFu;
+        // a damaged index (hi < lo, or past the stream) is never staged: the
+        // chunk goes to the exact serial decoder
+        const uint32_t bytes = (hi >= lo && hi <= plen) ? ((hi - lo + delta + 15u) & ~15u) : 0xFFFFFFFFu;
         const bool stage_ok = bytes <= Cfg::kStageCap;
 
         __syncthreads();  // previous task done with stage[] and T
@@ -507,10 +513,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segme
         }
         if (warp * 32 >= ns) continue;  // idle warp in a short task
         if (warp * 32 + Cfg::kThreads < ns)
-            decode_warp<2, Cfg::kThreads>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state,
+            decode_warp<2, Cfg::kThreads>(seg_shift, s0, ns, sb, lo, hi, delta, plen, olen, nseg_chunk, seg_state,
                                           seg_off, T.tab, stage, ob, obase, out_aligned, &status[c], fk);
         else
-            decode_warp<1, Cfg::kThreads>(seg_shift, s0, ns, sb, lo, delta, plen, olen, nseg_chunk, seg_state,
+            decode_warp<1, Cfg::kThreads>(seg_shift, s0, ns, sb, lo, hi, delta, plen, olen, nseg_chunk, seg_state,
                                           seg_off, T.tab, stage, ob, obase, out_aligned, &status[c], fk);
     }
 }

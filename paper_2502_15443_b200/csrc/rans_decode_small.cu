@@ -209,12 +209,16 @@ __global__ void __launch_bounds__(kSmThreads, 3) k_decode_small(
             if (r < ns) {
                 x[u] = seg_state[sb + rel];
                 const uint32_t so = seg_off[sb + rel];
-                p = gstream + so;
                 const uint64_t rem = olen - ((uint64_t)rel << seg_shift);
                 n[u] = rem < K ? (uint32_t)rem : K;
                 const uint32_t se = rel + 1 < nseg_chunk ? seg_off[sb + rel + 1] : plen;
-                for (uint32_t b = 0; b < se - so + 8; b += 128)  // segment stream -> L1
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(p + b));
+                if (so <= se && se <= plen) {
+                    p = gstream + so;
+                    for (uint32_t b = 0; b < se - so + 8; b += 128)  // segment stream -> L1
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(p + b));
+                } else {  // damaged index: never an address; the exact decoder re-runs the chunk
+                    atomicExch(&status[c], DC_CHUNK_CHAIN);
+                }
             } else {  // decodes harmless garbage from the stream start, never written
                 x[u] = kStateLower;
                 n[u] = 0;

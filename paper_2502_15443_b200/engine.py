@@ -10,8 +10,11 @@ Data layout in HBM:
   * SegmentIndex  per ANS chunk ceil(len / 2^shift) split points
                   (state u32, stream offset u32): 8 bytes per segment.  It
                   lives OUTSIDE the DCC1 bytes (which stay bit-exact) and is
-                  only an accelerator: a wrong index is detected by the chain
-                  checks and the chunk is re-decoded exactly.
+                  only an accelerator: the kernels never form an address from
+                  a split point outside its chunk's stream span, a wrong one
+                  is caught by the chain checks and the chunk is re-decoded
+                  exactly, and a sidecar whose body CRC fails is not trusted
+                  (every ANS chunk goes to the exact decoder).
 """
 
 from __future__ import annotations
@@ -85,6 +88,10 @@ class SegmentIndex:
     # lazy sidecar: pinned host bytes of (state, off) not yet copied; PipelinedDecode
     # uploads each chunk group's split points just ahead of that group's stream bytes
     pending: torch.Tensor | None = None
+    # sidecar body CRC still to be checked on the device (pinned sidecars): the
+    # device copy of the body (8 * n_segs bytes) and the CRC32 stored after it
+    raw: torch.Tensor | None = None
+    crc_expected: int | None = None
 
     @staticmethod
     def layout(out_len: np.ndarray, codec: np.ndarray, seg_shift: int) -> tuple[np.ndarray, int]:
@@ -155,23 +162,40 @@ class SegmentIndex:
         if ver != 1 or bind != binding or not 6 <= shift <= 10:
             return None
         base, want = cls.layout(jobs.out_len, jobs.codec, shift)
-        # The body CRC is written but not re-verified here: a damaged index can
-        # only slow decoding down (chain checks send the chunk to the exact path).
         if n != want or len(buf) != 22 + 8 * n + 4:
             return None
+        (crc,) = struct.unpack_from("<I", buf, 22 + 8 * n)
         dev = device or _dev()
         pending = None
         if src is not None and src.is_pinned():
+            # the body CRC is checked on the device after the upload
+            # (PipelinedDecode.finish, or right here when not lazy)
             d = nv.device_bytes(8 * n, dev)
             if lazy:
                 pending = src[22:22 + 8 * n]
             else:
                 d[:8 * n].copy_(src[22:22 + 8 * n], non_blocking=True)
+                if n and not _device_crc_ok(d, 8 * n, crc):
+                    return None
         else:
+            if zlib.crc32(memoryview(np.frombuffer(buf, np.uint8, 8 * n, 22))) != crc:
+                return None  # damaged sidecar: not trusted (index-less decode)
             d = nv.to_device_bytes(np.frombuffer(buf, np.uint8, 8 * n, 22), dev)  # pinned, pipelined upload
         off = np.frombuffer(buf, np.uint32, n, 22 + 4 * n)
-        return cls(shift, base, n, _t(base, torch.int64, dev), d[:4 * n].view(torch.int32),
-                   d[4 * n:8 * n].view(torch.int32), h_off=off, pending=pending)
+        idx = cls(shift, base, n, _t(base, torch.int64, dev), d[:4 * n].view(torch.int32),
+                  d[4 * n:8 * n].view(torch.int32), h_off=off, pending=pending)
+        if lazy and pending is not None and n:
+            idx.raw, idx.crc_expected = d, crc
+        return idx
+
+    def body_crc_ok(self) -> bool:
+        """Device check of a lazily uploaded sidecar's body CRC (True when
+        there is nothing to check); call after the upload was issued."""
+        if self.crc_expected is None:
+            return True
+        ok = _device_crc_ok(self.raw, 8 * self.n_segs, self.crc_expected)
+        self.crc_expected, self.raw = None, None
+        return ok
 
     # ---- work decomposition -------------------------------------------------
     def tasks(self, jobs: JobTable, ok: np.ndarray, max_segs: int | None = None) -> torch.Tensor:
@@ -229,6 +253,13 @@ class SegmentIndex:
         out[:, 0], out[:, 1], out[:, 2] = chunk, s0, cnt
         self.last_tasks_host = out
         return pin.to(_dev(), non_blocking=True)
+
+
+def _device_crc_ok(buf: torch.Tensor, nbytes: int, want: int) -> bool:
+    off = torch.zeros(1, dtype=torch.int64, device=buf.device)
+    ln = torch.full((1,), nbytes, dtype=torch.int64, device=buf.device)
+    got = crc32_ranges(buf, off, ln, nbytes)
+    return int(got.item()) & 0xFFFFFFFF == want
 
 
 # ------------------------------------------------------------------ decode
@@ -297,7 +328,8 @@ def crc32_ranges(data: torch.Tensor, d_off: torch.Tensor, d_len: torch.Tensor, m
     n = d_off.shape[0]
     out = torch.empty(max(n, 1), dtype=torch.int32, device=data.device)
     if n:
-        nv.call("dc_crc32_ranges", data.data_ptr(), d_off.data_ptr(), d_len.data_ptr(), n, int(max_len),
+        nv.call("dc_crc32_ranges", data.data_ptr(), data.numel() * data.element_size(), d_off.data_ptr(),
+                d_len.data_ptr(), n, int(max_len),
                 out.data_ptr(), nv.stream_ptr())
     return out[:n]
 
@@ -533,7 +565,8 @@ class PipelinedDecode:
                         status.data_ptr(), sp_comp)
             nv.call("dc_store_copy", image.data_ptr(), off8(jobs.d_blob_off), off8(jobs.d_out_off),
                     off8(jobs.d_out_len), jobs.d_codec.data_ptr() + g0, k, out.data_ptr(), sp_comp)
-            nv.call("dc_crc32_ranges", out.data_ptr(), off8(jobs.d_out_off), off8(jobs.d_out_len), k, max_len,
+            nv.call("dc_crc32_ranges", out.data_ptr(), out.numel(), off8(jobs.d_out_off), off8(jobs.d_out_len), k,
+                    max_len,
                     crc.data_ptr() + 4 * g0, sp_comp)
             ev_dec = torch.cuda.Event()
             ev_dec.record(s_comp)
@@ -552,6 +585,7 @@ class PipelinedDecode:
         if lazy:  # every group's split points are in flight on s_copy
             index.pending = None
             s_comp.wait_stream(s_copy)
+        self.index = index
         self._mark("issued", None)
 
     def _mark(self, name, stream):
@@ -578,9 +612,12 @@ class PipelinedDecode:
         torch.cuda.synchronize(self.dev)
         st = self.status[:n].cpu().numpy()
         redo = np.nonzero(st == nv.CHUNK_CHAIN)[0]
+        if not self.index.body_crc_ok():  # damaged sidecar: every ANS chunk by the exact decoder
+            redo = np.nonzero((st == nv.CHUNK_OK) | (st == nv.CHUNK_CHAIN))[0]
+            redo = redo[(jobs.codec[redo] == 1) & (jobs.out_len[redo] > 0)]
         if len(redo):  # broken split points: exact serial decode, then refresh CRC + host bytes
             decode_serial(self.image, jobs, redo, out, self.status, None)
-            nv.call("dc_crc32_ranges", out.data_ptr(), jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(), n,
+            nv.call("dc_crc32_ranges", out.data_ptr(), out.numel(), jobs.d_out_off.data_ptr(), jobs.d_out_len.data_ptr(), n,
                     self.max_len, self.crc.data_ptr(), self.s_comp.cuda_stream)
             torch.cuda.synchronize(self.dev)
             for c in redo:

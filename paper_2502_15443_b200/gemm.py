@@ -1,4 +1,5 @@
-"""W8A8 GEMMs on the tcgen05 tensor cores (csrc/gemm_w8a8.cu, csrc/fused_gemm.cu).
+"""W8A8 GEMMs on the tcgen05 tensor cores (csrc/gemm_w8a8.cu, csrc/gemm_grouped.cu,
+csrc/fused_ring.cu).
 
 ``w8a8_matmul_exact(qx, qw)`` returns the exact int32 products qx @ qw.T
 (the integer core of the reference's W8A8 numerics, scaling.py:127-152);
@@ -166,42 +167,7 @@ class GroupedInt8:
                     self.unit_p.data_ptr(), self.unit_p.shape[0], self.layers.ntok, int(max_ctas), nv.stream_ptr())
 
 
-class FusedCompressed:
-    """All linears of a model straight from the DCC1 container: the fused
-    decode -> TMEM -> tcgen05 W8A8 kernel (one launch)."""
-
-    def __init__(self, image: torch.Tensor, jobs, index, chunk_size: int, shapes, t_offs, xs, ntok: int):
-        if index is None or index.seg_shift != 8:
-            raise ValueError("fused path needs a split-point index with 256-symbol segments")
-        sl = nv.call("dc_fused_slice_bytes")
-        if chunk_size % sl or any(int(t) % sl for t in t_offs) or any(k % sl for _, k in shapes):
-            raise ValueError(f"fused path needs chunk_size, tensor offsets and K multiples of {sl}")
-        for (r, k), t in zip(shapes, t_offs):  # a 128-row tile may touch at most two chunks
-            if 128 * k > chunk_size:
-                raise ValueError("chunk too small for the fused path (128 rows x K must fit in one chunk)")
-        self.image, self.jobs, self.index, self.chunk_size = image, jobs, index, chunk_size
-        self.layers = _LayerSet(shapes, t_offs, xs, ntok)
-        self.unit_t = self.layers.units(lambda r, k: sl)
-        self.status = torch.zeros(max(jobs.n, 1), dtype=torch.int32, device=image.device)
-
-    @property
-    def accs(self):
-        return self.layers.accs
-
-    def run(self) -> None:
-        self.layers.acc_flat.zero_()
-        j, ix = self.jobs, self.index
-        nv.call("dc_fused_decode_gemm", self.image.data_ptr(), j.d_blob_off.data_ptr(), j.d_blob_len.data_ptr(),
-                j.d_out_len.data_ptr(), j.d_codec.data_ptr(), self.chunk_size, ix.d_seg_base.data_ptr(),
-                ix.d_state.data_ptr(), ix.d_off.data_ptr(), self.layers.tens.data_ptr(), self.unit_t.data_ptr(),
-                self.unit_t.shape[0], self.layers.ntok, self.status.data_ptr(), nv.stream_ptr())
-
-    def check(self) -> np.ndarray:
-        """Per-chunk status after run(); nonzero = chain broken / corrupt."""
-        return self.status[: self.jobs.n].cpu().numpy()
-
-
-class FusedRing(FusedCompressed):
+class FusedRing:
     """Fused decode -> TMEM ring -> tcgen05 W8A8 (csrc/fused_ring.cu): one
     persistent 16-warp CTA per SM, 1024 decode chains feeding the tensor core
     every 32 symbols.  Items: 1024 rows x K-slice (<= 2048 bytes).
@@ -284,6 +250,10 @@ class FusedRing(FusedCompressed):
     @property
     def accs(self):
         return self._accs
+
+    def check(self) -> np.ndarray:
+        """Per-chunk status after run(); nonzero = chain broken / corrupt."""
+        return self.status[: self.jobs.n].cpu().numpy()
 
     def run(self, max_ctas: int = 0) -> None:
         self.layers.acc_flat.zero_()

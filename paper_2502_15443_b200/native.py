@@ -57,7 +57,7 @@ SIGNATURES: dict[str, list] = {
     "dc_decode_small_max_chunk": [],
     "dc_ans_decode_small": [_P, _P, _P, _P, _P, _U32, _P, _P, _P, _P, _I64, _P, _P, _P],
     "dc_store_copy": [_P, _P, _P, _P, _P, _I64, _P, _P],
-    "dc_crc32_ranges": [_P, _P, _P, _I64, _U64, _P, _P],
+    "dc_crc32_ranges": [_P, _U64, _P, _P, _I64, _U64, _P, _P],
     "dc_hist_chunks": [_P, _U64, _U64, _I64, _P, _P],
     "dc_normalize_tables": [_P, _I64, _P, _P, _P],
     "dc_ans_encode_chunks": [_P, _U64, _U64, _I64, _P, _P, _P, _P, _P, _U32, _P, _P, _P, _U32, _P, _U64, _P],
@@ -76,8 +76,6 @@ SIGNATURES: dict[str, list] = {
     "dc_w8a8_grouped_maps": [_P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P],
     "dc_w8a8_grouped": [_P, _P, _P, _I64, ctypes.c_int, _P],
     "dc_w8a8_grouped_persist": [_P, _P, _P, _I64, ctypes.c_int, ctypes.c_int, _P],
-    "dc_fused_slice_bytes": [],
-    "dc_fused_decode_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P],
     "dc_fused_item_rows": [],
     "dc_fused_item_k": [],
     "dc_fused_ring_gemm": [_P, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P, _I64, ctypes.c_int, _P, _P, ctypes.c_int,

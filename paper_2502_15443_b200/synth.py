@@ -81,6 +81,66 @@ def build_from_layout(model: str, layout, alpha: float = 0.5, seed: int = 0, dev
     return DeviceModel(model, names, shapes, payload, scales, svec, cms, alpha)
 
 
+# ---- hash-generated weights (bench.py: both arms build identical containers) ----
+GEN_SCALE = 4.315837287515549e-06   # 0.2 / (65536 * sqrt(6/12)): Irwin-Hall(6) ~ N(0, 0.2)
+_M32 = 0xFFFFFFFF
+
+
+def _fmix32(h: torch.Tensor) -> torch.Tensor:
+    # uint32 arithmetic held in int64 (products wrap mod 2^64, the mask keeps the low word)
+    h = h ^ (h >> 16)
+    h = (h * 0x85EBCA6B) & _M32
+    h = h ^ (h >> 13)
+    h = (h * 0xC2B2AE35) & _M32
+    return h ^ (h >> 16)
+
+
+def hash_weights(key: int, start: int, n: int, device=None) -> torch.Tensor:
+    """f64 weights [start, start+n) of the bench's integer-hash generator:
+    u = sum of the six 16-bit halves of fmix32(key + 3j + t), t = 0..2, and
+    w = (u - 196605) * GEN_SCALE.  Restated in C by oracle/dcomp_oracle.c
+    (or_gen_weights) so the reference arm draws the same bytes on the host."""
+    j = torch.arange(start, start + n, dtype=torch.int64, device=device)
+    base = (j * 3 + (key & _M32)) & _M32
+    u = torch.zeros(n, dtype=torch.int64, device=device)
+    for t in range(3):
+        h = _fmix32((base + t) & _M32)
+        u += (h & 0xFFFF) + (h >> 16)
+    return (u - 196605).to(torch.float64) * GEN_SCALE
+
+
+def build_hash_model(model: str, layout, keys, cms, alpha: float = 0.5, device=None) -> DeviceModel:
+    """Device model from hash weights (``keys[i]`` per tensor) and host f64
+    channel maxima ``cms[i]``: s = compute_scale(cm, alpha) on the host (the
+    reference's numpy pow), scale + quantize on the GPU (kernel 1)."""
+    from .native import device_bytes
+    from .scaling import compute_scale
+    from .tensors import ActivationStats
+    dev = device or torch.device("cuda")
+    total = sum(r * c for _, r, c in layout)
+    payload = device_bytes(total, dev)
+    names, shapes, scales, svec, cmt = [], [], [], [], []
+    pos = 0
+    piece = 1 << 24
+    for (name, r, c), key, cm in zip(layout, keys, cms):
+        s_host = compute_scale(ActivationStats(name, np.asarray(cm, np.float64)), alpha).s
+        s = torch.from_numpy(np.ascontiguousarray(s_host)).to(dev)
+        w = torch.empty(r * c, dtype=torch.float64, device=dev)
+        for a in range(0, r * c, piece):
+            b = min(r * c, a + piece)
+            w[a:b] = hash_weights(key, a, b - a, dev)
+        q = payload[pos:pos + r * c].view(torch.int8).view(r, c)
+        _, ws = quantize_device(w.view(r, c), s, name, out=q)
+        del w
+        names.append(name)
+        shapes.append((r, c))
+        scales.append(ws)
+        svec.append(s)
+        cmt.append(torch.from_numpy(np.ascontiguousarray(cm, dtype=np.float64)).to(dev))
+        pos += r * c
+    return DeviceModel(model, names, shapes, payload, scales, svec, cmt, alpha)
+
+
 def header_for(m: DeviceModel, chunk_size: int) -> bytes:
     """DCC1 header body for a device model (f32 s / cm as the format stores)."""
     import struct

@@ -51,34 +51,6 @@ def test_persistent_int8_split_k_exact(cuda):
         assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
 
 
-@pytest.mark.parametrize("ntok,stored", [(1, False), (7, True), (16, False)])
-def test_fused_decode_gemm_exact(cuda, ntok, stored):
-    from paper_2502_15443_b200 import container, engine
-    from paper_2502_15443_b200.gemm import FusedCompressed
-    ws, xs = _weights(3), _xs(ntok, 4)
-    payload = torch.cat([w.reshape(-1).view(torch.uint8) for w in ws]).cuda()
-    t_offs = np.concatenate([[0], np.cumsum([w.numel() for w in ws])[:-1]])
-    chunk = 1 << 20
-    n = -(-payload.numel() // chunk)
-    plan = None
-    if stored:  # every other chunk stored raw: exercises the copy path
-        plan = np.array([i % 2 == 0 for i in range(n)])
-    header = b"\x00" * 8
-    image, enc, entries = container.pack_device(payload, header, chunk, plan, seg_shift=8)
-    jobs = container.jobs_for(entries, image.device)
-    fc = FusedCompressed(image, jobs, enc.index, chunk, [w.shape for w in ws], t_offs, [x.cuda() for x in xs], ntok)
-    fc.run()
-    torch.cuda.synchronize()
-    assert (fc.check() == 0).all()
-    for w, x, acc in zip(ws, xs, fc.accs):
-        assert torch.equal(acc.cpu().long(), x.long() @ w.long().T)
-    # a corrupted split point is detected (chain check) instead of trusted
-    enc.index.d_state[3] += 1
-    fc.run()
-    torch.cuda.synchronize()
-    assert (fc.check() != 0).any()
-
-
 @pytest.mark.parametrize("ntok,stored,chunk", [(1, False, 1 << 22), (5, True, 1 << 22), (16, False, 1 << 24)])
 def test_fused_ring_exact(cuda, ntok, stored, chunk):
     from paper_2502_15443_b200 import container
