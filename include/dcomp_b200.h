@@ -211,6 +211,9 @@ int dc_scale_weights(const double *w, const double *s, int64_t rows, int64_t col
 /* ------------------------------------------------------ pruning (kernel 1)
  * Zero the k lowest scores cm[c]*|q| (f64), ties by row-major index (rows*cols < 2^32).
  * replaces pruning.py:37-64 (prune_scores, _lowest_k, prune). */
+/* score[r, c] = cm[c] * |q[r, c]| as f64 (rows x cols, row-major).
+ * replaces pruning.py:37-40 (prune_scores). */
+int dc_prune_scores(const int8_t *q, const double *cm, int64_t rows, int64_t cols, double *out, void *stream);
 int dc_prune_scratch_bytes(int64_t rows, int64_t cols, uint64_t *out_host);
 int dc_prune_tensor(const int8_t *q, const double *cm, int64_t rows, int64_t cols, int64_t k, int8_t *out,
                     uint8_t *scratch, void *stream);

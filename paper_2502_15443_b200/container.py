@@ -21,7 +21,13 @@ What runs where:
 
 ``pack``/``unpack`` return exactly what the reference returns (bytes /
 ModelBundle); ``pack_indexed``, ``unpack(..., index=)``, the ``.dcidx``
-sidecar and ``DeviceContainer`` (device.py) are B200 extensions.
+sidecar and ``pack_device`` (a payload already on the GPU) are B200
+extensions.
+
+Memory note: ``unpack`` decodes into ONE pinned host buffer and the returned
+tensors' ``qvalues`` are views into it (the D2H runs at PCIe speed straight
+into them); the buffer lives as long as any of those arrays.  Pass
+``copy=True`` for the reference's independent per-tensor (pageable) copies.
 """
 
 from __future__ import annotations
@@ -511,12 +517,19 @@ def _prefix(view: np.ndarray) -> bytes:
     return bytes(view[: min(view.size, 14 + hlen + count * _ENTRY.size)])
 
 
-def unpack(data, index=None) -> ModelBundle:
+def _copied(b: ModelBundle) -> ModelBundle:
+    ts = [QuantizedTensor(t.name, np.array(t.qvalues, copy=True), t.w_scale, t.scale_vec) for t in b.tensors]
+    return ModelBundle(tensors=ts, stats=b.stats, chunk_size=b.chunk_size)
+
+
+def unpack(data, index=None, copy: bool = False) -> ModelBundle:
     """Decode and verify a container (inverse of pack).  ``index`` (a
     SegmentIndex or sidecar bytes) enables the split-point parallel decoder;
     without it each ANS chunk is decoded by one exact sequential walk.
     ``data`` (and a sidecar ``index``) may also be pinned CPU uint8 tensors:
-    the container is then copied to the GPU straight from that memory."""
+    the container is then copied to the GPU straight from that memory.
+    ``copy=True``: per-tensor pageable copies instead of views of the pinned
+    output buffer (see the module docstring)."""
     import time
     clock = [time.perf_counter()]
 
@@ -543,7 +556,7 @@ def unpack(data, index=None) -> ModelBundle:
     if index is None and _INDEX_CACHE_SIZE > 0:  # split points recorded by an earlier index-less unpack
         try:
             binding = binding_of(head)
-            index = _INDEX_CACHE.get(binding)
+            index = _INDEX_CACHE.get((torch.cuda.current_device(), binding))
         except struct.error:
             binding = None
     if index is not None:  # split-point path: H2D / decode / D2H pipelined per chunk group
@@ -577,7 +590,7 @@ def unpack(data, index=None) -> ModelBundle:
             bad = np.nonzero(crc != ent["crc32"])[0]
             if len(bad):
                 raise ChecksumError(int(bad[0]))
-            return out
+            return _copied(out) if copy else out
     chunk_size, directory, ent, _ = _parse(head, total)
     if len(ent) == 0:
         return _bundle(directory, np.empty(0, np.uint8), chunk_size)
@@ -588,20 +601,21 @@ def unpack(data, index=None) -> ModelBundle:
     res = decode_and_verify(base, ent, index=index, build_index=record)
     lap("decode_crc")
     if record and res.index is not None and res.index.n_segs:  # verified: keep for the next unpack
-        _INDEX_CACHE[binding] = res.index
+        _INDEX_CACHE[(torch.cuda.current_device(), binding)] = res.index
         while len(_INDEX_CACHE) > _INDEX_CACHE_SIZE:
             _INDEX_CACHE.pop(next(iter(_INDEX_CACHE)))
     host = nv.to_host(res.out)
     lap("d2h")
     out = _bundle(directory, host, chunk_size)
     lap("bundle")
-    return out
+    return _copied(out) if copy else out
 
 
 # Split-point indexes recorded by index-less unpacks (the serial pass records
 # them for free), keyed by the container's binding: a later unpack of the same
 # container takes the parallel path.  Device memory: 8 B per 256 B of weights
-# per entry; DCOMP_INDEX_CACHE=0 disables, clear_index_cache() frees.
+# per entry, keyed by (device, binding) so an index is only used on the device
+# that holds it; DCOMP_INDEX_CACHE=0 disables, clear_index_cache() frees.
 _INDEX_CACHE: dict = {}
 _INDEX_CACHE_SIZE = int(os.environ.get("DCOMP_INDEX_CACHE", "2"))
 

@@ -686,6 +686,43 @@ __global__ void __launch_bounds__(kPrThreads) k_prune_rows(const int8_t* __restr
 using namespace dc;
 
 // Per-tensor prune.  scratch: >= 8*65536 + 64 + 4*ceil(n/4096) + 4*cols*129 bytes.
+namespace dc {
+// Eq. 5 importance score (pruning.py:37-40): score[r, c] = cm[c] * |q[r, c]|,
+// f64 (exact: |q| <= 127 is exact and one IEEE multiply, never -0.0 since
+// cm >= 0 and |q| >= 0).  16 int8 per thread (one 16-B load), 8-B stores.
+__global__ void k_prune_scores(const int8_t* __restrict__ q, const double* __restrict__ cm, int64_t rows,
+                               int64_t cols, double* __restrict__ out) {
+    const int64_t n = rows * cols;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 16;
+    for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; i0 < n; i0 += stride) {
+        if (i0 + 16 <= n && (reinterpret_cast<uintptr_t>(q + i0) & 15) == 0) {
+            const int4 v = *reinterpret_cast<const int4*>(q + i0);
+            const int8_t* b = reinterpret_cast<const int8_t*>(&v);
+            int64_t c = i0 % cols;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                out[i0 + k] = cm[c] * (double)abs((int)b[k]);
+                if (++c == cols) c = 0;
+            }
+        } else {
+            for (int64_t i = i0; i < n && i < i0 + 16; ++i) out[i] = cm[i % cols] * (double)abs((int)q[i]);
+        }
+    }
+}
+}  // namespace dc
+
+extern "C" int dc_prune_scores(const int8_t* q, const double* cm, int64_t rows, int64_t cols, double* out,
+                               void* stream) {
+    if (rows < 0 || cols < 0) return DC_ERR_ARG;
+    const int64_t n = rows * cols;
+    if (n == 0) return DC_OK;
+    const int64_t want = (n + 16 * 256 - 1) / (16 * 256);
+    const int64_t grid = want < (int64_t)sm_count_pr() * 8 ? want : (int64_t)sm_count_pr() * 8;
+    k_prune_scores<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(q, cm, rows, cols, out);
+    DC_CHECK_LAUNCH("k_prune_scores");
+    return DC_OK;
+}
+
 extern "C" int dc_prune_scratch_bytes(int64_t rows, int64_t cols, uint64_t* out) {
     const int64_t n = rows * cols;
     const uint64_t n_cb = (uint64_t)((cols + kHcCols - 1) / kHcCols);

@@ -68,6 +68,7 @@ SIGNATURES: dict[str, list] = {
     "dc_dequantize": [_P, ctypes.c_double, _P, _I64, _I64, _P, _P],
     "dc_scale_weights": [_P, _P, _I64, _I64, _P, _P],
     "dc_prune_scratch_bytes": [_I64, _I64, _P],
+    "dc_prune_scores": [_P, _P, _I64, _I64, _P, _P],
     "dc_prune_tensor": [_P, _P, _I64, _I64, _I64, _P, _P, _P],
     "dc_prune_rows": [_P, _P, _I64, _I64, _I64, _P, _P],
     "dc_w8a8_gemm": [_P, _I64, _I64, _P, _I64, _P, _I64, _P],

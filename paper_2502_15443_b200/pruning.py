@@ -44,8 +44,10 @@ def prune_scores(q: QuantizedTensor, stats: ActivationStats) -> np.ndarray:
         raise DcompError(f"{q.name}: stats length {len(stats.channel_max)} != cols {q.cols}")
     dev = nv.require_cuda()
     dq = torch.from_numpy(np.ascontiguousarray(q.qvalues)).to(dev)
-    cm = torch.from_numpy(stats.channel_max).to(dev)
-    return (cm[None, :] * dq.to(torch.float64).abs()).cpu().numpy()
+    cm = torch.from_numpy(np.ascontiguousarray(stats.channel_max, dtype=np.float64)).to(dev)
+    out = torch.empty(q.qvalues.shape, dtype=torch.float64, device=dev)
+    nv.call("dc_prune_scores", dq.data_ptr(), cm.data_ptr(), q.rows, q.cols, out.data_ptr(), nv.stream_ptr())
+    return out.cpu().numpy()
 
 
 def prune_device(q: torch.Tensor, cm: torch.Tensor, sparsity: float, per_row: bool = False,

@@ -333,6 +333,9 @@ class StreamedRawFile:
 
     def step(self) -> None:
         G, S = len(self.groups), self.slots
+        # the previous step's GEMM (compute stream) must be done reading self.out
+        # before this step's copies overwrite it (same rule as StreamedCompressed)
+        self.s_copy.wait_stream(torch.cuda.current_stream())
         futs = {g: self.pool.submit(self._read, g) for g in range(min(S, G))}
         for g, (a, b) in enumerate(self.groups):
             off = futs.pop(g).result()

@@ -144,3 +144,26 @@ def test_no_gpu_means_loud_failure():
         pytest.skip("GPU present")
     with pytest.raises(native.NativeUnavailable):
         dc.compress_blob(b"abc")
+
+
+def test_choose_architecture_reference_cases():
+    """latency.py:234-241 with the reference's own cases (test_latency.py:183-197):
+    tiers by capacity, monotone in GPU memory."""
+    def profile(mem_gpu=48e9, mem_cpu=64e9):
+        return dc.HardwareProfile(B_stoc=7.0, B_ctog=32.0, B_gpu=696.0, D_max=156.08, c_sat=76.72e6,
+                                  I_gpu=300.0, mem_gpu=mem_gpu, mem_cpu=mem_cpu)
+    A = dc.Architecture
+    p = profile()
+    assert dc.choose_architecture(p, 4e9, 1e9) is A.GPU_BUFFER
+    assert dc.choose_architecture(p, 60e9, 1e9) is A.GPU_CPU
+    assert dc.choose_architecture(p, 200e9, 1e9) is A.STORAGE
+    order = [A.GPU_BUFFER, A.GPU_CPU, A.STORAGE]
+    prev = len(order)
+    for mem in (1e9, 10e9, 50e9, 70e9, 300e9):
+        rank = order.index(dc.choose_architecture(profile(mem_gpu=mem), 60e9, 1e9))
+        assert rank <= prev
+        prev = rank
+    # boundary: exactly full fits (<=), one byte more spills to the next tier
+    assert dc.choose_architecture(profile(mem_gpu=10.0), 6.0, 4.0) is A.GPU_BUFFER
+    assert dc.choose_architecture(profile(mem_gpu=10.0, mem_cpu=5.0), 6.0, 5.0) is A.GPU_CPU
+    assert dc.choose_architecture(profile(mem_gpu=10.0, mem_cpu=5.0), 11.0, 5.0) is A.STORAGE

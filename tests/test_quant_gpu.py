@@ -125,3 +125,31 @@ def test_prune_properties(cuda):
     assert np.array_equal(a.qvalues, b.qvalues)  # idempotent
     c = cuda.prune(qt, st, cuda.PruneConfig(0.4))
     assert np.all((a.qvalues == 0) <= (c.qvalues == 0))  # nested zero sets
+
+
+def test_prune_scores_reference_cases(cuda):
+    """pruning.py:37-40 through dc_prune_scores, with the reference's own
+    known answers (test_pruning.py:28-58) and an f64 numpy restatement."""
+    dc = cuda
+
+    def qt(vals, cm=None):
+        v = np.asarray(vals, dtype=np.int8)
+        cm = np.ones(v.shape[1]) if cm is None else np.asarray(cm, dtype=np.float64)
+        return (dc.QuantizedTensor("t", v, 1.0, dc.ScaleVector.identity(v.shape[1])),
+                dc.ActivationStats("t", cm))
+
+    q, st = qt([[10, -10]], [1.0, 2.0])
+    assert dc.prune_scores(q, st).tolist() == [[10.0, 20.0]]
+    q, st = qt([[0, 5]], [100.0, 1.0])
+    assert dc.prune_scores(q, st)[0, 0] == 0.0
+    q, _ = qt([[1, 2]])
+    with pytest.raises(dc.DcompError):
+        dc.prune_scores(q, dc.ActivationStats("t", np.ones(3)))
+    rng = np.random.default_rng(4)
+    for r, c in [(6, 5), (33, 77), (512, 1024), (3, 4099)]:
+        v = rng.integers(-127, 128, (r, c)).astype(np.int8)
+        cm = rng.uniform(0.0, 3.0, c)
+        q, st = qt(v, cm)
+        got = dc.prune_scores(q, st)
+        want = cm[None, :] * np.abs(v.astype(np.float64))
+        assert got.dtype == np.float64 and np.array_equal(got.view(np.uint64), want.view(np.uint64))
