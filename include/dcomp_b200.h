@@ -205,6 +205,12 @@ int dc_quantize(const void *w, int dtype, const double *s, int64_t rows, int64_t
 int dc_dequantize(const int8_t *q, double w_scale, const double *s, int64_t rows, int64_t cols, double *out,
                   void *stream);
 
+/* Calibration statistics: acc_bits[c] = max(acc_bits[c], bits(|x[r, c]| as f64))
+ * over rows x cols activations x (dtype as dc_quantize), i.e. a running
+ * per-input-channel max|x| kept as f64 bit patterns (zero-initialise once).
+ * replaces the exporter's forward pre-hook (exporter export.py:85-90). */
+int dc_channel_absmax(const void *x, int dtype, int64_t rows, int64_t cols, uint64_t *acc_bits, void *stream);
+
 /* out = W * s[c].  replaces scaling.py:78-81 (scale_weights). */
 int dc_scale_weights(const double *w, const double *s, int64_t rows, int64_t cols, double *out, void *stream);
 

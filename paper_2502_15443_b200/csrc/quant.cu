@@ -15,6 +15,8 @@
 
 namespace dc {
 
+int sm_count();  // rans_decode.cu
+
 enum : int { kF64 = 0, kF32 = 1, kBF16 = 2, kF16 = 3 };
 
 template <int T>
@@ -280,6 +282,54 @@ static int64_t rows_per(int64_t rows, int64_t cols) {
 }  // namespace dc
 
 using namespace dc;
+
+namespace dc {
+// Calibration statistics (exporter export.py:77-123): per input channel, the
+// running max of |x| over every token that enters a linear layer.  x is
+// [rows = tokens][cols = channels] in any of the input dtypes, widened to f64
+// exactly.  Thread j of a CTA owns column c0 + j over a slab of rows (so
+// loads are coalesced across the warp); one atomicMax per column per CTA on
+// the f64 bit pattern (non-negative doubles order like their bits; a NaN
+// propagates as the largest pattern, like torch's amax).
+template <int T>
+__global__ void __launch_bounds__(kQThreads) k_channel_absmax(const typename In<T>::type* __restrict__ x,
+                                                               int64_t rows, int64_t cols, int64_t rows_per_cta,
+                                                               unsigned long long* __restrict__ acc) {
+    const int64_t c = (int64_t)blockIdx.y * kQThreads + threadIdx.x;
+    if (c >= cols) return;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+    const int64_t r1 = min(rows, r0 + rows_per_cta);
+    unsigned long long m = 0;
+    for (int64_t r = r0; r < r1; ++r) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(In<T>::f64(x[r * cols + c])));
+        m = b > m ? b : m;
+    }
+    if (r1 > r0) atomicMax(&acc[c], m);
+}
+}  // namespace dc
+
+extern "C" int dc_channel_absmax(const void* x, int dtype, int64_t rows, int64_t cols, uint64_t* acc_bits,
+                                 void* stream) {
+    if (rows < 0 || cols < 0 || dtype < 0 || dtype > 3) return DC_ERR_ARG;
+    if (rows == 0 || cols == 0) return DC_OK;
+    const int64_t cblocks = (cols + kQThreads - 1) / kQThreads;
+    int64_t rblocks = (int64_t)sm_count() * 8 / cblocks;
+    rblocks = rblocks < 1 ? 1 : (rblocks > rows ? rows : rblocks);
+    const int64_t per = (rows + rblocks - 1) / rblocks;
+    dim3 grid((unsigned)((rows + per - 1) / per), (unsigned)cblocks);
+    auto* a = reinterpret_cast<unsigned long long*>(acc_bits);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (dtype) {
+        case kF64: k_channel_absmax<kF64><<<grid, kQThreads, 0, st>>>((const double*)x, rows, cols, per, a); break;
+        case kF32: k_channel_absmax<kF32><<<grid, kQThreads, 0, st>>>((const float*)x, rows, cols, per, a); break;
+        case kBF16:
+            k_channel_absmax<kBF16><<<grid, kQThreads, 0, st>>>((const __nv_bfloat16*)x, rows, cols, per, a);
+            break;
+        default: k_channel_absmax<kF16><<<grid, kQThreads, 0, st>>>((const __half*)x, rows, cols, per, a); break;
+    }
+    DC_CHECK_LAUNCH("k_channel_absmax");
+    return DC_OK;
+}
 
 extern "C" int dc_quant_absmax(const void* w, int dtype, const double* s, int64_t rows, int64_t cols,
                                unsigned long long* absmax_bits, int* nonfinite, void* stream) {

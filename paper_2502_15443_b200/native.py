@@ -58,6 +58,7 @@ SIGNATURES: dict[str, list] = {
     "dc_ans_decode_small": [_P, _P, _P, _P, _P, _U32, _P, _P, _P, _P, _I64, _P, _P, _P],
     "dc_store_copy": [_P, _P, _P, _P, _P, _I64, _P, _P],
     "dc_crc32_ranges": [_P, _U64, _P, _P, _I64, _U64, _P, _P],
+    "dc_channel_absmax": [_P, ctypes.c_int, _I64, _I64, _P, _P],
     "dc_hist_chunks": [_P, _U64, _U64, _I64, _P, _P],
     "dc_normalize_tables": [_P, _I64, _P, _P, _P],
     "dc_ans_encode_chunks": [_P, _U64, _U64, _I64, _P, _P, _P, _P, _P, _U32, _P, _P, _P, _U32, _P, _U64, _P],
