@@ -153,3 +153,24 @@ def test_prune_scores_reference_cases(cuda):
         got = dc.prune_scores(q, st)
         want = cm[None, :] * np.abs(v.astype(np.float64))
         assert got.dtype == np.float64 and np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_analyze_quantized_gpu_equals_reference(cuda):
+    """analyze_quantized on the B200 (k_hist + report_from_histogram) equals
+    the reference's reports (tests/golden/analyze.json), for host arrays,
+    QuantizedTensors and int8 CUDA tensors alike."""
+    import json
+    import os
+    import dataclasses
+    import torch
+    from conftest import GOLDEN
+    from test_analyze_cpu import check_report, int8_cases
+    with open(os.path.join(GOLDEN, "analyze.json")) as f:
+        gold = json.load(f)["int8"]
+    for name, v in int8_cases():
+        check_report(dataclasses.asdict(cuda.analyze_quantized(v)), gold[name])
+        check_report(dataclasses.asdict(cuda.analyze_quantized(torch.from_numpy(v).cuda())), gold[name])
+        qt = cuda.QuantizedTensor(name, v, 1.0, cuda.ScaleVector.identity(v.shape[1]))
+        check_report(dataclasses.asdict(cuda.analyze_quantized(qt)), gold[name])
+    with pytest.raises(cuda.DcompError):
+        cuda.analyze_quantized(np.zeros((0, 3), np.int8))
