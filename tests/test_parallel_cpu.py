@@ -89,3 +89,130 @@ def test_tp_allreduce_gloo_world2():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+# ------------------------------------------------- sharded unpack (C3, N GPUs)
+def _oracle_decode(image, loc, body, seg_shift):
+    """Test decoder: the oracle restatement decodes this rank's chunks
+    (the GPU engine's role); same (out, status, crc) contract."""
+    from oracle import oracle as O
+    from paper_2502_15443_b200 import native as nv
+    outs, status, crcs = [], [], []
+    for e in loc:
+        blob = image[int(e["file_offset"]):int(e["file_offset"] + e["comp_len"])].tobytes()
+        n = int(e["uncomp_len"])
+        st, raw = nv.CHUNK_OK, np.zeros(n, np.uint8)
+        if e["codec"] == 0:
+            raw = np.frombuffer(blob, np.uint8).copy()
+        else:
+            try:
+                raw = np.frombuffer(O.decompress_blob(blob, n), np.uint8).copy()
+            except O.OracleError as x:
+                st = {"TruncatedError": nv.CHUNK_TRUNC_TABLE}.get(x.kind, nv.CHUNK_CORRUPT)
+                if "frequency table" in x.msg:
+                    st = nv.CHUNK_BAD_TABLE
+                elif "out of range" in x.msg:
+                    st = nv.CHUNK_STATE_RANGE
+        outs.append(raw)
+        status.append(st)
+        crcs.append(O.crc32(raw))
+    return np.concatenate(outs), np.array(status, np.int32), np.array(crcs, np.uint32)
+
+
+def _model_bytes(seed=0):
+    from oracle import oracle as O
+    rng = np.random.default_rng(seed)
+    ents = []
+    for i, (r, c) in enumerate([(300, 700), (128, 1024), (77, 513), (256, 600)]):
+        q = np.clip(np.round(rng.normal(0, 9, (r, c))), -127, 127).astype(np.int8)
+        ents.append((f"w{i}", q, 0.01, 0.5, np.ones(c), np.ones(c)))
+    n = -(-sum(e[1].size for e in ents) // 16384)
+    mask = np.array([i % 5 != 3 for i in range(n)])  # a few stored chunks
+    data = O.pack(ents, 16384, mask=mask)
+    return data, np.concatenate([e[1].reshape(-1).view(np.uint8) for e in ents])
+
+
+def _outcome(fn):
+    try:
+        return ("ok", fn())
+    except Exception as e:  # noqa: BLE001
+        return (type(e).__name__, str(e))
+
+
+def _sharded_worker(rank, world, port, q, path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_15443_b200 import container, sharded
+        data, payload = _model_bytes()
+        ent = container._parse(data)[2]
+        res = {}
+        r = sharded.unpack_shard(path, rank, world, decode=_oracle_decode)
+        res["exact"] = bool(np.array_equal(r.out, payload[r.shard.out0:r.shard.out1]))
+        res["range"] = (r.shard.c0, r.shard.c1)
+        # damage: a corrupt ANS stream on the last rank, a prologue error and a
+        # stored-chunk bit flip (CRC) on the first: every rank must raise the
+        # reference's first error (prologue before corrupt before checksum)
+        ans = [i for i in range(len(ent)) if ent["codec"][i] == 1]
+        store = [i for i in range(len(ent)) if ent["codec"][i] == 0]
+        cases = {}
+        b = bytearray(data)
+        last = ans[-1]
+        b[int(ent["file_offset"][last]) + 400] ^= 0x20
+        cases["corrupt_last"] = bytes(b)
+        b2 = bytearray(cases["corrupt_last"])
+        b2[int(ent["file_offset"][ans[0]]) + 384] = 0  # start state -> out of range (prologue)
+        b2[int(ent["file_offset"][ans[0]]) + 387] = 0
+        cases["prologue_first_and_corrupt_last"] = bytes(b2)
+        b3 = bytearray(data)
+        b3[int(ent["file_offset"][store[-1]]) + 10] ^= 1
+        cases["crc_store"] = bytes(b3)
+        for k, v in cases.items():
+            res[k] = _outcome(lambda: sharded.unpack_shard(v, rank, world, decode=_oracle_decode) and None)
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_unpack_gloo_world2(tmp_path):
+    """One container, two ranks: each reads and decodes only its chunk range;
+    the union is the payload; verdicts agree with the single-process unpack
+    (oracle) on every rank."""
+    from oracle import oracle as O
+    from paper_2502_15443_b200 import container, sharded
+    data, _ = _model_bytes()
+    path = tmp_path / "m.dcc"
+    path.write_bytes(data)
+    ent = container._parse(data)[2]
+    plan = sharded.plan_shards(ent, 2)
+    assert plan[0].c0 == 0 and plan[0].c1 == plan[1].c0 and plan[1].c1 == len(ent)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q, str(path))) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0]["exact"] and res[1]["exact"]
+    assert res[0]["range"][1] == res[1]["range"][0]
+    # expected verdicts: the oracle's single-process unpack of the same bytes
+    data2, _ = _model_bytes()
+    for k in ("corrupt_last", "prologue_first_and_corrupt_last", "crc_store"):
+        assert res[0][k] == res[1][k], k
+        assert res[0][k][0] != "ok", k
+    ans = [i for i in range(len(ent)) if ent["codec"][i] == 1]
+    assert res[0]["corrupt_last"] == ("CorruptStreamError", f"corrupt stream (chunk {ans[-1]})")
+    assert res[0]["prologue_first_and_corrupt_last"][0] == "CorruptStreamError"
+    assert f"chunk {ans[0]})" in res[0]["prologue_first_and_corrupt_last"][1]
+    assert res[0]["crc_store"][0] == "ChecksumError"
+    # the oracle agrees on which chunk fails first
+    b = bytearray(data2)
+    b[int(ent["file_offset"][ans[-1]]) + 400] ^= 0x20
+    try:
+        O.unpack(bytes(b))
+        raise AssertionError("oracle accepted a corrupt stream")
+    except O.OracleError as e:
+        assert e.chunk == ans[-1] or f"chunk {ans[-1]}" in e.msg
