@@ -277,7 +277,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": workload_config(args, raw_total, file_total, digest),
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": f"unpack (decode on {threads} threads in the reference's groups of four "
@@ -307,30 +307,50 @@ class DeviceUnpack:
     compared with the chunk table -- with no host synchronisation (verdicts
     accumulate on the device and are checked after the timed region)."""
 
-    def __init__(self, pm, dev):
+    def __init__(self, pm, dev, chunks=None):
+        """``chunks`` = (c0, c1): only that chunk range (this rank's shard of
+        the container under chunk sharding, sharded.plan_shards)."""
         import torch
+        from paper_2502_15443_b200 import engine
         from paper_2502_15443_b200 import native as nv
         self.pm, self.nv = pm, nv
+        c0, c1 = chunks or (0, pm.jobs.n)
+        ent = pm.entries[c0:c1]
+        j = pm.jobs
+        self.jobs = j if (c0, c1) == (0, j.n) else engine.JobTable.build(
+            j.blob_off[c0:c1], j.blob_len[c0:c1], j.out_off[c0:c1], j.out_len[c0:c1], j.codec[c0:c1], dev)
+        ix = pm.index
+        self.index = ix if (c0, c1) == (0, j.n) else engine.SegmentIndex(
+            ix.seg_shift, ix.seg_base[c0:c1], ix.n_segs, ix.d_seg_base[c0:c1].contiguous(), ix.d_state, ix.d_off,
+            h_off=ix.host_offsets())
+        self.tasks = pm.tasks if (c0, c1) == (0, j.n) else self.index.tasks(self.jobs, np.ones(self.jobs.n, bool))
+        self.range = (int(j.out_off[c0]), int(j.out_off[c1 - 1] + j.out_len[c1 - 1])) if c1 > c0 else (0, 0)
+        self.raw_bytes = self.range[1] - self.range[0]
+        self.ans_raw = int(ent["uncomp_len"][ent["codec"] == 1].sum())
+        self.ans_comp = int(ent["comp_len"][ent["codec"] == 1].sum())
         self.out = nv.device_bytes(pm.raw_bytes, dev)
-        self.status = torch.zeros(max(pm.jobs.n, 1), dtype=torch.int32, device=dev)
-        self.crc = torch.zeros(max(pm.jobs.n, 1), dtype=torch.int32, device=dev)
-        self.want = torch.from_numpy(pm.entries["crc32"].astype(np.uint32).view(np.int32).copy()).to(dev)
+        n = max(self.jobs.n, 1)
+        self.status = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.crc = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.want = torch.from_numpy(ent["crc32"].astype(np.uint32).view(np.int32).copy()).to(dev)
         self.bad = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.has_store = bool((pm.entries["codec"] == 0).any())
-        self.max_len = int(pm.jobs.out_len.max())
+        self.has_store = bool((ent["codec"] == 0).any())
+        self.max_len = int(self.jobs.out_len.max()) if self.jobs.n else 0
         self.events = []
         self.launches = 4 + int(self.has_store)  # validate, decode, [store], crc pieces + finalize
 
     def __call__(self, record: bool = False):
         import torch
         from paper_2502_15443_b200 import engine
-        pm, j, nv = self.pm, self.pm.jobs, self.nv
+        pm, j, nv = self.pm, self.jobs, self.nv
+        if j.n == 0:
+            return
         sp = nv.stream_ptr()
         engine.validate(pm.image, j, self.status)
         if record:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
-        engine.decode_segments(pm.image, j, pm.index, pm.tasks, self.out, self.status)
+        engine.decode_segments(pm.image, j, self.index, self.tasks, self.out, self.status)
         if record:
             ev[1].record()
             self.events.append(ev)
@@ -343,6 +363,15 @@ class DeviceUnpack:
 
     def kernel_ms(self) -> float:
         return sum(a.elapsed_time(b) for a, b in self.events) / max(len(self.events), 1)
+
+
+def allreduce_max(v: float, dev) -> float:
+    """Max over ranks (NCCL on the device; CPU tensor under gloo)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def time_steps(fn, steps: int, world: int, dev):
@@ -360,10 +389,8 @@ def time_steps(fn, steps: int, world: int, dev):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    return float(ms.item())
+    ms = e0.elapsed_time(e1)
+    return allreduce_max(ms, dev) if world > 1 else ms
 
 
 def time_ms(fn, iters):
@@ -430,6 +457,37 @@ def decode_step_tokens(m, pm, out, dev, iters, batches=(1, 16), unfused_step=Non
     return tokens
 
 
+def sharded_e2e(args, host_file: bytes, side: bytes, raw: int, rank: int, world: int, dev) -> dict:
+    """N GPUs, end to end through the public sharded API: every rank calls
+    sharded.unpack_shard(file bytes, rank, world, index=sidecar) -- it reads
+    only its chunk range's bytes and split points, H2D, validate + decode +
+    CRC on its GPU, verdict all-reduce -- then copies its decoded range back
+    to pinned host memory.  Time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_15443_b200 import sharded
+    times = []
+    host_out = None
+    for i in range(args.e2e_steps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = sharded.unpack_shard(host_file, rank, world, index=side)
+        if host_out is None:
+            host_out = torch.empty(r.out.numel(), dtype=torch.uint8, pin_memory=True)
+        host_out.copy_(r.out[: host_out.numel()])
+        torch.cuda.synchronize()
+        dt = allreduce_max(time.perf_counter() - t0, dev)
+        if i >= 1:
+            times.append(dt)
+    e2e_s = statistics.median(times)
+    return {"value": raw / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": len(host_file) + len(side),
+            "d2h_bytes_per_step": raw,
+            "api": f"sharded.unpack_shard(file bytes, rank, {world}, index=sidecar) on every rank + D2H of each "
+                   f"rank's decoded range (max over ranks)"}
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
@@ -441,9 +499,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_DIST_BACKEND=gloo + BENCH_ONE_GPU=1: every rank on cuda:0 (a
+    # functional check of the N > 1 path on a one-GPU box; never a measurement)
+    if os.environ.get("BENCH_ONE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     from paper_2502_15443_b200 import container, engine, native
@@ -453,15 +519,21 @@ def main():
     raw = pm.raw_bytes
     comp = pm.comp_bytes
     cr_file = raw / pm.file_bytes
-    unp = DeviceUnpack(pm, dev)
+    # N GPUs: one container, chunk-sharded (sharded.plan_shards): every rank
+    # unpacks only its contiguous chunk range -- strong scaling, no collective
+    # on the data path
+    from paper_2502_15443_b200 import sharded
+    shard = sharded.plan_shards(pm.entries, world)[rank]
+    unp = DeviceUnpack(pm, dev, chunks=(shard.c0, shard.c1))
     out = unp.out
+    r0, r1 = unp.range
 
     clocks = ClockSampler(local).__enter__()
     time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
     for _ in range(args.warmup):
         unp()
     torch.cuda.synchronize()
-    if int(unp.bad.item()) != 0 or not torch.equal(out, m.payload):
+    if int(unp.bad.item()) != 0 or not torch.equal(out[r0:r1], m.payload[r0:r1]):
         raise SystemExit("unpack mismatch: status / CRC verdicts or GPU output != encoder input")
     # the timed region; the dominant kernel's own duration is taken from events
     # around its launch inside every timed step (same stream)
@@ -470,19 +542,21 @@ def main():
     if int(unp.bad.item()) != 0:
         raise SystemExit("unpack verdicts changed inside the timed region")
     kms = unp.kernel_ms()
-    value = raw * world * args.steps / (ms / 1e3) / 1e9
+    value = raw * args.steps / (ms / 1e3) / 1e9  # the whole container per step, all ranks together
     hbm, peak_kind = peaks()
-    ans_raw = int(pm.entries["uncomp_len"][pm.entries["codec"] == 1].sum())
-    ans_comp = int(pm.entries["comp_len"][pm.entries["codec"] == 1].sum())
-    alg_bytes = ans_raw + ans_comp  # decompressed bytes written + compressed bytes read
+    alg_bytes = unp.ans_raw + unp.ans_comp  # this rank's decompressed bytes written + compressed bytes read
     achieved = alg_bytes / (kms / 1e3) / 1e9
 
+    full_status = torch.zeros(max(pm.jobs.n, 1), dtype=torch.int32, device=dev)
+
     def decode_only():
-        engine.decode_segments(pm.image, pm.jobs, pm.index, pm.tasks, out, unp.status)
+        engine.decode_segments(pm.image, pm.jobs, pm.index, pm.tasks, out, full_status)
         if unp.has_store:
             engine.store_copy(pm.image, pm.jobs, out)
 
-    tokens = decode_step_tokens(m, pm, out, dev, max(5, min(args.steps // 5, 20)), unfused_step=decode_only)
+    # decode-step tokens/s of the whole model on one GPU (N > 1: the TP key below)
+    tokens = (decode_step_tokens(m, pm, out, dev, max(5, min(args.steps // 5, 20)), unfused_step=decode_only)
+              if world == 1 else None)
     offs = m.offsets()[:-1]
 
     # GPU_CPU tier: weights in pinned host memory streamed over
@@ -577,40 +651,43 @@ def main():
     pin_file.numpy()[:] = np.frombuffer(host_file, np.uint8)
     pin_side = torch.empty(len(side), dtype=torch.uint8, pin_memory=True)
     pin_side.numpy()[:] = np.frombuffer(side, np.uint8)
-    e2e_times = []
-    e2e_phases = []
-    for i in range(args.e2e_steps + 2):  # 2 untimed: pinned output blocks get cached
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        bundle = container.unpack(pin_file, index=pin_side)
-        torch.cuda.synchronize()
-        if i >= 2:
-            e2e_times.append(time.perf_counter() - t0)
-            e2e_phases.append(dict(container.LAST_UNPACK_MS))
-    ok = bundle.tensors[0].qvalues.tobytes() == m.payload[: m.shapes[0][0] * m.shapes[0][1]].cpu().numpy().tobytes()
-    if not ok:
-        raise SystemExit("e2e mismatch")
-    e2e_s = statistics.median(e2e_times)
-    e2e = {"value": raw / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": len(host_file) + len(side),
-           "d2h_bytes_per_step": raw + 8 * pm.jobs.n,
-           "api": "container.unpack(pinned host file, index=pinned sidecar) -> host ModelBundle",
-           "phases_ms": {k: statistics.median(p[k] for p in e2e_phases) for k in e2e_phases[0]}}
-    del bundle
-    # the reference's exact call, unpack(file) with no sidecar: every chunk is one
-    # serial rANS chain on the GPU (no split points exist yet); one timed step
-    if not args.no_index_less:
-        container.clear_index_cache()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        b2 = container.unpack(pin_file)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        same = b2.tensors[-1].qvalues.tobytes() == m.payload[-m.shapes[-1][0] * m.shapes[-1][1]:].cpu().numpy().tobytes()
-        e2e["index_less"] = {"value": raw / dt / 1e9, "unit": "GB/s",
-                             "api": "container.unpack(pinned host file) -- no sidecar, first call", "seconds": dt,
-                             "equal": same}
-        del b2
-        container.clear_index_cache()
+    if world > 1:
+        e2e = sharded_e2e(args, host_file, side, raw, rank, world, dev)
+    else:
+        e2e_times = []
+        e2e_phases = []
+        for i in range(args.e2e_steps + 2):  # 2 untimed: pinned output blocks get cached
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            bundle = container.unpack(pin_file, index=pin_side)
+            torch.cuda.synchronize()
+            if i >= 2:
+                e2e_times.append(time.perf_counter() - t0)
+                e2e_phases.append(dict(container.LAST_UNPACK_MS))
+        ok = bundle.tensors[0].qvalues.tobytes() == m.payload[: m.shapes[0][0] * m.shapes[0][1]].cpu().numpy().tobytes()
+        if not ok:
+            raise SystemExit("e2e mismatch")
+        e2e_s = statistics.median(e2e_times)
+        e2e = {"value": raw / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": len(host_file) + len(side),
+               "d2h_bytes_per_step": raw + 8 * pm.jobs.n,
+               "api": "container.unpack(pinned host file, index=pinned sidecar) -> host ModelBundle",
+               "phases_ms": {k: statistics.median(p[k] for p in e2e_phases) for k in e2e_phases[0]}}
+        del bundle
+        # the reference's exact call, unpack(file) with no sidecar: every chunk is one
+        # serial rANS chain on the GPU (no split points exist yet); one timed step
+        if not args.no_index_less:
+            container.clear_index_cache()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            b2 = container.unpack(pin_file)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            same = b2.tensors[-1].qvalues.tobytes() == m.payload[-m.shapes[-1][0] * m.shapes[-1][1]:].cpu().numpy().tobytes()
+            e2e["index_less"] = {"value": raw / dt / 1e9, "unit": "GB/s",
+                                 "api": "container.unpack(pinned host file) -- no sidecar, first call", "seconds": dt,
+                                 "equal": same}
+            del b2
+            container.clear_index_cache()
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -630,11 +707,12 @@ def main():
     index_bytes = pm.index.nbytes
     file_bytes = pm.file_bytes
     launches_per_step = unp.launches
+    shard_bytes = unp.raw_bytes
     del unp, out, m, pm
     torch.cuda.empty_cache()
 
     extra = None
-    if args.extra_model != "none":
+    if args.extra_model != "none" and world == 1:
         try:
             m2, pm2, digest2, _ = build_packed(args, args.extra_model, dev)
             u2 = DeviceUnpack(pm2, dev)
@@ -659,18 +737,23 @@ def main():
         cfg.update({"seg_len": 1 << args.seg_shift, "n_chunks": n_chunks, "n_tasks": n_tasks,
                     "cr_resident": raw / (file_bytes + index_bytes), "index_bytes": index_bytes,
                     "l2": "inputs (compressed) and outputs exceed the 126 MB L2",
-                    "parallelism": f"dp{world} (replicas)", "build_s": t_build,
+                    "parallelism": (f"chunk-sharded over {world} GPUs (one container, contiguous chunk ranges "
+                                    f"balanced by decompressed bytes, no data-path collective)" if world > 1
+                                    else "single GPU"),
+                    "shard": {"chunks": [shard.c0, shard.c1], "decompressed_bytes": shard_bytes},
+                    "build_s": t_build,
                     "reference_arm": "bench.py --impl reference builds the same container from the same spec "
                                      "(same container_digest) and unpacks whole-layer samples of it"})
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": cfg,
-            "decode_kernel_gbs": raw / (kms / 1e3) / 1e9,
+            "decode_kernel_gbs": shard_bytes / (kms / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "kernel": "k_decode_segments", "achieved": achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "traffic_src": traffic_src, "alg_bytes_per_launch": alg_bytes, "launch_ms": kms,
-                         "frac_decompressed": raw / (kms / 1e3) / 1e9 / hbm,
+                         "frac_decompressed": shard_bytes / (kms / 1e3) / 1e9 / hbm,
                          # the decode is bound by instruction issue on the ALU pipe, not HBM
                          # (same ncu capture): see DESIGN.md "Why the decode is not at the HBM roofline"
                          "ncu_pipes": pipes},
