@@ -6,6 +6,11 @@ baseline.  A step runs every local linear for ``ntok`` tokens in one grouped
 launch (fused decode -> TMEM -> tcgen05, or the INT8 tcgen05 GEMM), then
 all-reduces each row-parallel layer's int32 partial outputs over NCCL
 (2 per transformer layer; exact integer sums).
+
+``graph(compressed)`` captures that whole step -- the one grouped GEMM
+launch and the row-parallel all-reduces (80 for LLaMA-13B) -- in ONE CUDA
+graph, so a decode step is a single graph launch instead of ~80 eager NCCL
+calls from Python.
 """
 
 from __future__ import annotations
@@ -62,6 +67,21 @@ class TPDecodeStep:
     def step(self, compressed: bool) -> None:
         self.compute(compressed)
         self.allreduce(compressed)
+
+    def graph(self, compressed: bool) -> torch.cuda.CUDAGraph:
+        """The step captured in a CUDA graph (warmed up on a side stream first,
+        as capture requires); replay() re-runs it on the same buffers."""
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                self.step(compressed)
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(compressed)
+        return g
 
     def check(self) -> bool:
         """Fused and INT8 paths give identical reduced outputs."""
@@ -123,6 +143,12 @@ def measure(step: TPDecodeStep, iters: int = 10) -> dict:
     for name, comp in (("int8", False), ("compressed_fused", True)):
         out[f"{name}_step_ms"] = timed(lambda: step.step(comp))
         out[f"{name}_compute_ms"] = timed(lambda: step.compute(comp))
+        try:  # the whole step (GEMM launch + every all-reduce) as one CUDA graph
+            g = step.graph(comp)
+            out[f"{name}_graph_step_ms"] = timed(g.replay)
+            del g
+        except Exception as e:  # report, never hide
+            out[f"{name}_graph_error"] = repr(e)[:200]
     out["allreduce_ms"] = timed(lambda: step.allreduce(True))
     out["allreduces_per_step"] = len(step.row_idx)
     out["local_weight_bytes"] = step.raw_bytes
