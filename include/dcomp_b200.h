@@ -205,6 +205,15 @@ int dc_quantize(const void *w, int dtype, const double *s, int64_t rows, int64_t
 int dc_dequantize(const int8_t *q, double w_scale, const double *s, int64_t rows, int64_t cols, double *out,
                   void *stream);
 
+/* W8A8 activation prologue (scaling.py:143-149 on decode activations): for each
+ * of n_tensors records {const void *x; const double *s; int8_t *q; double *sx;
+ * int64_t k} (dc_act_quant_bytes() each, device array): X' = X / s (IEEE f64),
+ * *sx = max|X'| / 127, q = clip(sign * floor(|X'| / sx + 0.5), +-127) over
+ * [ntok][k] activations of `dtype` (as dc_quantize).  status[i] (zeroed by
+ * the caller) = 1 non-finite input, 2 zero dynamic range (q = 0, sx = 0). */
+int dc_act_quant_bytes(void);
+int dc_act_quant(const void *tensors, int n_tensors, int dtype, int64_t ntok, int32_t *status, void *stream);
+
 /* Calibration statistics: acc_bits[c] = max(acc_bits[c], bits(|x[r, c]| as f64))
  * over rows x cols activations x (dtype as dc_quantize), i.e. a running
  * per-input-channel max|x| kept as f64 bit patterns (zero-initialise once).
@@ -270,7 +279,8 @@ int dc_w8a8_grouped_persist(const void *maps, const void *tens, const int32_t *u
  * weights decoded by ans.py:71-94. */
 int dc_fused_item_rows(void);
 int dc_fused_item_k(void);
-/* `epi` (nullable): per layer {float *y; uint32_t *cnt; float scale; int32 n_slices}
+/* `epi` (nullable): per layer {float *y; uint32_t *cnt; float scale; int32 n_slices;
+ * const double *sx; double sw} -- y = acc * (sx ? (float)(*sx * sw) : scale)
  * (dc_fused_epi_bytes() each): the fused dequant epilogue y = acc * scale written
  * by the last K-slice item of each 1024-row block (cnt zeroed before first use).
  * `max_ctas` > 0 caps the persistent grid (one CTA per SM) so a concurrent INT8

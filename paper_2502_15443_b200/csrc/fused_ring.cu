@@ -40,8 +40,10 @@ struct GemmTensorR {  // identical layout to GemmTensor (gemm_grouped.cu)
 struct RingEpi {
     float* y;          // fp32 [ntok, n_rows] or null (int32 accumulators only)
     uint32_t* cnt;     // per 1024-row block: items finished (zero between launches)
-    float scale;
+    float scale;       // sx * sw when sx is null
     int32_t n_slices;  // K-slices per row block
+    const double* sx;  // device activation scale (dc_act_quant) or null
+    double sw;         // weight scale: y = acc * (float)(sx * sw)
 };
 
 constexpr int kRDec = 16;                     // decoder warps
@@ -490,10 +492,11 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
             if (S.last) {
                 __threadfence();
                 const int rows = min(kRTiles * 128, T.n_rows - m0);
+                const float scale = E.sx ? (float)(*E.sx * E.sw) : E.scale;
                 for (int i = threadIdx.x; i < rows * ntok; i += kRThreads) {
                     const int t = i / rows, r = m0 + i % rows;
                     const int32_t a = __ldcg(&T.acc[(int64_t)t * T.n_rows + r]);
-                    E.y[(int64_t)t * T.n_rows + r] = (float)a * E.scale;
+                    E.y[(int64_t)t * T.n_rows + r] = (float)a * scale;
                 }
                 if (threadIdx.x == 0) E.cnt[blk] = 0;  // ready for the next launch
             }

@@ -308,6 +308,84 @@ __global__ void __launch_bounds__(kQThreads) k_channel_absmax(const typename In<
 }
 }  // namespace dc
 
+namespace dc {
+// W8A8 activation prologue (scaling.py:143-149 applied to a decode step's
+// activations): X' = X / s (per input channel, IEEE f64 division), one
+// per-tensor symmetric quantization of X' exactly as the weights'
+// (w_scale = max|X'| / 127, q = clip(sign * floor(|X'| / sx + 0.5))).  One
+// CTA per activation tensor (decode-sized: ntok x K <= a few MB): a block
+// max-reduction, then the quantize pass from the same (L1/L2-hot) data.
+struct ActQ {
+    const void* x;      // [ntok][k] in dtype
+    const double* s;    // [k] channel scales (null = identity)
+    int8_t* q;          // [ntok][k] out
+    double* sx;         // out: per-tensor activation scale (0 when X' == 0)
+    int64_t k;
+};
+
+template <int T>
+__global__ void __launch_bounds__(1024) k_act_quant(const ActQ* __restrict__ t, int64_t ntok,
+                                                     int32_t* __restrict__ status) {
+    const ActQ a = t[blockIdx.x];
+    const auto* x = static_cast<const typename In<T>::type*>(a.x);
+    const int64_t n = ntok * a.k;
+    double m = 0.0;
+    bool bad = false;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = In<T>::f64(x[i]);
+        bad |= !isfinite(v);
+        const double d = fabs(a.s ? __ddiv_rn(v, a.s[i % a.k]) : v);
+        m = d > m ? d : m;
+    }
+    __shared__ double red[32];
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, m, d);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    const int anybad = __syncthreads_or(bad);
+    if (threadIdx.x < 32) {
+        double b = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            const double o = __shfl_xor_sync(0xffffffffu, b, d);
+            b = o > b ? o : b;
+        }
+        if (threadIdx.x == 0) red[0] = b;
+    }
+    __syncthreads();
+    const double sx = red[0] / 127.0;  // scaling.py:102
+    if (threadIdx.x == 0) {
+        *a.sx = sx;
+        if (anybad) status[blockIdx.x] = 1;       // non-finite activations
+        else if (sx == 0.0) status[blockIdx.x] = 2;  // zero dynamic range (q = 0)
+    }
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = In<T>::f64(x[i]);
+        a.q[i] = sx == 0.0 ? (int8_t)0 : q_of(a.s ? __ddiv_rn(v, a.s[i % a.k]) : v, sx);
+    }
+}
+}  // namespace dc
+
+extern "C" int dc_act_quant_bytes(void) { return (int)sizeof(ActQ); }
+
+extern "C" int dc_act_quant(const void* tensors, int n_tensors, int dtype, int64_t ntok, int32_t* status,
+                            void* stream) {
+    if (n_tensors < 0 || ntok < 0 || dtype < 0 || dtype > 3) return DC_ERR_ARG;
+    if (n_tensors == 0 || ntok == 0) return DC_OK;
+    const auto* t = static_cast<const ActQ*>(tensors);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (dtype) {
+        case kF64: k_act_quant<kF64><<<n_tensors, 1024, 0, st>>>(t, ntok, status); break;
+        case kF32: k_act_quant<kF32><<<n_tensors, 1024, 0, st>>>(t, ntok, status); break;
+        case kBF16: k_act_quant<kBF16><<<n_tensors, 1024, 0, st>>>(t, ntok, status); break;
+        default: k_act_quant<kF16><<<n_tensors, 1024, 0, st>>>(t, ntok, status); break;
+    }
+    DC_CHECK_LAUNCH("k_act_quant");
+    return DC_OK;
+}
+
 extern "C" int dc_channel_absmax(const void* x, int dtype, int64_t rows, int64_t cols, uint64_t* acc_bits,
                                  void* stream) {
     if (rows < 0 || cols < 0 || dtype < 0 || dtype > 3) return DC_ERR_ARG;

@@ -165,8 +165,52 @@ __device__ __forceinline__ FmaK fma_consts(uint32_t one) {
 // Slot address without the ALU mask: with t = (x >> 12) - 4096 (needed for the
 // state update anyway), tab + 4*(x & 4095) = (tab - 2^26) + 4x - 16384 t: two
 // IMADs on the FMA pipe instead of LOP3 + IMAD.  `tabm` = tab - 2^26.
+#ifndef DC_DEC_VARIANT
+#define DC_DEC_VARIANT 0
+#endif
 __device__ __forceinline__ uint32_t dec_sym_fa(uint32_t& x, uint32_t& s, uint32_t v, uint32_t tabm, const FmaK& k) {
     uint32_t e;
+#if DC_DEC_VARIANT == 1  // f and b extraction on the FMA pipe (IMAD.HI by 2^12 / 2^24)
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
+        "shr.u32 t, %0, 12;\n\t"
+        "sub.u32 t, t, 4096;\n\t"
+        "mad.lo.u32 a, %0, %5, %4;\n\t"
+        "mad.lo.u32 a, t, %6, a;\n\t"
+        "ld.shared.u32 %2, [a];\n\t"
+        "mul.hi.u32 f, %2, %7;\n\t"
+        "mul.hi.u32 b, %2, %8;\n\t"
+        "mad.lo.u32 %0, f, t, b;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q prmt.b32 %0, %0, %3, %1;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q prmt.b32 %0, %0, %3, %1;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t}"
+        : "+r"(x), "+r"(s), "=r"(e)
+        : "r"(v), "r"(tabm), "r"(k.c4), "r"(k.cm16384), "r"(k.c2p12), "r"(k.c2p24));
+    return e;
+#elif DC_DEC_VARIANT == 2  // b on the FMA pipe only
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
+        "shr.u32 t, %0, 12;\n\t"
+        "sub.u32 t, t, 4096;\n\t"
+        "mad.lo.u32 a, %0, %5, %4;\n\t"
+        "mad.lo.u32 a, t, %6, a;\n\t"
+        "ld.shared.u32 %2, [a];\n\t"
+        "shr.u32 f, %2, 20;\n\t"
+        "mul.hi.u32 b, %2, %7;\n\t"
+        "mad.lo.u32 %0, f, t, b;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q prmt.b32 %0, %0, %3, %1;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t"
+        "setp.lt.u32 q, %0, 0x100000;\n\t"
+        "@q prmt.b32 %0, %0, %3, %1;\n\t"
+        "@q add.u32 %1, %1, 1;\n\t}"
+        : "+r"(x), "+r"(s), "=r"(e)
+        : "r"(v), "r"(tabm), "r"(k.c4), "r"(k.cm16384), "r"(k.c2p24));
+    return e;
+#endif
     asm volatile(
         "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
         "shr.u32 t, %0, 12;\n\t"
@@ -242,6 +286,28 @@ __device__ __forceinline__ void win_advance(Win& w, uint32_t s, const FmaK& k) {
         : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
         : "r"(s), "r"(k.c1));
 }
+
+// Fast-path advance for pair J (0..7) of a 16-symbol group.  o is not
+// re-biased per pair: it carries the selector bias of the J+1 pairs so far
+// (8 * kSelBase = 0x10820 each, a multiple of 32, so SHF.R.W's shift amount
+// o mod 32 is unaffected), the crossing test compares against a per-pair
+// immediate, and win_rebase() removes the 8 pairs' bias once per group.  The
+// word move is one SEL plus a predicated LDS and two predicated adds (no
+// if-converted IMAD/SEL pairs): 6 instructions per pair instead of 9.
+template <int J>
+__device__ __forceinline__ void win_advance_g(Win& w, uint32_t s) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "mad.lo.u32 %3, %4, 8, %3;\n\t"
+        "setp.ge.u32 q, %3, %5;\n\t"
+        "selp.b32 %0, %1, %0, q;\n\t"
+        "@q ld.shared.u32 %1, [%2+4];\n\t"
+        "@q add.u32 %2, %2, 4;\n\t"
+        "@q add.u32 %3, %3, -32;\n\t}"
+        : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
+        : "r"(s), "n"(32u + (J + 1) * 0x10820u));
+}
+__device__ __forceinline__ void win_rebase(Win& w) { w.o -= 8u * 0x10820u; }
 
 // Same inside a 128-byte ring (fused kernel): the word address wraps.
 __device__ __forceinline__ void win_advance_ring(Win& w, uint32_t s) {

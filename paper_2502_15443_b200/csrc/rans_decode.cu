@@ -348,9 +348,19 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
                     const uint32_t t = __byte_perm(e0[u], dec_sym_fa(x[u], sel[u], wv[u], tabm, fk), 0x0040);
                     w[u][v >> 2] = (v & 2) ? __byte_perm(w[u][v >> 2], t, 0x5410) : t;
                 }
-#pragma unroll
-                for (int u = 0; u < NU; ++u) win_advance(W[u], sel[u], fk);
+                switch (v >> 1) {  // compile-time after unrolling
+                    case 0: for (int u = 0; u < NU; ++u) win_advance_g<0>(W[u], sel[u]); break;
+                    case 1: for (int u = 0; u < NU; ++u) win_advance_g<1>(W[u], sel[u]); break;
+                    case 2: for (int u = 0; u < NU; ++u) win_advance_g<2>(W[u], sel[u]); break;
+                    case 3: for (int u = 0; u < NU; ++u) win_advance_g<3>(W[u], sel[u]); break;
+                    case 4: for (int u = 0; u < NU; ++u) win_advance_g<4>(W[u], sel[u]); break;
+                    case 5: for (int u = 0; u < NU; ++u) win_advance_g<5>(W[u], sel[u]); break;
+                    case 6: for (int u = 0; u < NU; ++u) win_advance_g<6>(W[u], sel[u]); break;
+                    default: for (int u = 0; u < NU; ++u) win_advance_g<7>(W[u], sel[u]); break;
+                }
             }
+#pragma unroll
+            for (int u = 0; u < NU; ++u) win_rebase(W[u]);
         } else {
 #pragma unroll
             for (int u = 0; u < NU; ++u) w[u][0] = w[u][1] = w[u][2] = w[u][3] = 0;
