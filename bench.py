@@ -447,13 +447,31 @@ def decode_step_tokens(m, pm, out, dev, iters, batches=(1, 16), unfused_step=Non
         t_fu = time_ms(fc.run, iters)
         row = {"int8_tok_s": B / (t_i8 / 1e3), "compressed_fused_tok_s": B / (t_fu / 1e3), "int8_ms": t_i8,
                "fused_ms": t_fu, "fused_vs_int8": t_i8 / t_fu, "int8_weight_gbs": raw / (t_i8 / 1e3) / 1e9}
+        del fc
+        # the full W8A8 layer path from fp32 activations in one call: prologue
+        # (X / s, per-tensor absmax, int8) + fused decode -> tcgen05 + dequant epilogue
+        try:
+            from paper_2502_15443_b200.gemm import CompressedLinears
+            cl = CompressedLinears(pm.image, pm.jobs, pm.index, pm.chunk_size, m.shapes, offs, m.w_scales,
+                                   [s.cpu().numpy() for s in m.s], B)
+            for xb in cl.x_in:
+                xb.normal_(generator=gx)
+            cl.run()
+            torch.cuda.synchronize()
+            if (cl.check() != 0).any():
+                raise RuntimeError("fp-activation path chain check failed")
+            t_fp = time_ms(cl.run, iters)
+            row.update({"compressed_fp_act_tok_s": B / (t_fp / 1e3), "fp_act_ms": t_fp})
+            del cl
+        except Exception as e:  # report, never hide
+            row["fp_act_error"] = repr(e)[:200]
         if unfused_step is not None:
             gd = GroupedInt8(w_dec, xs, B)
             t_un = time_ms(lambda: (unfused_step(), gd.run()), iters)
             row.update({"compressed_unfused_tok_s": B / (t_un / 1e3), "unfused_ms": t_un})
             del gd
         tokens[f"B{B}"] = row
-        del gi, fc
+        del gi
     return tokens
 
 

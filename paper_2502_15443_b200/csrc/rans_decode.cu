@@ -68,6 +68,60 @@ __global__ void k_validate(const uint8_t* __restrict__ base, const uint64_t* __r
 }
 
 // ------------------------------------------------------------- serial decode
+// One latency-shortened symbol step for the serial chain.  `e` is the table
+// entry of the current state (loaded during the previous step).  The next
+// state's slot is one of three candidates -- no refill (xn & 4095), one
+// refill ((xn & 15) << 8 | b0) or two refills ((b0 & 15) << 8 | b1, which
+// does not depend on xn at all) -- so all three table entries are loaded
+// right after xn = f*t + b is known and the refill compares / PRMTs run in
+// parallel with the loads; the right entry is selected afterwards.  Critical
+// path per symbol: IMAD, LOP + IMAD, LDS, two SEL, SHF (the refills and the
+// next t are off it).  Returns the symbol (low byte of the old entry).
+__device__ __forceinline__ uint32_t serial_step(uint32_t& x, uint32_t& e, uint32_t& s, uint32_t v, uint32_t tab) {
+    const uint32_t sym = e;
+    // written as one asm block so the three loads stay unconditional (issued
+    // as soon as their addresses exist) and only the selection waits on the
+    // refill compares; ptxas would otherwise turn the selects into
+    // predicated loads into one register, serialising them behind the compare.
+    asm volatile(
+        "{\n\t.reg .pred p1, p2;\n\t.reg .u32 f, b, t, xn, y2, b0, a0, a1, a2, e0, e1, e2, r1, r2, k;\n\t"
+        "shr.u32 f, %1, 20;\n\t"
+        "shr.u32 b, %1, 8;\n\t"
+        "shr.u32 t, %0, 12;\n\t"
+        "sub.u32 t, t, 4096;\n\t"
+        "mad.lo.u32 xn, f, t, b;\n\t"                 // f*(x>>12) + slot - cum (mod 2^32)
+        "mad.lo.u32 k, %2, 17, %5;\n\t"              // selector of (b0 << 8 | b1)
+        "prmt.b32 y2, %3, 0, k;\n\t"
+        "add.u32 k, %2, %6;\n\t"                      // selector of b0 (zero-extended)
+        "prmt.b32 b0, %3, 0, k;\n\t"
+        "and.b32 a2, y2, 4095;\n\t"
+        "mad.lo.u32 a2, a2, 4, %4;\n\t"               // two refills: slot (b0 & 15) << 8 | b1
+        "mad.lo.u32 b0, b0, 4, %4;\n\t"
+        "and.b32 a0, xn, 4095;\n\t"
+        "mad.lo.u32 a0, a0, 4, %4;\n\t"               // no refill: slot xn & 4095
+        "and.b32 a1, xn, 15;\n\t"
+        "mad.lo.u32 a1, a1, 1024, b0;\n\t"            // one refill: slot (xn & 15) << 8 | b0
+        "ld.shared.u32 e2, [a2];\n\t"
+        "ld.shared.u32 e0, [a0];\n\t"
+        "ld.shared.u32 e1, [a1];\n\t"
+        "setp.lt.u32 p1, xn, 0x100000;\n\t"
+        "setp.lt.u32 p2, xn, 4096;\n\t"
+        "prmt.b32 r1, xn, %3, %2;\n\t"
+        "add.u32 k, %2, 1;\n\t"
+        "prmt.b32 r2, r1, %3, k;\n\t"
+        "selp.b32 r1, r2, r1, p2;\n\t"
+        "selp.b32 %0, r1, xn, p1;\n\t"
+        "selp.b32 e1, e2, e1, p2;\n\t"
+        "selp.b32 %1, e1, e0, p1;\n\t"
+        "selp.b32 k, 1, 0, p1;\n\t"
+        "add.u32 %2, %2, k;\n\t"
+        "selp.b32 k, 1, 0, p2;\n\t"
+        "add.u32 %2, %2, k;\n\t}"
+        : "+r"(x), "+r"(e), "+r"(s)
+        : "r"(v), "r"(tab), "n"(0x4401u - 17u * kSelBase), "n"(0x4440u - kSelBase));
+    return sym;
+}
+
 // One CTA per chunk: the whole CTA builds the table, then one thread walks
 // the stream exactly as the reference does.  That walk is a serial
 // recurrence, so its speed is its dependency chain: the stream is staged into
@@ -179,34 +233,51 @@ __global__ void __launch_bounds__(kSerialThreads) k_decode_serial(
         uint32_t x = x0;
         bool bad = false;
         uint64_t j = 0;
-        while (j < n) {
-            // refill: a 16-symbol group reads at most 32 bytes (+ the 8-byte window)
-            const uint64_t rp = rpos();
-            wait_upto((rp + 40) / kSerSlot);
-            issue_upto(rp / kSerSlot + 4);
+        // one 16-symbol group (split point recorded at segment starts)
+        auto group16 = [&]() {
             if (seg_state && (j & (K - 1)) == 0) {
                 seg_state[sb + (j >> seg_shift)] = x;
-                seg_off[sb + (j >> seg_shift)] = (uint32_t)(rp - delta);
+                seg_off[sb + (j >> seg_shift)] = (uint32_t)(rpos() - delta);
             }
-            if (j + 16 <= n) {
-                uint32_t w[4];
+            uint32_t w[4];
+            uint32_t e = lds_u32(tab + 4u * (x & 4095u));  // entry of the current state
 #pragma unroll
-                for (int v = 0; v < 16; v += 2) {
-                    uint32_t vb, sel = kSelBase;
-                    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(vb) : "r"(w0), "r"(w1), "r"(ob));
-                    const uint32_t e0 = dec_sym(x, sel, vb, tab);
-                    const uint32_t t = __byte_perm(e0, dec_sym(x, sel, vb, tab), 0x0040);
-                    w[v >> 2] = (v & 2) ? __byte_perm(w[v >> 2], t, 0x5410) : t;
-                    advance(sel);
-                }
-                if (oal) {
-                    *reinterpret_cast<uint4*>(o + j) = make_uint4(w[0], w[1], w[2], w[3]);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) o[j + k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
-                }
-                j += 16;
+            for (int v = 0; v < 16; v += 2) {
+                uint32_t vb, sel = kSelBase;
+                asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(vb) : "r"(w0), "r"(w1), "r"(ob));
+                const uint32_t e0 = serial_step(x, e, sel, vb, tab);
+                const uint32_t t = __byte_perm(e0, serial_step(x, e, sel, vb, tab), 0x0040);
+                w[v >> 2] = (v & 2) ? __byte_perm(w[v >> 2], t, 0x5410) : t;
+                advance(sel);
+            }
+            if (oal) {
+                *reinterpret_cast<uint4*>(o + j) = make_uint4(w[0], w[1], w[2], w[3]);
             } else {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) o[j + k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+            }
+            j += 16;
+        };
+        while (j < n) {
+            // ring: a block of g groups reads at most 32 g bytes (+ the 8-byte window);
+            // the waits and issues are done once per 64 symbols
+            const uint64_t rp = rpos();
+            const uint64_t left = n - j;
+            const int groups = left >= 64 ? 4 : (left >= 16 ? 1 : 0);
+            wait_upto((rp + 32 * (uint64_t)(groups ? groups : 1) + 8) / kSerSlot);
+            issue_upto(rp / kSerSlot + 4);
+            if (groups == 4) {
+                group16();
+                group16();
+                group16();
+                group16();
+            } else if (groups == 1) {
+                group16();
+            } else {
+                if (seg_state && (j & (K - 1)) == 0) {
+                    seg_state[sb + (j >> seg_shift)] = x;
+                    seg_off[sb + (j >> seg_shift)] = (uint32_t)(rp - delta);
+                }
                 for (; j < n; ++j) {
                     uint32_t vb, sel = kSelBase;
                     asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(vb) : "r"(w0), "r"(w1), "r"(ob));
