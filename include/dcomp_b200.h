@@ -207,12 +207,15 @@ int dc_dequantize(const int8_t *q, double w_scale, const double *s, int64_t rows
 
 /* W8A8 activation prologue (scaling.py:143-149 on decode activations): for each
  * of n_tensors records {const void *x; const double *s; int8_t *q; double *sx;
- * int64_t k} (dc_act_quant_bytes() each, device array): X' = X / s (IEEE f64),
- * *sx = max|X'| / 127, q = clip(sign * floor(|X'| / sx + 0.5), +-127) over
- * [ntok][k] activations of `dtype` (as dc_quantize).  status[i] (zeroed by
- * the caller) = 1 non-finite input, 2 zero dynamic range (q = 0, sx = 0). */
+ * double *xp; uint64_t *mbits; int64_t k} (dc_act_quant_bytes() each, device
+ * array; xp = [ntok][k] f64 scratch, *mbits zeroed by the caller): X' = X / s
+ * (IEEE f64), *sx = max|X'| / 127, q = clip(sign * floor(|X'| / sx + 0.5), +-127)
+ * over [ntok][k] activations of `dtype` (as dc_quantize); max_k >= every k.
+ * status[i] (zeroed by the caller) = 1 non-finite input, 2 zero dynamic range
+ * (q = 0, sx = 0).  Two launches (scale + max, then round), all tensors each. */
 int dc_act_quant_bytes(void);
-int dc_act_quant(const void *tensors, int n_tensors, int dtype, int64_t ntok, int32_t *status, void *stream);
+int dc_act_quant(const void *tensors, int n_tensors, int dtype, int64_t ntok, int64_t max_k, int32_t *status,
+                 void *stream);
 
 /* Calibration statistics: acc_bits[c] = max(acc_bits[c], bits(|x[r, c]| as f64))
  * over rows x cols activations x (dtype as dc_quantize), i.e. a running

@@ -320,69 +320,75 @@ struct ActQ {
     const double* s;    // [k] channel scales (null = identity)
     int8_t* q;          // [ntok][k] out
     double* sx;         // out: per-tensor activation scale (0 when X' == 0)
+    double* xp;         // scratch [ntok][k] f64: X' = X / s
+    uint64_t* mbits;    // scratch: max|X'| as f64 bits (zeroed by the caller)
     int64_t k;
 };
 
+// pass 1 (grid x = tensors, y = slices): X' = X / s into the scratch, running max
 template <int T>
-__global__ void __launch_bounds__(1024) k_act_quant(const ActQ* __restrict__ t, int64_t ntok,
-                                                     int32_t* __restrict__ status) {
+__global__ void __launch_bounds__(256) k_act_scale(const ActQ* __restrict__ t, int64_t ntok,
+                                                   int32_t* __restrict__ status) {
     const ActQ a = t[blockIdx.x];
     const auto* x = static_cast<const typename In<T>::type*>(a.x);
     const int64_t n = ntok * a.k;
     double m = 0.0;
     bool bad = false;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.y * blockDim.x) {
         const double v = In<T>::f64(x[i]);
         bad |= !isfinite(v);
-        const double d = fabs(a.s ? __ddiv_rn(v, a.s[i % a.k]) : v);
-        m = d > m ? d : m;
+        const double d = a.s ? __ddiv_rn(v, a.s[i % a.k]) : v;
+        a.xp[i] = d;
+        const double ad = fabs(d);
+        m = ad > m ? ad : m;
     }
-    __shared__ double red[32];
 #pragma unroll
     for (int d = 16; d; d >>= 1) {
         const double o = __shfl_xor_sync(0xffffffffu, m, d);
         m = o > m ? o : m;
     }
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    const int anybad = __syncthreads_or(bad);
-    if (threadIdx.x < 32) {
-        double b = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-#pragma unroll
-        for (int d = 16; d; d >>= 1) {
-            const double o = __shfl_xor_sync(0xffffffffu, b, d);
-            b = o > b ? o : b;
-        }
-        if (threadIdx.x == 0) red[0] = b;
-    }
-    __syncthreads();
-    const double sx = red[0] / 127.0;  // scaling.py:102
-    if (threadIdx.x == 0) {
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax((unsigned long long*)a.mbits, (unsigned long long)__double_as_longlong(m));
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(&status[blockIdx.x], 1);  // non-finite activations
+}
+
+// pass 2: sx = max / 127 (scaling.py:102), q = round-half-away(X' / sx) clipped
+__global__ void __launch_bounds__(256) k_act_round(const ActQ* __restrict__ t, int64_t ntok,
+                                                   int32_t* __restrict__ status) {
+    const ActQ a = t[blockIdx.x];
+    const double sx = __longlong_as_double((long long)*a.mbits) / 127.0;
+    const int64_t n = ntok * a.k;
+    if (blockIdx.y == 0 && threadIdx.x == 0) {
         *a.sx = sx;
-        if (anybad) status[blockIdx.x] = 1;       // non-finite activations
-        else if (sx == 0.0) status[blockIdx.x] = 2;  // zero dynamic range (q = 0)
+        if (sx == 0.0 && status[blockIdx.x] == 0) status[blockIdx.x] = 2;  // zero dynamic range (q = 0)
     }
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const double v = In<T>::f64(x[i]);
-        a.q[i] = sx == 0.0 ? (int8_t)0 : q_of(a.s ? __ddiv_rn(v, a.s[i % a.k]) : v, sx);
-    }
+    const double inv = sx == 0.0 ? 0.0 : 1.0 / sx;
+    for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.y * blockDim.x)
+        a.q[i] = sx == 0.0 ? (int8_t)0 : q_of_fast(a.xp[i], sx, inv);
 }
 }  // namespace dc
 
 extern "C" int dc_act_quant_bytes(void) { return (int)sizeof(ActQ); }
 
-extern "C" int dc_act_quant(const void* tensors, int n_tensors, int dtype, int64_t ntok, int32_t* status,
-                            void* stream) {
-    if (n_tensors < 0 || ntok < 0 || dtype < 0 || dtype > 3) return DC_ERR_ARG;
+extern "C" int dc_act_quant(const void* tensors, int n_tensors, int dtype, int64_t ntok, int64_t max_k,
+                            int32_t* status, void* stream) {
+    if (n_tensors < 0 || ntok < 0 || max_k < 0 || dtype < 0 || dtype > 3) return DC_ERR_ARG;
     if (n_tensors == 0 || ntok == 0) return DC_OK;
     const auto* t = static_cast<const ActQ*>(tensors);
     cudaStream_t st = (cudaStream_t)stream;
+    // slices per tensor: ~8 elements per thread per slice, grid <= 8 CTAs per SM in total
+    int64_t slices = (ntok * max_k + 256 * 8 - 1) / (256 * 8);
+    const int64_t cap = ((int64_t)sm_count() * 8 + n_tensors - 1) / n_tensors;
+    slices = slices < 1 ? 1 : (slices > cap ? (cap < 1 ? 1 : cap) : slices);
+    dim3 grid((unsigned)n_tensors, (unsigned)slices);
     switch (dtype) {
-        case kF64: k_act_quant<kF64><<<n_tensors, 1024, 0, st>>>(t, ntok, status); break;
-        case kF32: k_act_quant<kF32><<<n_tensors, 1024, 0, st>>>(t, ntok, status); break;
-        case kBF16: k_act_quant<kBF16><<<n_tensors, 1024, 0, st>>>(t, ntok, status); break;
-        default: k_act_quant<kF16><<<n_tensors, 1024, 0, st>>>(t, ntok, status); break;
+        case kF64: k_act_scale<kF64><<<grid, 256, 0, st>>>(t, ntok, status); break;
+        case kF32: k_act_scale<kF32><<<grid, 256, 0, st>>>(t, ntok, status); break;
+        case kBF16: k_act_scale<kBF16><<<grid, 256, 0, st>>>(t, ntok, status); break;
+        default: k_act_scale<kF16><<<grid, 256, 0, st>>>(t, ntok, status); break;
     }
-    DC_CHECK_LAUNCH("k_act_quant");
+    DC_CHECK_LAUNCH("k_act_scale");
+    k_act_round<<<grid, 256, 0, st>>>(t, ntok, status);
+    DC_CHECK_LAUNCH("k_act_round");
     return DC_OK;
 }
 

@@ -449,13 +449,18 @@ class CompressedLinears:
         self.s = [None if s is None else torch.from_numpy(np.ascontiguousarray(s, dtype=np.float64)).to(dev)
                   for s in s_vecs]
         self.act_status = torch.zeros(max(len(self.shapes), 1), dtype=torch.int32, device=dev)
-        dt = np.dtype([("x", "<u8"), ("s", "<u8"), ("q", "<u8"), ("sx", "<u8"), ("k", "<i8")])
+        self.xp = [torch.empty((ntok, k), dtype=torch.float64, device=dev) for _, k in self.shapes]
+        self.mbits = torch.zeros(max(len(self.shapes), 1), dtype=torch.int64, device=dev)
+        dt = np.dtype([("x", "<u8"), ("s", "<u8"), ("q", "<u8"), ("sx", "<u8"), ("xp", "<u8"), ("mbits", "<u8"),
+                       ("k", "<i8")])
         assert dt.itemsize == nv.call("dc_act_quant_bytes")
         t = np.zeros(len(self.shapes), dtype=dt)
         t["x"] = [x.data_ptr() for x in self.x_in]
         t["s"] = [0 if s is None else s.data_ptr() for s in self.s]
         t["q"] = [q.data_ptr() for q in self.qx]
         t["sx"] = [self.sx.data_ptr() + 8 * i for i in range(len(self.shapes))]
+        t["xp"] = [x.data_ptr() for x in self.xp]
+        t["mbits"] = [self.mbits.data_ptr() + 8 * i for i in range(len(self.shapes))]
         t["k"] = [k for _, k in self.shapes]
         self.table = torch.from_numpy(t.view(np.uint8).copy()).to(dev)
         self.ring = FusedRing(image, jobs, index, chunk_size, self.shapes, t_offs, self.qx, ntok,
@@ -463,8 +468,9 @@ class CompressedLinears:
 
     def prologue(self) -> None:
         self.act_status.zero_()
+        self.mbits.zero_()
         nv.call("dc_act_quant", self.table.data_ptr(), len(self.shapes), self._DT[self.dtype], self.ntok,
-                self.act_status.data_ptr(), nv.stream_ptr())
+                max(k for _, k in self.shapes), self.act_status.data_ptr(), nv.stream_ptr())
 
     def run(self, xs=None, max_ctas: int = 0) -> list[torch.Tensor]:
         """(Copies ``xs`` into the static input buffers, then) prologue + fused

@@ -60,7 +60,7 @@ SIGNATURES: dict[str, list] = {
     "dc_crc32_ranges": [_P, _U64, _P, _P, _I64, _U64, _P, _P],
     "dc_channel_absmax": [_P, ctypes.c_int, _I64, _I64, _P, _P],
     "dc_act_quant_bytes": [],
-    "dc_act_quant": [_P, ctypes.c_int, ctypes.c_int, _I64, _P, _P],
+    "dc_act_quant": [_P, ctypes.c_int, ctypes.c_int, _I64, _I64, _P, _P],
     "dc_hist_chunks": [_P, _U64, _U64, _I64, _P, _P],
     "dc_normalize_tables": [_P, _I64, _P, _P, _P],
     "dc_ans_encode_chunks": [_P, _U64, _U64, _I64, _P, _P, _P, _P, _P, _U32, _P, _P, _P, _U32, _P, _U64, _P],
