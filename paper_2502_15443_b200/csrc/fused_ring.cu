@@ -185,6 +185,26 @@ __device__ __forceinline__ void fwin_advance(Chain& c, uint32_t s) {
         : "r"(c.rb), "r"(s));
 }
 
+// Fast-path advance for pair J (0..7) of a 16-symbol group, as
+// win_advance_g (rans_common.cuh): o carries the J+1 pairs' selector bias
+// (multiples of 32), the crossing test uses a per-pair immediate, the word
+// move is SEL + predicated add / LDS; fwin_rebase() once per group.
+template <int J>
+__device__ __forceinline__ void fwin_advance_g(Chain& c, uint32_t s) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 a;\n\t"
+        "mad.lo.u32 %3, %5, 8, %3;\n\t"
+        "setp.ge.u32 q, %3, %6;\n\t"
+        "selp.b32 %0, %1, %0, q;\n\t"
+        "@q add.u32 %2, %2, 4;\n\t"
+        "lop3.b32 a, %2, 127, %4, 0xEA;\n\t"
+        "@q ld.shared.u32 %1, [a];\n\t"
+        "@q add.u32 %3, %3, -32;\n\t}"
+        : "+r"(c.w0), "+r"(c.w1), "+r"(c.pr), "+r"(c.o)
+        : "r"(c.rb), "r"(s), "n"(32u + (J + 1) * 0x10820u));
+}
+__device__ __forceinline__ void fwin_rebase(Chain& c) { c.o -= 8u * 0x10820u; }
+
 // fwin_advance with the moves and the offset wrap on the FMA pipe (see
 // win_advance(Win&, s, FmaK) in rans_common.cuh)
 __device__ __forceinline__ void fwin_advance(Chain& c, uint32_t s, const FmaK& k) {
@@ -391,9 +411,19 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
                                 e0[u], dec_sym_fa(ch[u].x, sel[u], wv[u], ch[u].tab - (1u << 26), fk), 0x0040);
                             w[u][v >> 2] = (v & 2) ? __byte_perm(w[u][v >> 2], t, 0x5410) : t;
                         }
-#pragma unroll
-                        for (int u = 0; u < 2; ++u) fwin_advance(ch[u], sel[u], fk);
+                        switch (v >> 1) {  // compile-time after unrolling
+                            case 0: for (int u = 0; u < 2; ++u) fwin_advance_g<0>(ch[u], sel[u]); break;
+                            case 1: for (int u = 0; u < 2; ++u) fwin_advance_g<1>(ch[u], sel[u]); break;
+                            case 2: for (int u = 0; u < 2; ++u) fwin_advance_g<2>(ch[u], sel[u]); break;
+                            case 3: for (int u = 0; u < 2; ++u) fwin_advance_g<3>(ch[u], sel[u]); break;
+                            case 4: for (int u = 0; u < 2; ++u) fwin_advance_g<4>(ch[u], sel[u]); break;
+                            case 5: for (int u = 0; u < 2; ++u) fwin_advance_g<5>(ch[u], sel[u]); break;
+                            case 6: for (int u = 0; u < 2; ++u) fwin_advance_g<6>(ch[u], sel[u]); break;
+                            default: for (int u = 0; u < 2; ++u) fwin_advance_g<7>(ch[u], sel[u]); break;
+                        }
                     }
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) fwin_rebase(ch[u]);
                 } else if (fast) {
 #pragma unroll
                     for (int v = 0; v < 16; v += 2) {  // 3 PRMT per 4 output bytes
