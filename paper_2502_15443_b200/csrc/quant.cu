@@ -103,6 +103,23 @@ __device__ __forceinline__ int8_t q_of_fast(double v, double w_scale, double inv
     return (int8_t)(int)sg;
 }
 
+// q from the f32 product xf = w * c with c = s[col] / w_scale rounded to
+// f32 (FP32 pipe only): |xf - x| < 2e-5 for the exact f64 quotient
+// x = (w * s) / w_scale (|x| <= 127.5), so round-half-away(xf) equals the
+// reference's floor(|x| + 0.5) unless |xf| is within 1e-4 of a half-integer,
+// where the exact f64 path decides (rare).  The nearest integer comes from the
+// mantissa of |xf| + 2^23 (no conversion instruction).
+__device__ __forceinline__ int8_t q_of_f32(float wf, float cf, double w64, double sc, double w_scale) {
+    const float xf = wf * cf;
+    const float a = fabsf(xf);
+    const float t = __fadd_rn(a, 8388608.0f);  // 2^23
+    const float d = __fsub_rn(a, __fsub_rn(t, 8388608.0f));
+    if (fabsf(fabsf(d) - 0.5f) < 1e-4f) return q_of(__dmul_rn(w64, sc), w_scale);
+    int r = (int)(__float_as_uint(t) & 0x7FFFFFu);
+    r = r > 127 ? 127 : r;
+    return (int8_t)(xf < 0.0f ? -r : r);
+}
+
 // q[r, c] plus, optionally, the per-(column, |q|) histogram used by pruning
 // (counts[c * 129 + |q|], u32, must be zeroed).
 template <int T>
@@ -158,6 +175,42 @@ __device__ __forceinline__ void load8(const typename In<T>::type* __restrict__ w
     }
 }
 
+// Raw 16-byte vectors of 8 consecutive elements (4 for f64, 2 for f32, 1 for
+// bf16/f16): kept un-widened so several rows can be in flight per thread
+// without the register cost of 8 doubles per row.
+template <int T>
+struct Raw8 {
+    static constexpr int kVec = T == kF64 ? 4 : (T == kF32 ? 2 : 1);
+    uint4 u[kVec];
+};
+template <int T>
+__device__ __forceinline__ void load_raw8(const typename In<T>::type* __restrict__ w, int64_t e, Raw8<T>& r) {
+#pragma unroll
+    for (int k = 0; k < Raw8<T>::kVec; ++k) r.u[k] = __ldg(reinterpret_cast<const uint4*>(w + e) + k);
+}
+template <int T>
+__device__ __forceinline__ double raw_at(const Raw8<T>& r, int k) {
+    const uint32_t* x = reinterpret_cast<const uint32_t*>(r.u);
+    if constexpr (T == kF64) {
+        return __hiloint2double((int)x[2 * k + 1], (int)x[2 * k]);
+    } else if constexpr (T == kF32) {
+        return (double)__uint_as_float(x[k]);
+    } else {
+        const uint16_t h = (uint16_t)(x[k >> 1] >> (16 * (k & 1)));
+        typename In<T>::type v;
+        memcpy(&v, &h, 2);
+        return In<T>::f64(v);
+    }
+}
+template <int T>
+__device__ __forceinline__ float raw_at_f32(const Raw8<T>& r, int k) {
+    const uint32_t* x = reinterpret_cast<const uint32_t*>(r.u);
+    if constexpr (T == kF64) return __double2float_rn(__hiloint2double((int)x[2 * k + 1], (int)x[2 * k]));
+    else if constexpr (T == kF32) return __uint_as_float(x[k]);
+    else if constexpr (T == kBF16) return __uint_as_float((x[k >> 1] >> (16 * (k & 1))) << 16);
+    else return __half2float(__ushort_as_half((uint16_t)(x[k >> 1] >> (16 * (k & 1)))));
+}
+
 __device__ __forceinline__ void load_s8(const double* __restrict__ s, int64_t c, double (&sc)[8]) {
     if (s) {
 #pragma unroll
@@ -185,15 +238,24 @@ __global__ void __launch_bounds__(kQThreads) k_absmax_v(const typename In<T>::ty
     const int64_t cg = t % gpr, rp = t / gpr;
     double sc[8];
     load_s8(s, cg * 8, sc);
-    for (int64_t r = rp; r < rows && rp < rows_par; r += rows_par) {
-        const int64_t e = r * cols + cg * 8;
-        double v[8];
-        load8<T>(w, e, v);
+    constexpr int kQR = T == kF64 ? 2 : 4;  // rows in flight per thread (see k_quantize_v)
+    for (int64_t r0 = rp; r0 < rows && rp < rows_par; r0 += kQR * rows_par) {
+        Raw8<T> v[kQR];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            bad |= !isfinite(v[k]);
-            const double a = fabs(__dmul_rn(v[k], sc[k]));
-            m = a > m ? a : m;
+        for (int j = 0; j < kQR; ++j) {
+            const int64_t r = r0 + j * rows_par;
+            if (r < rows) load_raw8<T>(w, r * cols + cg * 8, v[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < kQR; ++j) {
+            if (r0 + j * rows_par >= rows) break;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double x = raw_at<T>(v[j], k);
+                bad |= !isfinite(x);
+                const double a = fabs(__dmul_rn(x, sc[k]));
+                m = a > m ? a : m;
+            }
         }
     }
     __shared__ double red[kQThreads / 32];
@@ -216,25 +278,41 @@ template <int T>
 __global__ void __launch_bounds__(kQThreads) k_quantize_v(const typename In<T>::type* __restrict__ w,
                                                            const double* __restrict__ s, int64_t rows, int64_t cols,
                                                            int64_t rows_par, double w_scale, int8_t* __restrict__ q) {
-    const double inv = 1.0 / w_scale;
     const int64_t gpr = cols / 8, t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t cg = t % gpr, rp = t / gpr;
     double sc[8];
     load_s8(s, cg * 8, sc);
-    for (int64_t r = rp; r < rows && rp < rows_par; r += rows_par) {
-        const int64_t e = r * cols + cg * 8;
-        double v[8];
-        load8<T>(w, e, v);
-        uint32_t lo = 0, hi = 0;
+    float cf[8];  // s[col] / w_scale in f32 (see q_of_f32)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint32_t b = (uint8_t)q_of_fast(__dmul_rn(v[k], sc[k]), w_scale, inv);
-            if (k < 4)
-                lo |= b << (8 * k);
-            else
-                hi |= b << (8 * (k - 4));
+    for (int k = 0; k < 8; ++k) cf[k] = __double2float_rn(sc[k] / w_scale);
+    // kQR rows per iteration, raw (un-widened) loads all issued before any use:
+    // the kernel is memory-latency bound with one row in flight per thread
+#ifndef DC_QUANT_ROWS
+#define DC_QUANT_ROWS 1
+#endif
+    constexpr int kQR = T == kF64 ? 1 : DC_QUANT_ROWS;
+    for (int64_t r0 = rp; r0 < rows && rp < rows_par; r0 += kQR * rows_par) {
+        Raw8<T> v[kQR];
+#pragma unroll
+        for (int j = 0; j < kQR; ++j) {
+            const int64_t r = r0 + j * rows_par;
+            if (r < rows) load_raw8<T>(w, r * cols + cg * 8, v[j]);
         }
-        *reinterpret_cast<uint2*>(q + e) = make_uint2(lo, hi);
+#pragma unroll
+        for (int j = 0; j < kQR; ++j) {
+            const int64_t r = r0 + j * rows_par;
+            if (r >= rows) break;
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t b = (uint8_t)q_of_f32(raw_at_f32<T>(v[j], k), cf[k], raw_at<T>(v[j], k), sc[k], w_scale);
+                if (k < 4)
+                    lo |= b << (8 * k);
+                else
+                    hi |= b << (8 * (k - 4));
+            }
+            *reinterpret_cast<uint2*>(q + r * cols + cg * 8) = make_uint2(lo, hi);
+        }
     }
 }
 
