@@ -49,3 +49,25 @@ def test_simulate_layer_matches_reference_formula(cuda):
         qe = np.linalg.norm(yq - y) / np.linalg.norm(y)
         assert rep.fp_identity_error == pytest.approx(fp, rel=1e-6, abs=1e-15)
         assert rep.quantized_error == pytest.approx(qe, rel=1e-9)
+
+
+def test_simulate_layer_equals_reference_golden(cuda):
+    """simulate_layer (GPU quantize + tcgen05 W8A8, f64 references on the GPU)
+    against reports the REFERENCE computed on the same seeded inputs
+    (tests/golden/make_simulate_golden.py); only the f64 summation order
+    differs, so the errors agree to 1e-9 relative."""
+    import json
+    import os
+
+    import numpy as np
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "simulate.json")) as f:
+        gold = json.load(f)
+    for g in gold:
+        w, st = cuda.synth_ensemble(cuda.SynthSpec(rows=g["rows"], cols=g["cols"], name=f"t{g['seed']}"),
+                                    40 + g["seed"])
+        x = np.random.default_rng([g["seed"], 7]).normal(0.0, 1.0, (g["batch"], g["cols"])) * st.channel_max[None, :]
+        rep = cuda.simulate_layer(x, w, st, g["alpha"])
+        assert rep.alpha == g["alpha"]
+        assert abs(rep.fp_identity_error - g["fp_identity_error"]) <= 1e-9 * max(g["fp_identity_error"], 1e-12)
+        assert abs(rep.quantized_error - g["quantized_error"]) <= 1e-9 * g["quantized_error"]
