@@ -165,52 +165,8 @@ __device__ __forceinline__ FmaK fma_consts(uint32_t one) {
 // Slot address without the ALU mask: with t = (x >> 12) - 4096 (needed for the
 // state update anyway), tab + 4*(x & 4095) = (tab - 2^26) + 4x - 16384 t: two
 // IMADs on the FMA pipe instead of LOP3 + IMAD.  `tabm` = tab - 2^26.
-#ifndef DC_DEC_VARIANT
-#define DC_DEC_VARIANT 0
-#endif
 __device__ __forceinline__ uint32_t dec_sym_fa(uint32_t& x, uint32_t& s, uint32_t v, uint32_t tabm, const FmaK& k) {
     uint32_t e;
-#if DC_DEC_VARIANT == 1  // f and b extraction on the FMA pipe (IMAD.HI by 2^12 / 2^24)
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
-        "shr.u32 t, %0, 12;\n\t"
-        "sub.u32 t, t, 4096;\n\t"
-        "mad.lo.u32 a, %0, %5, %4;\n\t"
-        "mad.lo.u32 a, t, %6, a;\n\t"
-        "ld.shared.u32 %2, [a];\n\t"
-        "mul.hi.u32 f, %2, %7;\n\t"
-        "mul.hi.u32 b, %2, %8;\n\t"
-        "mad.lo.u32 %0, f, t, b;\n\t"
-        "setp.lt.u32 q, %0, 0x100000;\n\t"
-        "@q prmt.b32 %0, %0, %3, %1;\n\t"
-        "@q add.u32 %1, %1, 1;\n\t"
-        "setp.lt.u32 q, %0, 0x100000;\n\t"
-        "@q prmt.b32 %0, %0, %3, %1;\n\t"
-        "@q add.u32 %1, %1, 1;\n\t}"
-        : "+r"(x), "+r"(s), "=r"(e)
-        : "r"(v), "r"(tabm), "r"(k.c4), "r"(k.cm16384), "r"(k.c2p12), "r"(k.c2p24));
-    return e;
-#elif DC_DEC_VARIANT == 2  // b on the FMA pipe only
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
-        "shr.u32 t, %0, 12;\n\t"
-        "sub.u32 t, t, 4096;\n\t"
-        "mad.lo.u32 a, %0, %5, %4;\n\t"
-        "mad.lo.u32 a, t, %6, a;\n\t"
-        "ld.shared.u32 %2, [a];\n\t"
-        "shr.u32 f, %2, 20;\n\t"
-        "mul.hi.u32 b, %2, %7;\n\t"
-        "mad.lo.u32 %0, f, t, b;\n\t"
-        "setp.lt.u32 q, %0, 0x100000;\n\t"
-        "@q prmt.b32 %0, %0, %3, %1;\n\t"
-        "@q add.u32 %1, %1, 1;\n\t"
-        "setp.lt.u32 q, %0, 0x100000;\n\t"
-        "@q prmt.b32 %0, %0, %3, %1;\n\t"
-        "@q add.u32 %1, %1, 1;\n\t}"
-        : "+r"(x), "+r"(s), "=r"(e)
-        : "r"(v), "r"(tabm), "r"(k.c4), "r"(k.cm16384), "r"(k.c2p24));
-    return e;
-#endif
     asm volatile(
         "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
         "shr.u32 t, %0, 12;\n\t"
