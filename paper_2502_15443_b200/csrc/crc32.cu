@@ -87,6 +87,9 @@ __device__ __forceinline__ uint32_t pow_for(uint64_t j) {
 #ifndef DC_CRC_SLOTS
 #define DC_CRC_SLOTS 1  // measured: warps, not prefetch depth, hide the latency (1 slot x 32 warps: 4.46 TB/s; 3 x 14: 3.41)
 #endif
+#ifndef DC_CRC_L2PF
+#define DC_CRC_L2PF 1  // L2 prefetch of the next round: +3 % (tools/ab_crc.sh)
+#endif
 #ifndef DC_CRC_WARPS
 #define DC_CRC_WARPS 32
 #endif
@@ -237,6 +240,14 @@ __global__ void __launch_bounds__(kLaneWarps * 32, 1) k_crc_lanes(const __grid_c
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&bar[slot], kRoundBytes);
             tma_load_2d(ring + slot * kRoundBytes, &tmap, 0, i_row + (int32_t)(iq * (kRoundBytes / 128)), &bar[slot]);
+#if DC_CRC_L2PF
+            // pull the next DC_CRC_L2PF rounds of this span into L2 so their
+            // (serialised, one-slot) TMA loads hit L2 instead of HBM
+            if (iq + DC_CRC_L2PF < kRounds) {
+                const uint64_t nxt = map_base + ((uint64_t)(i_row + (int32_t)((iq + DC_CRC_L2PF) * (kRoundBytes / 128))) << 7);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt), "r"(kRoundBytes) : "memory");
+            }
+#endif
         }
         ++gq_issue;
         if (++iq == kRounds) {
