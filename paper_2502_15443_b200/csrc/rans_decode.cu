@@ -359,13 +359,18 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
     const uint32_t tabm = tab - (1u << 26);
     const uint32_t K = 1u << seg_shift;
     const int G = (int)(K >> 4);
-    uint32_t x[NU], n[NU];
+    uint32_t x[NU], n[NU], xe[NU], pe[NU];
     Win W[NU];
     bool wild = false;  // a split point outside the staged span: never used as an address
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
         const int r = warp * 32 + lane + u * TH;
         const uint32_t rel = (uint32_t)(s0 + r);
+        // the chain check's targets (the next split point), loaded now so the
+        // loads' latency hides behind the decode instead of the task tail
+        const bool inner = rel + 1 < nseg_chunk;
+        xe[u] = (r < ns && inner) ? seg_state[sb + rel + 1] : kStateLower;
+        pe[u] = (r < ns && inner) ? seg_off[sb + rel + 1] : plen;
         uint32_t p;
         if (r < ns) {
             x[u] = seg_state[sb + rel];
@@ -495,16 +500,7 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
     for (int u = 0; u < NU; ++u) {
         const int r = warp * 32 + lane + u * TH;
         if (r >= ns) continue;
-        const uint32_t rel = (uint32_t)(s0 + r);
-        uint32_t xe, pe;
-        if (rel + 1 < nseg_chunk) {
-            xe = seg_state[sb + rel + 1];
-            pe = seg_off[sb + rel + 1];
-        } else {
-            xe = kStateLower;
-            pe = plen;
-        }
-        if (x[u] != xe || win_pos(W[u]) - stage - delta + lo != pe) atomicExch(st, DC_CHUNK_CHAIN);
+        if (x[u] != xe[u] || win_pos(W[u]) - stage - delta + lo != pe[u]) atomicExch(st, DC_CHUNK_CHAIN);
     }
 }
 
