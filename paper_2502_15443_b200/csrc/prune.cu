@@ -10,7 +10,11 @@
 //   per row: one CTA per row, 8 x 8-bit radix select in shared memory and
 //     the same ordered tie pass.
 // Non-negative doubles order like their u64 bit patterns, so keys are bits.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace dc {
 
@@ -30,174 +34,6 @@ __device__ __forceinline__ unsigned long long key_of(double cm, int a) {
 
 __device__ __forceinline__ int absq(int8_t v) { return v < 0 ? -(int)v : (int)v; }
 
-// counts[c * 129 + |q|]; CTA = 256 columns x a row range, u16 private bins.
-__global__ void __launch_bounds__(kPrThreads) k_colhist(const int8_t* __restrict__ q, int64_t rows, int64_t cols,
-                                                         int64_t rows_per_cta, uint32_t* __restrict__ counts) {
-    extern __shared__ uint16_t bins[];  // [256][130]
-    const int t = threadIdx.x;
-    for (int i = t; i < kPrThreads * 130; i += blockDim.x) bins[i] = 0;
-    __syncthreads();
-    const int64_t c = (int64_t)blockIdx.y * kPrThreads + t;
-    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
-    const int64_t r1 = min(rows, r0 + rows_per_cta);
-    if (c < cols) {
-        uint16_t* b = bins + t * 130;
-        for (int64_t r = r0; r < r1; ++r) b[absq(q[r * cols + c])]++;
-        for (int a = 0; a < kBins; ++a)
-            if (b[a]) atomicAdd(&counts[c * kBins + a], (uint32_t)b[a]);
-    }
-}
-
-// one radix pass over the (column, |q|) entries
-__global__ void k_select_hist(const uint32_t* __restrict__ counts, const double* __restrict__ cm, int64_t cols,
-                              int shift, const SelectState* __restrict__ st, unsigned long long* __restrict__ hist) {
-    const int64_t n = cols * kBins;
-    const unsigned long long prefix = st->prefix;
-    const int top = shift + 16;  // bits above this pass's digit
-    // whole warps iterate together so equal digits can be combined: the first
-    // pass (top 16 key bits) sends nearly every entry to a handful of bins
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-        const int64_t i = base + threadIdx.x;
-        uint32_t cnt = 0, bin = 0xFFFFFFFFu;
-        if (i < n) {
-            cnt = counts[i];
-            if (cnt) {
-                const uint32_t col = (uint32_t)i / (uint32_t)kBins;  // n < 2^32: 32-bit magic division
-                const unsigned long long key = key_of(cm[col], (int)((uint32_t)i - col * (uint32_t)kBins));
-                if (top >= 64 || (key >> top) == prefix) bin = (uint32_t)((key >> shift) & 0xFFFF);
-            }
-        }
-        const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-        const uint32_t sum = __reduce_add_sync(peers, bin == 0xFFFFFFFFu ? 0u : cnt);
-        if (bin != 0xFFFFFFFFu && (threadIdx.x & 31) == __ffs(peers) - 1)
-            atomicAdd(&hist[bin], (unsigned long long)sum);
-    }
-}
-
-// single CTA: find the digit bucket holding rank st->k
-__global__ void __launch_bounds__(1024) k_select_pick(const unsigned long long* __restrict__ hist,
-                                                      SelectState* __restrict__ st) {
-    __shared__ unsigned long long part[1024];
-    const int t = threadIdx.x;
-    unsigned long long s = 0;
-    for (int i = 0; i < 64; ++i) s += hist[t * 64 + i];
-    part[t] = s;
-    __syncthreads();
-    if (t == 0) {
-        unsigned long long k = st->k, acc = 0;
-        int blk = 0;
-        while (blk < 1023 && acc + part[blk] < k) acc += part[blk++];
-        int b = blk * 64;
-        while (b < blk * 64 + 63 && acc + hist[b] < k) acc += hist[b++];
-        st->prefix = (st->prefix << 16) | (unsigned long long)b;
-        st->k = k - acc;
-        st->below += acc;
-    }
-}
-
-// per 4096-element block: how many entries have key == T
-__global__ void k_eq_count(const int8_t* __restrict__ q, const double* __restrict__ cm, int64_t n, int64_t cols,
-                           const SelectState* __restrict__ st, uint32_t* __restrict__ blk_cnt) {
-    const unsigned long long T = st->prefix;
-    const int64_t b = blockIdx.x;
-    uint32_t cnt = 0;
-    for (int64_t i = b * kEqBlock + threadIdx.x; i < min(n, (b + 1) * kEqBlock); i += blockDim.x)
-        cnt += key_of(cm[i % cols], absq(q[i])) == T;
-    __shared__ uint32_t red[kPrThreads / 32];
-#pragma unroll
-    for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t s = 0;
-        for (int w = 0; w < kPrThreads / 32; ++w) s += red[w];
-        blk_cnt[b] = s;
-    }
-}
-
-__global__ void __launch_bounds__(1024) k_excl_scan(uint32_t* __restrict__ v, int64_t n) {
-    __shared__ unsigned long long part[1024];
-    const int t = threadIdx.x;
-    const int64_t per = (n + 1023) / 1024;
-    unsigned long long s = 0;
-#pragma unroll 8
-    for (int64_t i = t * per; i < min(n, (t + 1) * per); ++i) s += v[i];
-    // block-wide exclusive scan of the 1024 thread sums (warp scans + a scan of
-    // the 32 warp totals; counts < 2^32, see dc_prune_tensor)
-    const int lane = t & 31, w = t >> 5;
-    uint32_t inc = (uint32_t)s;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += o;
-    }
-    __shared__ uint32_t wtot[32];
-    if (lane == 31) wtot[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-        const uint32_t x0 = wtot[lane];
-        uint32_t x = x0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += o;
-        }
-        wtot[lane] = x - x0;
-    }
-    __syncthreads();
-    part[t] = wtot[w] + inc - (uint32_t)s;
-    __syncthreads();
-    unsigned long long acc = part[t];
-    const int64_t e = min(n, (t + 1) * per);
-    for (int64_t i0 = t * per; i0 < e; i0 += 8) {  // 8 loads in flight, then the stores
-        uint32_t x[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = i0 + j < e ? v[i0 + j] : 0u;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (i0 + j < e) {
-                v[i0 + j] = (uint32_t)acc;
-                acc += x[j];
-            }
-    }
-}
-
-// zero key < T, and key == T while the ordered tie rank < r
-__global__ void __launch_bounds__(kPrThreads) k_apply(const int8_t* __restrict__ q, const double* __restrict__ cm,
-                                                       int64_t n, int64_t cols, const SelectState* __restrict__ st,
-                                                       const uint32_t* __restrict__ blk_prefix,
-                                                       int8_t* __restrict__ out) {
-    const unsigned long long T = st->prefix, r = st->k;
-    const int64_t b = blockIdx.x;
-    __shared__ uint32_t wc[kPrThreads / 32];
-    unsigned long long run = blk_prefix[b];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int64_t base = b * kEqBlock; base < min(n, (b + 1) * kEqBlock); base += kPrThreads) {
-        const int64_t i = base + threadIdx.x;
-        int8_t v = 0;
-        bool eq = false, lt = false;
-        if (i < n) {
-            v = q[i];
-            const unsigned long long key = key_of(cm[i % cols], absq(v));
-            eq = key == T;
-            lt = key < T;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, eq);
-        if (lane == 0) wc[warp] = __popc(m);
-        __syncthreads();
-        uint32_t before = 0, total = 0;
-        for (int w = 0; w < kPrThreads / 32; ++w) {
-            before += (w < warp) ? wc[w] : 0;
-            total += wc[w];
-        }
-        const unsigned long long rank = run + before + __popc(m & ((1u << lane) - 1));
-        if (i < n) out[i] = (lt || (eq && rank < r)) ? (int8_t)0 : v;
-        run += total;
-        __syncthreads();
-    }
-}
-
 __global__ void k_sel_init(SelectState* st, unsigned long long k) {
     st->prefix = 0;
     st->k = k;
@@ -209,117 +45,6 @@ __global__ void k_sel_init(SelectState* st, unsigned long long k) {
 // shared memory (thread = column x row phase, coalesced byte loads), partial
 // histograms written whole (no global atomics) and summed by k_colhist_sum.
 constexpr int kHcCols = 64;
-
-__global__ void __launch_bounds__(kPrThreads) k_colhist2(const int8_t* __restrict__ q, int64_t rows, int64_t cols,
-                                                          int64_t rows_per, uint32_t* __restrict__ partial) {
-    __shared__ uint32_t bins[kHcCols * kBins];
-    for (int i = threadIdx.x; i < kHcCols * kBins; i += blockDim.x) bins[i] = 0;
-    __syncthreads();
-    const int cl = threadIdx.x % kHcCols, rph = threadIdx.x / kHcCols;  // 4 row phases
-    const int64_t c = (int64_t)blockIdx.y * kHcCols + cl;
-    const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(rows, r0 + rows_per);
-    if (c < cols)
-        for (int64_t r = r0 + rph; r < r1; r += kPrThreads / kHcCols) atomicAdd(&bins[cl * kBins + absq(q[r * cols + c])], 1u);
-    __syncthreads();
-    uint32_t* out = partial + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * (kHcCols * kBins);
-    for (int i = threadIdx.x; i < kHcCols * kBins; i += blockDim.x) out[i] = bins[i];
-}
-
-// counts[c * 129 + a] = sum over row blocks of the partials
-__global__ void k_colhist_sum(const uint32_t* __restrict__ partial, int64_t n_rb, int64_t n_cb, int64_t cols,
-                              uint32_t* __restrict__ counts) {
-    const int64_t per_rb = n_cb * kHcCols * kBins;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols * kBins;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t s = 0;
-        for (int64_t rb = 0; rb < n_rb; ++rb) s += partial[rb * per_rb + i];
-        counts[i] = s;
-    }
-}
-
-// single CTA: find the 16-bit digit bucket holding rank st->k.  Coalesced
-// 1024-bin tiles -> 2048 partial sums of 32 bins -> block scan -> one warp
-// resolves the bin inside its 32.
-__global__ void __launch_bounds__(1024) k_select_pick2(const unsigned long long* __restrict__ hist,
-                                                       SelectState* __restrict__ st) {
-    __shared__ unsigned long long part[2048];
-    __shared__ unsigned long long wsum[32];
-    __shared__ int s_part;
-    __shared__ unsigned long long s_base;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    // partial p = bins [32p, 32p + 32): warp w, round i reduces partial 32i + w
-    // from one coalesced 256-B load with one REDUX (the host caps a tensor at
-    // 2^32 - 1 elements, so every partial fits 32 bits); 16 loads in flight
-    for (int i0 = 0; i0 < 64; i0 += 16) {
-        unsigned long long v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = hist[(i0 + j) * 1024 + t];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t sum = __reduce_add_sync(0xffffffffu, (uint32_t)v[j]);
-            if (lane == 0) part[(i0 + j) * 32 + w] = sum;
-        }
-    }
-    __syncthreads();
-    const unsigned long long a = part[2 * t], b = part[2 * t + 1], s = a + b;
-    unsigned long long inc = s;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += o;
-    }
-    if (lane == 31) wsum[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-        unsigned long long v = wsum[lane], x = v;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const unsigned long long o = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += o;
-        }
-        wsum[lane] = x - v;  // exclusive
-    }
-    __syncthreads();
-    inc += wsum[w];
-    const unsigned long long k = st->k, excl = inc - s;
-    if (excl < k && k <= inc) {  // exactly one thread owns the rank
-        const bool first = k <= excl + a;
-        s_part = 2 * t + (first ? 0 : 1);
-        s_base = first ? excl : excl + a;
-    }
-    __syncthreads();
-    if (w == 0) {  // resolve inside the 32 bins of partial s_part
-        const int bin0 = s_part * 32;
-        const unsigned long long v = hist[bin0 + lane];
-        unsigned long long x = v;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const unsigned long long o = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += o;
-        }
-        const unsigned long long lo = s_base + x - v, hi = s_base + x;
-        if (lo < k && k <= hi) {
-            st->prefix = (st->prefix << 16) | (unsigned long long)(bin0 + lane);
-            st->k = k - lo;
-            st->below += lo;
-        }
-    }
-}
-
-// per column: |q| < lo -> score < T; lo <= |q| < hi -> score == T (cm >= 0, so
-// the score is non-decreasing in |q|; strictly increasing when cm > 0)
-__global__ void k_col_bounds(const double* __restrict__ cm, int64_t cols, const SelectState* __restrict__ st,
-                             uint8_t* __restrict__ lo, uint8_t* __restrict__ hi) {
-    const unsigned long long T = st->prefix;
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
-        int l = 0, h;
-        while (l < kBins && key_of(cm[c], l) < T) ++l;
-        h = l;
-        while (h < kBins && key_of(cm[c], h) == T) ++h;
-        lo[c] = (uint8_t)l;
-        hi[c] = (uint8_t)h;
-    }
-}
 
 // 16 consecutive elements per thread (one 4096-element block per CTA):
 // lt / eq flags from the column bounds, no f64 work per element
@@ -367,45 +92,223 @@ __device__ __forceinline__ void flags16(const int8_t* __restrict__ q, const uint
 constexpr int kEqSub = 4;
 constexpr int64_t kEqBlock2 = (int64_t)kEqSub * kEqBlock;
 
-__global__ void __launch_bounds__(kPrThreads) k_eq_count2(const int8_t* __restrict__ q, const uint8_t* __restrict__ lo,
-                                                           const uint8_t* __restrict__ hi, int64_t n, int64_t cols,
-                                                           bool vec, uint32_t* __restrict__ blk_cnt) {
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int r = 0; r < kEqSub; ++r) {
-        int8_t v[16];
-        uint32_t ltm, eqm;
-        flags16(q, lo, hi, n, cols, (int64_t)blockIdx.x * kEqBlock2 + r * kEqBlock + threadIdx.x * 16, vec, v, ltm,
-                eqm);
-        cnt += __popc(eqm);
-    }
-    __shared__ uint32_t red[kPrThreads / 32];
-#pragma unroll
-    for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+// ------------------------------------------- per tensor, round-2 path
+// (column, |q|) histogram with 16-byte loads: a CTA is 8 column groups of 16
+// columns (one uint4 per row each) x 128 row phases, 4 rows in flight per
+// thread; u32 bins for its 128 columns in shared memory; partial histograms
+// per row block, summed by k_colhist3_sum.
+constexpr int kH3Cols = 128;
+constexpr int kH3Threads = 1024;
+
+__global__ void __launch_bounds__(kH3Threads, 2) k_colhist3(const int8_t* __restrict__ q, int64_t rows, int64_t cols,
+                                                             int64_t rows_per, bool vec, uint32_t* __restrict__ partial) {
+    extern __shared__ uint32_t hb[];  // [kH3Cols][kBins]
+    for (int i = threadIdx.x; i < kH3Cols * kBins; i += blockDim.x) hb[i] = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    const int cg8 = threadIdx.x & 7, rph = threadIdx.x >> 3;  // 8 column groups x 128 row phases
+    const int64_t c0 = (int64_t)blockIdx.y * kH3Cols + cg8 * 16;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(rows, r0 + rows_per);
+    uint32_t* b = hb + cg8 * 16 * kBins;
+    if (vec && c0 + 16 <= cols) {
+        for (int64_t r = r0 + rph; r < r1; r += 4 * (kH3Threads / 8)) {
+            uint4 v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t rr = r + j * (kH3Threads / 8);
+                v[j] = rr < r1 ? __ldg(reinterpret_cast<const uint4*>(q + rr * cols + c0)) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (r + j * (kH3Threads / 8) >= r1) break;
+                const uint32_t w[4] = {__vabs4(v[j].x), __vabs4(v[j].y), __vabs4(v[j].z), __vabs4(v[j].w)};
+#pragma unroll
+                for (int e = 0; e < 16; ++e) atomicAdd(&b[e * kBins + ((w[e >> 2] >> (8 * (e & 3))) & 0xFF)], 1u);
+            }
+        }
+    } else {
+        for (int64_t r = r0 + rph; r < r1; r += kH3Threads / 8)
+            for (int e = 0; e < 16 && c0 + e < cols; ++e) atomicAdd(&b[e * kBins + absq(q[r * cols + c0 + e])], 1u);
+    }
+    __syncthreads();
+    uint32_t* out = partial + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * (kH3Cols * kBins);
+    for (int i = threadIdx.x; i < kH3Cols * kBins; i += blockDim.x) out[i] = hb[i];
+}
+
+// counts[c * 129 + a] = sum over row blocks of the k_colhist3 partials
+__global__ void k_colhist3_sum(const uint32_t* __restrict__ partial, int64_t n_rb, int64_t n_cb, int64_t cols,
+                               uint32_t* __restrict__ counts) {
+    const int64_t per_rb = n_cb * kH3Cols * kBins;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols * kBins;
+         i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t s = 0;
-        for (int w = 0; w < kPrThreads / 32; ++w) s += red[w];
-        blk_cnt[blockIdx.x] = s;
+        for (int64_t rb = 0; rb < n_rb; ++rb) s += partial[rb * per_rb + i];
+        counts[i] = s;
     }
 }
 
-__global__ void __launch_bounds__(kPrThreads) k_apply2(const int8_t* __restrict__ q, const uint8_t* __restrict__ lo,
+// Block-wide: find the entry of v[0..m) (m <= blockDim.x, u32 counts) holding
+// rank k (1-based) given `base` = count before v[0]; returns index and the
+// count before it through shared memory.  All threads participate.
+__device__ __forceinline__ void block_find(const uint32_t* v, int m, unsigned long long k, unsigned long long base,
+                                           int* s_idx, unsigned long long* s_before, unsigned long long* wsum) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const unsigned long long x = t < m ? __ldcg(v + t) : 0ull;  // written by other CTAs: bypass L1
+    unsigned long long inc = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    unsigned long long before = base;
+    for (int i = 0; i < w; ++i) before += wsum[i];
+    inc += before;
+    if (t < m && inc - x < k && k <= inc) {
+        *s_idx = t;
+        *s_before = inc - x;
+    }
+    __syncthreads();
+}
+
+// The whole k-th-score selection in ONE cooperative launch (grid = SMs):
+// per 16-bit digit pass, a grid-strided (column, |q|) histogram with
+// warp-aggregated atomics into u32 bins (n < 2^32), per-CTA slice sums, and
+// CTA 0 picks the slice and then the bin with block scans; the two histogram
+// buffers alternate so the next pass's zeroing overlaps the pick.  Then the
+// per-column |q| bounds of score < T and score == T.  Replaces 4 x (memset,
+// k_select_hist, k_select_pick2) + k_col_bounds (13 launches).
+constexpr int kSelThreads = 512;
+
+__global__ void __launch_bounds__(kSelThreads) k_select_coop(const uint32_t* __restrict__ counts,
+                                                             const double* __restrict__ cm, int64_t cols,
+                                                             SelectState* __restrict__ st, uint32_t* __restrict__ hist2,
+                                                             uint32_t* __restrict__ psum2, uint8_t* __restrict__ lo,
+                                                             uint8_t* __restrict__ hi) {
+    // hist2 / psum2: two buffers each (pass parity), zeroed by the host before
+    // the launch; the buffer of pass p + 2 is re-zeroed during pass p + 1's pick
+    cg::grid_group grid = cg::this_grid();
+    const int64_t n = cols * kBins;
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int slice = (65536 + gridDim.x - 1) / gridDim.x;
+    __shared__ unsigned long long wsum[kSelThreads / 32], s_before;
+    __shared__ int s_idx;
+    for (int pass = 0; pass < 4; ++pass) {
+        uint32_t* hist = hist2 + (pass & 1) * 65536;
+        uint32_t* psum = psum2 + (pass & 1) * 4096;
+        const int shift = 48 - 16 * pass, top = shift + 16;
+        // st / hist / psum are written by other CTAs between grid barriers: every
+        // read of them bypasses L1 (ld.cg), which is not coherent across SMs
+        const unsigned long long prefix = __ldcg(&st->prefix);
+        // histogram of this pass's digit; the slice totals accumulate alongside
+        for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += gs) {
+            const int64_t i = base + threadIdx.x;
+            uint32_t cnt = 0, bin = 0xFFFFFFFFu;
+            if (i < n) {
+                cnt = counts[i];
+                if (cnt) {
+                    const uint32_t col = (uint32_t)i / (uint32_t)kBins;
+                    const unsigned long long key = key_of(cm[col], (int)((uint32_t)i - col * (uint32_t)kBins));
+                    if (top >= 64 || (key >> top) == prefix) bin = (uint32_t)((key >> shift) & 0xFFFF);
+                }
+            }
+            const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+            const uint32_t sum = __reduce_add_sync(peers, bin == 0xFFFFFFFFu ? 0u : cnt);
+            if (bin != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], sum);
+        }
+        grid.sync();
+        {  // per-CTA slice sums (an atomic per slice would serialise: pass 0 sends
+           // nearly every key to a handful of bins)
+            __shared__ uint32_t red[kSelThreads / 32];
+            uint32_t v = 0;
+            const int b0 = blockIdx.x * slice;
+            for (int b = b0 + threadIdx.x; b < min(65536, b0 + slice); b += blockDim.x) v += __ldcg(hist + b);
+            v = __reduce_add_sync(0xffffffffu, v);
+            if (lane == 0) red[threadIdx.x >> 5] = v;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t t = 0;
+                for (int k = 0; k < kSelThreads / 32; ++k) t += red[k];
+                psum[blockIdx.x] = t;
+            }
+        }
+        grid.sync();
+        if (blockIdx.x == 0) {
+            const unsigned long long k = __ldcg(&st->k);
+            // windows of kSelThreads entries: (index, count before) of the rank-k entry
+            auto find = [&](const uint32_t* v, int m, unsigned long long& base) -> int {
+                for (int c0 = 0; c0 < m; c0 += kSelThreads) {
+                    if (threadIdx.x == 0) s_idx = -1;
+                    __syncthreads();
+                    block_find(v + c0, min(kSelThreads, m - c0), k, base, &s_idx, &s_before, wsum);
+                    const int idx = s_idx;
+                    if (idx >= 0) {
+                        base = s_before;
+                        __syncthreads();
+                        return c0 + idx;
+                    }
+                    for (int i = 0; i < kSelThreads / 32; ++i) base += wsum[i];
+                    __syncthreads();
+                }
+                return m - 1;  // unreachable for 1 <= k <= total
+            };
+            unsigned long long base = 0;
+            const int sl = find(psum, (int)gridDim.x, base);  // slice holding rank k
+            const int b0 = sl * slice;
+            const int bin = b0 + find(hist + b0, min(65536, b0 + slice) - b0, base);  // bin inside it
+            if (threadIdx.x == 0) {
+                st->prefix = (__ldcg(&st->prefix) << 16) | (unsigned long long)bin;
+                st->k = k - base;
+                st->below = __ldcg(&st->below) + base;
+            }
+        }
+        // the buffers of pass - 1 were consumed by its pick: zero them for pass + 1
+        if (pass >= 1 && pass < 3 && (blockIdx.x != 0 || gridDim.x == 1)) {
+            uint32_t* h = hist2 + ((pass - 1) & 1) * 65536;
+            const bool solo = gridDim.x == 1;
+            const int64_t zt = solo ? threadIdx.x : (int64_t)(blockIdx.x - 1) * blockDim.x + threadIdx.x;
+            const int64_t zs = solo ? blockDim.x : (int64_t)(gridDim.x - 1) * blockDim.x;
+            for (int64_t i = zt; i < 65536; i += zs) h[i] = 0;
+        }
+        grid.sync();
+    }
+    const unsigned long long T = __ldcg(&st->prefix);
+    for (int64_t c = gt; c < cols; c += gs) {
+        int l = 0, h;
+        while (l < kBins && key_of(cm[c], l) < T) ++l;
+        h = l;
+        while (h < kBins && key_of(cm[c], h) == T) ++h;
+        lo[c] = (uint8_t)l;
+        hi[c] = (uint8_t)h;
+    }
+}
+
+// Single-pass tie ranks (decoupled look-back): tiles of kEqBlock2 elements
+// are claimed in order from a counter; a tile publishes its tie count (flag
+// A), then warp 0 looks back 32 predecessors at a time, adding counts until
+// a predecessor with an inclusive prefix (flag P), and publishes its own
+// inclusive prefix -- eq_count + scan + apply as one pass over q.
+constexpr unsigned long long kLbA = 1ull << 62, kLbP = 2ull << 62, kLbMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kPrThreads) k_apply3(const int8_t* __restrict__ q, const uint8_t* __restrict__ lo,
                                                         const uint8_t* __restrict__ hi, int64_t n, int64_t cols,
                                                         bool vec, const SelectState* __restrict__ st,
-                                                        const uint32_t* __restrict__ blk_prefix,
-                                                        int8_t* __restrict__ out) {
+                                                        unsigned long long* __restrict__ look,
+                                                        uint32_t* __restrict__ tile_ctr, int8_t* __restrict__ out) {
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
     const unsigned long long r_keep = st->k;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int8_t v[kEqSub][16];
     uint32_t ltm[kEqSub], eqm[kEqSub];
 #pragma unroll
     for (int r = 0; r < kEqSub; ++r)
-        flags16(q, lo, hi, n, cols, (int64_t)blockIdx.x * kEqBlock2 + r * kEqBlock + threadIdx.x * 16, vec, v[r],
-                ltm[r], eqm[r]);
+        flags16(q, lo, hi, n, cols, tile * kEqBlock2 + r * kEqBlock + threadIdx.x * 16, vec, v[r], ltm[r], eqm[r]);
     __shared__ uint32_t ws[kEqSub][kPrThreads / 32];
-    // tie ranks in row-major order: sub-tile r before r + 1, thread t before t + 1
     uint32_t inc[kEqSub];
 #pragma unroll
     for (int r = 0; r < kEqSub; ++r) {
@@ -418,7 +321,39 @@ __global__ void __launch_bounds__(kPrThreads) k_apply2(const int8_t* __restrict_
         if (lane == 31) ws[r][w] = inc[r];
     }
     __syncthreads();
-    unsigned long long base = blk_prefix[blockIdx.x];
+    if (w == 0) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int r = 0; r < kEqSub; ++r) tot += lane < kPrThreads / 32 ? ws[r][lane] : 0u;
+        tot = __reduce_add_sync(0xffffffffu, tot);
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            if (lane == 0) atomicExch(&look[0], kLbP | tot);
+        } else {
+            if (lane == 0) atomicExch(&look[tile], kLbA | tot);
+            int64_t j = tile - 1;  // window [j - 31, j], lane l reads j - l
+            while (true) {
+                unsigned long long f = kLbP;  // before tile 0: an empty inclusive prefix
+                if (j - lane >= 0) {
+                    do f = *((volatile unsigned long long*)&look[j - lane]);
+                    while ((f & ~kLbMask) == 0);
+                }
+                const uint32_t pm = __ballot_sync(0xffffffffu, (f & ~kLbMask) == kLbP);
+                const int stop = pm ? __ffs(pm) - 1 : 32;  // nearest predecessor with a prefix
+                const unsigned long long add = lane <= stop ? (f & kLbMask) : 0ull;
+                unsigned long long sum = add;
+#pragma unroll
+                for (int d = 16; d; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+                excl += sum;
+                if (pm) break;
+                j -= 32;
+            }
+            if (lane == 0) atomicExch(&look[tile], kLbP | (excl + tot));
+        }
+        if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    unsigned long long base = s_excl;
 #pragma unroll
     for (int r = 0; r < kEqSub; ++r) {
         uint32_t before = 0, total = 0;
@@ -434,12 +369,12 @@ __global__ void __launch_bounds__(kPrThreads) k_apply2(const int8_t* __restrict_
             if (rank < r_keep) zero |= e & (0u - e);
             ++rank;
         }
-        const int64_t i0 = (int64_t)blockIdx.x * kEqBlock2 + r * kEqBlock + threadIdx.x * 16;
+        const int64_t i0 = tile * kEqBlock2 + r * kEqBlock + threadIdx.x * 16;
         if (vec && i0 + 16 <= n) {
             uint32_t o[4];
             memcpy(o, v[r], 16);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)  // 4 zero bits -> 4 byte masks
+            for (int k = 0; k < 4; ++k)
                 o[k] &= ~((((zero >> (4 * k)) & 15u) * 0x00204081u & 0x01010101u) * 0xFFu);
             *reinterpret_cast<uint4*>(out + i0) = make_uint4(o[0], o[1], o[2], o[3]);
         } else {
@@ -723,18 +658,28 @@ extern "C" int dc_prune_scores(const int8_t* q, const double* cm, int64_t rows, 
     return DC_OK;
 }
 
+static int64_t colhist3_rb(int64_t rows, int64_t cols) {
+    const int64_t n_cb = (cols + kH3Cols - 1) / kH3Cols;
+    int64_t n_rb = (2 * (int64_t)sm_count_pr() + n_cb - 1) / n_cb;
+    n_rb = n_rb < 1 ? 1 : (n_rb > 64 ? 64 : n_rb);
+    return n_rb > rows ? (rows > 0 ? rows : 1) : n_rb;
+}
+
 extern "C" int dc_prune_scratch_bytes(int64_t rows, int64_t cols, uint64_t* out) {
     const int64_t n = rows * cols;
-    const uint64_t n_cb = (uint64_t)((cols + kHcCols - 1) / kHcCols);
-    *out = 8ull * 65536 + 64 + 4ull * (uint64_t)((n + kEqBlock - 1) / kEqBlock) + 4ull * (uint64_t)cols * kBins + 256 +
-           2ull * (uint64_t)cols + 256 + 4ull * kHcCols * kBins * n_cb * 16 + 256;
+    const uint64_t n_cb = (uint64_t)((cols + kH3Cols - 1) / kH3Cols);
+    const uint64_t tiles = (uint64_t)((n + kEqBlock2 - 1) / kEqBlock2);
+    *out = 4ull * 2 * 65536 + 4ull * 2 * 4096 + 64 + 256 + 8ull * tiles + 256 + 4ull * (uint64_t)cols * kBins + 256 +
+           2ull * (uint64_t)cols + 256 + 4ull * kH3Cols * kBins * n_cb * (uint64_t)colhist3_rb(rows, cols) + 256;
     return DC_OK;
 }
 
+// Per tensor: (column, |q|) histogram -> one cooperative selection launch ->
+// one look-back apply pass (5 launches + 2 memsets, was 20).
 extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, int64_t cols, int64_t k,
                                int8_t* out, uint8_t* scratch, void* stream) {
     if (rows < 0 || cols < 0 || k < 0 || k > rows * cols) return DC_ERR_ARG;
-    if (rows * cols > 0xFFFFFFFFll) {  // selection partials are summed in 32 bits
+    if (rows * cols > 0xFFFFFFFFll) {  // selection bins are u32
         set_error_msg("dc_prune_tensor: at most 2^32 - 1 elements per tensor");
         return DC_ERR_ARG;
     }
@@ -749,57 +694,78 @@ extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, 
         }
         return DC_OK;
     }
+    auto align = [](uint8_t* p) {
+        return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255);
+    };
     uint8_t* p = scratch;
-    auto* hist = reinterpret_cast<unsigned long long*>(p);
-    p += 8ull * 65536;
+    auto* hist2 = reinterpret_cast<uint32_t*>(p);
+    p += 4ull * 2 * 65536;
+    auto* psum = reinterpret_cast<uint32_t*>(p);
+    p += 4ull * 2 * 4096;
     auto* sel = reinterpret_cast<SelectState*>(p);
     p += 64;
-    const int64_t nblk = (n + kEqBlock - 1) / kEqBlock;
-    auto* blk = reinterpret_cast<uint32_t*>(p);
-    p += 4ull * nblk;
-    p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255);
+    auto* tile_ctr = reinterpret_cast<uint32_t*>(p);
+    p = align(p + 4);
+    const int64_t tiles = (n + kEqBlock2 - 1) / kEqBlock2;
+    auto* look = reinterpret_cast<unsigned long long*>(p);
+    p = align(p + 8ull * tiles);
     auto* counts = reinterpret_cast<uint32_t*>(p);
-
-    p += 4ull * cols * kBins;
-    p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255);
+    p = align(p + 4ull * cols * kBins);
     uint8_t* lo = p;
     uint8_t* hi = p + cols;
-    p += 2ull * cols;
-    p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255);
+    p = align(p + 2ull * cols);
     auto* partial = reinterpret_cast<uint32_t*>(p);
+    const bool vec = cols % 16 == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(out) & 15) == 0;
 
     k_sel_init<<<1, 1, 0, st>>>(sel, (unsigned long long)k);  // (a pageable H2D copy would synchronize)
     DC_CHECK_LAUNCH("k_sel_init");
-    // (column, |q|) histogram: <= 16 row blocks, ~4 CTAs per SM
-    const int64_t n_cb = (cols + kHcCols - 1) / kHcCols;
-    int64_t n_rb = (4 * 148 + n_cb - 1) / n_cb;
-    n_rb = n_rb < 1 ? 1 : (n_rb > 16 ? 16 : n_rb);
-    if (n_rb > rows) n_rb = rows;
+    const int64_t n_cb = (cols + kH3Cols - 1) / kH3Cols;
+    int64_t n_rb = colhist3_rb(rows, cols);
     const int64_t rows_per = (rows + n_rb - 1) / n_rb;
     n_rb = (rows + rows_per - 1) / rows_per;
-    k_colhist2<<<dim3((unsigned)n_rb, (unsigned)n_cb), kPrThreads, 0, st>>>(q, rows, cols, rows_per, partial);
-    DC_CHECK_LAUNCH("k_colhist2");
-    k_colhist_sum<<<(unsigned)((cols * kBins + 255) / 256 < 1184 ? (cols * kBins + 255) / 256 : 1184), 256, 0, st>>>(partial, n_rb, n_cb, cols,
-                                                                                          counts);
-    DC_CHECK_LAUNCH("k_colhist_sum");
-    for (int pass = 0; pass < 4; ++pass) {
-        cudaMemsetAsync(hist, 0, 8ull * 65536, st);
-        k_select_hist<<<592, 256, 0, st>>>(counts, cm, cols, 48 - 16 * pass, sel, hist);
-        DC_CHECK_LAUNCH("k_select_hist");
-        k_select_pick2<<<1, 1024, 0, st>>>(hist, sel);
-        DC_CHECK_LAUNCH("k_select_pick2");
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_colhist3, cudaFuncAttributeMaxDynamicSharedMemorySize, kH3Cols * kBins * 4);
+        attr = true;
     }
-    k_col_bounds<<<(unsigned)((cols + 255) / 256 < 1184 ? (cols + 255) / 256 : 1184), 256, 0, st>>>(cm, cols, sel, lo, hi);
-    DC_CHECK_LAUNCH("k_col_bounds");
-    const bool vec = cols % 16 == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
-                     (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    const int64_t nblk2 = (n + kEqBlock2 - 1) / kEqBlock2;  // <= nblk: fits the scratch
-    k_eq_count2<<<(unsigned)nblk2, kPrThreads, 0, st>>>(q, lo, hi, n, cols, vec, blk);
-    DC_CHECK_LAUNCH("k_eq_count2");
-    k_excl_scan<<<1, 1024, 0, st>>>(blk, nblk2);
-    DC_CHECK_LAUNCH("k_excl_scan");
-    k_apply2<<<(unsigned)nblk2, kPrThreads, 0, st>>>(q, lo, hi, n, cols, vec, sel, blk, out);
-    DC_CHECK_LAUNCH("k_apply2");
+    k_colhist3<<<dim3((unsigned)n_rb, (unsigned)n_cb), kH3Threads, kH3Cols * kBins * 4, st>>>(q, rows, cols, rows_per,
+                                                                                           vec, partial);
+    DC_CHECK_LAUNCH("k_colhist3");
+    const int64_t sb = (cols * kBins + 255) / 256;
+    k_colhist3_sum<<<(unsigned)(sb < 1184 ? sb : 1184), 256, 0, st>>>(partial, n_rb, n_cb, cols, counts);
+    DC_CHECK_LAUNCH("k_colhist3_sum");
+    {  // the k-th score and the per-column bounds: one cooperative launch
+        cudaError_t ez = cudaMemsetAsync(hist2, 0, 4ull * 2 * 65536 + 4ull * 2 * 4096, st);  // hist2 + psum2
+        if (ez != cudaSuccess) {
+            set_error("prune memset", ez);
+            return DC_ERR_CUDA;
+        }
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_coop, kSelThreads, 0);
+        if (per_sm < 1) {
+            set_error_msg("k_select_coop: not resident");
+            return DC_ERR_CUDA;
+        }
+        int grid = sm_count_pr();
+        if (grid > 4096) grid = 4096;
+        void* args[] = {(void*)&counts, (void*)&cm, (void*)&cols, (void*)&sel, (void*)&hist2, (void*)&psum,
+                        (void*)&lo, (void*)&hi};
+        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_select_coop, dim3((unsigned)grid), dim3(kSelThreads),
+                                                    args, 0, st);
+        if (e != cudaSuccess) {
+            set_error("k_select_coop", e);
+            return DC_ERR_CUDA;
+        }
+    }
+    cudaError_t e = cudaMemsetAsync(tile_ctr, 0, 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(look, 0, 8ull * tiles, st);
+    if (e != cudaSuccess) {
+        set_error("prune memset", e);
+        return DC_ERR_CUDA;
+    }
+    k_apply3<<<(unsigned)tiles, kPrThreads, 0, st>>>(q, lo, hi, n, cols, vec, sel, look, tile_ctr, out);
+    DC_CHECK_LAUNCH("k_apply3");
     return DC_OK;
 }
 
