@@ -3,14 +3,17 @@
 // lowest score cm[c] * |q[r,c]| (f64), ties broken by flat row-major index
 // (np.argsort kind="stable").  No sort is needed:
 //   per tensor: scores take at most cols * 129 distinct values, so one pass
-//     builds the (column, |q|) histogram; a 4 x 16-bit radix select over
-//     those weighted keys finds the k-th smallest score T and how many of
-//     the ties r must go; a final ordered pass zeroes score < T and the
-//     first r entries with score == T (block counts + exclusive scan).
+//     builds the (column, |q|) histogram; a radix select over those weighted
+//     keys (20 bits grid-wide, the rest over the few candidates left) finds
+//     the k-th smallest score T and how many ties r must go; the ties live
+//     only in the columns where some |q| scores exactly T, so the flat index
+//     of the r-th tie (row-major) is found by scanning just those columns;
+//     a streaming pass then zeroes score < T and the ties up to that index.
 //   per row: one CTA per row, 8 x 8-bit radix select in shared memory and
 //     the same ordered tie pass.
 // Non-negative doubles order like their u64 bit patterns, so keys are bits.
 #include <cooperative_groups.h>
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -20,12 +23,16 @@ namespace dc {
 
 constexpr int kPrThreads = 256;
 constexpr int kBins = 129;  // |q| in 0..128
-constexpr int kEqBlock = 4096;
 
-struct SelectState {
-    unsigned long long prefix;  // key bits selected so far
-    unsigned long long k;       // 1-based rank still to find within the prefix bucket
-    unsigned long long below;   // elements with key < current bucket
+constexpr int kSelThreads = 512;
+constexpr int kSelHBins = 4096;  // 12-bit digit passes (two), in shared memory
+
+struct SelectOut {
+    unsigned long long T;         // the k-th smallest score's bits
+    unsigned long long kk;        // ties (score == T) to zero, the first kk in row-major order
+    unsigned long long eq_total;  // elements with score == T
+    unsigned long long cut;       // flat index of the last tie to zero (~0: every tie goes)
+    uint32_t n_cand, n_eqc, bin, pad;
 };
 
 __device__ __forceinline__ unsigned long long key_of(double cm, int a) {
@@ -34,356 +41,630 @@ __device__ __forceinline__ unsigned long long key_of(double cm, int a) {
 
 __device__ __forceinline__ int absq(int8_t v) { return v < 0 ? -(int)v : (int)v; }
 
-__global__ void k_sel_init(SelectState* st, unsigned long long k) {
-    st->prefix = 0;
-    st->k = k;
-    st->below = 0;
-}
+// ------------------------------------------------------------ per tensor
+// (column, |q|) histogram, conflict-free: a CTA covers 128 columns, each warp
+// one row per step with lane L loading the 4 bytes of columns 4L..4L+3; the
+// shared bins are laid out [|q|][e][lane] so the atomic for byte e of every
+// lane lands in bank L whatever the |q| values (the round-1 column-major bins
+// took random-bank conflicts and same-address collisions: ~2.5x slower).
+// Row blocks (<= 65535 rows, so u16 counts) write partial histograms in the
+// same layout; k_colhist4_sum adds them up.
+constexpr int kH4Cols = 128;
+constexpr int kH4Threads = 512;
+constexpr int kH4Unr = 8;
+constexpr int kH4Words = kBins * kH4Cols;  // [a][e][lane]
+constexpr int kH4Smem = kH4Words * 4;
 
-// ------------------------------------------------- per tensor, fast path
-// (column, |q|) histogram: CTA = 64 columns x a row range, u32 bins in
-// shared memory (thread = column x row phase, coalesced byte loads), partial
-// histograms written whole (no global atomics) and summed by k_colhist_sum.
-constexpr int kHcCols = 64;
-
-// 16 consecutive elements per thread (one 4096-element block per CTA):
-// lt / eq flags from the column bounds, no f64 work per element
-__device__ __forceinline__ void flags16(const int8_t* __restrict__ q, const uint8_t* __restrict__ lo,
-                                        const uint8_t* __restrict__ hi, int64_t n, int64_t cols, int64_t i0,
-                                        bool vec, int8_t (&v)[16], uint32_t& ltm, uint32_t& eqm) {
-    ltm = eqm = 0;
-    if (vec && i0 + 16 <= n) {  // cols % 16 == 0: one row, 16-B aligned
-        const int64_t c0 = (uint32_t)i0 % (uint32_t)cols;  // n < 2^32 (dc_prune_tensor): 32-bit division
-        const uint4 qv = *reinterpret_cast<const uint4*>(q + i0);
-        const uint4 lv = *reinterpret_cast<const uint4*>(lo + c0);
-        const uint4 hv = *reinterpret_cast<const uint4*>(hi + c0);
-        memcpy(v, &qv, 16);
-        // four bytes per SIMD op: |q| (0x80 -> 128, unsigned), byte compares
-        // against the column bounds, byte masks folded to 4 bits each
-        const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w},
-                       hw[4] = {hv.x, hv.y, hv.z, hv.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t a = __vabs4(qw[k]);
-            const uint32_t lt = __vcmpltu4(a, lw[k]);
-            const uint32_t eq = __vcmpltu4(a, hw[k]) & ~lt;
-            ltm |= (((lt & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
-            eqm |= (((eq & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
-        }
-        return;
-    }
-    int64_t c = (uint32_t)i0 % (uint32_t)cols;
-    for (int k = 0; k < 16; ++k) {
-        const int64_t i = i0 + k;
-        v[k] = 0;
-        if (i < n) {
-            v[k] = q[i];
-            const int a = absq(v[k]);
-            ltm |= (uint32_t)(a < lo[c]) << k;
-            eqm |= (uint32_t)(a >= lo[c] && a < hi[c]) << k;
-        }
-        if (++c == cols) c = 0;
-    }
-}
-
-// Fast per-element passes: a block covers kEqSub sub-tiles of kEqBlock
-// elements (thread t: 16 elements at sub-tile r, offset 16t); all kEqSub
-// 16-B loads are issued before any use, so each thread keeps 4 in flight.
-constexpr int kEqSub = 4;
-constexpr int64_t kEqBlock2 = (int64_t)kEqSub * kEqBlock;
-
-// ------------------------------------------- per tensor, round-2 path
-// (column, |q|) histogram with 16-byte loads: a CTA is 8 column groups of 16
-// columns (one uint4 per row each) x 128 row phases, 4 rows in flight per
-// thread; u32 bins for its 128 columns in shared memory; partial histograms
-// per row block, summed by k_colhist3_sum.
-constexpr int kH3Cols = 128;
-constexpr int kH3Threads = 1024;
-
-__global__ void __launch_bounds__(kH3Threads, 2) k_colhist3(const int8_t* __restrict__ q, int64_t rows, int64_t cols,
-                                                             int64_t rows_per, bool vec, uint32_t* __restrict__ partial) {
-    extern __shared__ uint32_t hb[];  // [kH3Cols][kBins]
-    for (int i = threadIdx.x; i < kH3Cols * kBins; i += blockDim.x) hb[i] = 0;
+__global__ void __launch_bounds__(kH4Threads, 3) k_colhist4(const int8_t* __restrict__ q, int64_t rows, int64_t cols,
+                                                             int64_t rows_per, bool vec4,
+                                                             uint16_t* __restrict__ partial) {
+    extern __shared__ __align__(16) uint32_t hb[];
+    for (int i = threadIdx.x; i < kH4Words / 4; i += blockDim.x) reinterpret_cast<uint4*>(hb)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    const int cg8 = threadIdx.x & 7, rph = threadIdx.x >> 3;  // 8 column groups x 128 row phases
-    const int64_t c0 = (int64_t)blockIdx.y * kH3Cols + cg8 * 16;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = kH4Threads / 32;
+    const int64_t c0 = (int64_t)blockIdx.y * kH4Cols + lane * 4;
     const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(rows, r0 + rows_per);
-    uint32_t* b = hb + cg8 * 16 * kBins;
-    if (vec && c0 + 16 <= cols) {
-        for (int64_t r = r0 + rph; r < r1; r += 4 * (kH3Threads / 8)) {
-            uint4 v[4];
+    uint32_t* hl = hb + lane;
+#ifdef DC_PRUNE_NOATOMS
+    uint32_t sink = 0;
+#endif
+    if (vec4) {  // cols % 4 == 0, q 4-byte aligned
+        if (c0 < cols) {
+            const int8_t* p = q + c0;
+            for (int64_t r = r0 + warp; r < r1; r += nwarp * kH4Unr) {
+                uint32_t w[kH4Unr];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int64_t rr = r + j * (kH3Threads / 8);
-                v[j] = rr < r1 ? __ldg(reinterpret_cast<const uint4*>(q + rr * cols + c0)) : make_uint4(0, 0, 0, 0);
-            }
+                for (int u = 0; u < kH4Unr; ++u) {
+                    const int64_t rr = r + u * nwarp;
+                    w[u] = rr < r1 ? __ldg(reinterpret_cast<const uint32_t*>(p + rr * cols)) : 0u;
+                }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (r + j * (kH3Threads / 8) >= r1) break;
-                const uint32_t w[4] = {__vabs4(v[j].x), __vabs4(v[j].y), __vabs4(v[j].z), __vabs4(v[j].w)};
+                for (int u = 0; u < kH4Unr; ++u) {
+                    if (r + u * nwarp >= r1) break;
+                    const uint32_t a4 = __vabs4(w[u]);  // 0x80 -> 128 (unsigned)
+#ifdef DC_PRUNE_NOATOMS
+                    sink += a4;
+#else
 #pragma unroll
-                for (int e = 0; e < 16; ++e) atomicAdd(&b[e * kBins + ((w[e >> 2] >> (8 * (e & 3))) & 0xFF)], 1u);
+                    for (int e = 0; e < 4; ++e) atomicAdd(hl + ((a4 >> (8 * e)) & 0xFFu) * kH4Cols + e * 32, 1u);
+#endif
+                }
             }
         }
     } else {
-        for (int64_t r = r0 + rph; r < r1; r += kH3Threads / 8)
-            for (int e = 0; e < 16 && c0 + e < cols; ++e) atomicAdd(&b[e * kBins + absq(q[r * cols + c0 + e])], 1u);
+        for (int64_t r = r0 + warp; r < r1; r += nwarp)
+            for (int e = 0; e < 4; ++e)
+                if (c0 + e < cols) atomicAdd(hl + absq(q[r * cols + c0 + e]) * kH4Cols + e * 32, 1u);
     }
+#ifdef DC_PRUNE_NOATOMS
+    hl[0] += sink;
+#endif
     __syncthreads();
-    uint32_t* out = partial + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * (kH3Cols * kBins);
-    for (int i = threadIdx.x; i < kH3Cols * kBins; i += blockDim.x) out[i] = hb[i];
-}
-
-// counts[c * 129 + a] = sum over row blocks of the k_colhist3 partials
-__global__ void k_colhist3_sum(const uint32_t* __restrict__ partial, int64_t n_rb, int64_t n_cb, int64_t cols,
-                               uint32_t* __restrict__ counts) {
-    const int64_t per_rb = n_cb * kH3Cols * kBins;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols * kBins;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t s = 0;
-        for (int64_t rb = 0; rb < n_rb; ++rb) s += partial[rb * per_rb + i];
-        counts[i] = s;
+    uint32_t* out = reinterpret_cast<uint32_t*>(partial + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * kH4Words);
+    for (int i = threadIdx.x; i < kH4Words / 2; i += blockDim.x) {
+        const uint2 v = reinterpret_cast<const uint2*>(hb)[i];
+        out[i] = v.x | (v.y << 16);
     }
 }
 
-// Block-wide: find the entry of v[0..m) (m <= blockDim.x, u32 counts) holding
-// rank k (1-based) given `base` = count before v[0]; returns index and the
-// count before it through shared memory.  All threads participate.
-__device__ __forceinline__ void block_find(const uint32_t* v, int m, unsigned long long k, unsigned long long base,
-                                           int* s_idx, unsigned long long* s_before, unsigned long long* wsum) {
+// Same with 16-byte loads: lane L holds columns 16L..16L+15 of a row (a warp
+// reads 512 contiguous bytes), counters are u16 pairs (even / odd column of
+// the lane's 16) in words laid out [|q|][e / 2][lane]: still bank L for every
+// lane, 132 KB of shared bins for 512 columns, one CTA of 32 warps per SM.
+constexpr int kH5Cols = 512;
+constexpr int kH5Threads = 1024;
+constexpr int kH5Unr = 4;
+constexpr int kH5Words = kBins * kH5Cols / 2;  // [a][e/2 (8)][lane (32)], u16 pairs
+constexpr int kH5Smem = kH5Words * 4;
+
+__global__ void __launch_bounds__(kH5Threads, 1) k_colhist5(const int8_t* __restrict__ q, int64_t rows, int64_t cols,
+                                                             int64_t rows_per, uint32_t* __restrict__ partial) {
+    extern __shared__ __align__(16) uint32_t hb[];
+    for (int i = threadIdx.x; i < kH5Words / 4; i += blockDim.x) reinterpret_cast<uint4*>(hb)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = kH5Threads / 32;
+    const int64_t c0 = (int64_t)blockIdx.y * kH5Cols + lane * 16;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(rows, r0 + rows_per);
+    uint32_t* hl = hb + lane;
+#ifdef DC_PRUNE_NOATOMS
+    uint32_t sink = 0;
+#endif
+    if (c0 < cols) {  // cols % 16 == 0, q 16-byte aligned (caller)
+        const int8_t* p = q + c0;
+        for (int64_t r = r0 + warp; r < r1; r += nwarp * kH5Unr) {
+            uint4 v[kH5Unr];
+#pragma unroll
+            for (int u = 0; u < kH5Unr; ++u) {
+                const int64_t rr = r + u * nwarp;
+                v[u] = rr < r1 ? __ldcs(reinterpret_cast<const uint4*>(p + rr * cols)) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < kH5Unr; ++u) {
+                if (r + u * nwarp >= r1) break;
+                const uint32_t w[4] = {__vabs4(v[u].x), __vabs4(v[u].y), __vabs4(v[u].z), __vabs4(v[u].w)};
+#ifdef DC_PRUNE_NOATOMS
+                sink += w[0] + w[1] + w[2] + w[3];
+#else
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    atomicAdd(hl + ((w[e >> 2] >> (8 * (e & 3))) & 0xFFu) * (kH5Cols / 2) + (e >> 1) * 32,
+                              (e & 1) ? 0x10000u : 1u);
+#endif
+            }
+        }
+    }
+#ifdef DC_PRUNE_NOATOMS
+    hl[0] += sink & 1;
+#endif
+    __syncthreads();
+    uint4* out = reinterpret_cast<uint4*>(partial + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * kH5Words);
+    for (int i = threadIdx.x; i < kH5Words / 4; i += blockDim.x) out[i] = reinterpret_cast<const uint4*>(hb)[i];
+}
+
+// counts[c * 129 + a] from the k_colhist5 partials (u16 pairs)
+__global__ void k_colhist5_sum(const uint32_t* __restrict__ partial, int64_t n_rb, int64_t n_cb, int64_t cols,
+                               uint32_t* __restrict__ counts, uint32_t* __restrict__ hist,
+                               uint32_t* __restrict__ eqmask, SelectOut* __restrict__ so) {
+    const int64_t per_rb = n_cb * kH5Words;
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = gt; i < per_rb; i += gs) {
+        const uint32_t cb = (uint32_t)(i / kH5Words), rem = (uint32_t)(i - (int64_t)cb * kH5Words);
+        const uint32_t a = rem / (kH5Cols / 2), slot = rem % (kH5Cols / 2);  // slot = (e/2) * 32 + lane
+        const int64_t c = (int64_t)cb * kH5Cols + (slot & 31) * 16 + (slot >> 5) * 2;
+        uint32_t s0 = 0, s1 = 0;
+        for (int64_t rb = 0; rb < n_rb; rb += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = rb + u < n_rb ? partial[(rb + u) * per_rb + i] : 0u;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                s0 += v[u] & 0xFFFFu;
+                s1 += v[u] >> 16;
+            }
+        }
+        if (c < cols) counts[c * kBins + a] = s0;
+        if (c + 1 < cols) counts[(c + 1) * kBins + a] = s1;
+    }
+    for (int64_t i = gt; i < 2 * kSelHBins / 4; i += gs) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0, 0, 0, 0);
+    for (int64_t i = gt; i < (cols + 31) / 32; i += gs) eqmask[i] = 0;
+    if (gt == 0) so->n_cand = 0;
+}
+
+// counts[c * 129 + a] = sum over row blocks of the k_colhist4 partials (read
+// in their layout, coalesced; n_rb loads in flight); also zeroes k_select4's
+// histograms, tie-column bits and candidate counter.
+__global__ void k_colhist4_sum(const uint16_t* __restrict__ partial, int64_t n_rb, int64_t n_cb, int64_t cols,
+                               uint32_t* __restrict__ counts, uint32_t* __restrict__ hist,
+                               uint32_t* __restrict__ eqmask, SelectOut* __restrict__ so) {
+    const int64_t per_rb = n_cb * kH4Words;
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = gt; i < per_rb; i += gs) {
+        const uint32_t cb = (uint32_t)(i / kH4Words), rem = (uint32_t)(i - (int64_t)cb * kH4Words);
+        const uint32_t a = rem / kH4Cols, slot = rem % kH4Cols;
+        const int64_t c = (int64_t)cb * kH4Cols + (slot & 31) * 4 + (slot >> 5);
+        uint32_t s = 0;
+        for (int64_t rb = 0; rb < n_rb; rb += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = rb + u < n_rb ? partial[(rb + u) * per_rb + i] : 0u;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        if (c < cols) counts[c * kBins + a] = s;
+    }
+    for (int64_t i = gt; i < 2 * kSelHBins / 4; i += gs) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0, 0, 0, 0);
+    for (int64_t i = gt; i < (cols + 31) / 32; i += gs) eqmask[i] = 0;
+    if (gt == 0) so->n_cand = 0;
+}
+
+// The whole k-th-score selection and the tie cut in ONE cooperative launch
+// (grid = SMs, 4 grid barriers, 6 when only some ties stay):
+//   A  every CTA: histogram of the top 12 key bits (sign + exponent) of its
+//      (column, |q|) items in shared memory, flushed with one global atomic
+//      per non-empty bin; every CTA then picks the bin holding rank k;
+//   A2 the same for the next 12 bits, over the items inside that exponent
+//      (global atomics on a few thousand hot bins of a flat 2^20-bin table
+//      were 20 us of L2 atomic serialization);
+//   D  every CTA appends the items whose top 24 key bits match to a list;
+//   E  every CTA redundantly: the k-th key among those (few) candidates by
+//      direct rank comparison in shared memory (8-bit radix passes from L2
+//      when there are many) -> T, the ties to zero (kk), the entries == T;
+//   F  every CTA, its own column slice: |q| bounds of score < T and score ==
+//      T by binary search (keys are nondecreasing in |q|) and a bit per
+//      column holding ties;
+//   G/H only when some ties stay: ties (only in those columns) counted per
+//      CTA over row ranges; the CTA holding the kk-th tie in row-major order
+//      records its flat index as the cut.
+// Loops over global data batch their loads (the serial L2 round trips of a
+// plain loop dominated).  Replaces a 4 x 16-bit grid-wide radix select (12
+// grid barriers) and the look-back tie scan of the round-1 apply pass.
+// rank-k entry of v[0..m) for any m: thread t sums a contiguous run of
+// ceil(m / blockDim) entries (independent loads), one block scan picks the run,
+// its owner walks it.  Returns the index; `base` becomes the count before it.
+__device__ int block_find_all(const uint32_t* v, bool gmem, int m, unsigned long long k, unsigned long long& base,
+                              int* s_idx, unsigned long long* s_before, unsigned long long* wsum) {
+    const int per = (m + blockDim.x - 1) / blockDim.x;
+    const int j0 = threadIdx.x * per, j1 = min(m, j0 + per);
+    auto ld = [&](int j) -> uint32_t { return j < j1 ? (gmem ? __ldcg(v + j) : v[j]) : 0u; };
+    unsigned long long x = 0;
+    for (int j = j0; j < j1; j += 8) {  // 8 independent loads in flight
+        uint32_t e[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) e[u] = ld(j + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x += e[u];
+    }
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const unsigned long long x = t < m ? __ldcg(v + t) : 0ull;  // written by other CTAs: bypass L1
     unsigned long long inc = x;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
         if (lane >= d) inc += o;
     }
+    if (t == 0) *s_idx = m - 1;  // unreachable for 1 <= k <= total
     if (lane == 31) wsum[w] = inc;
     __syncthreads();
     unsigned long long before = base;
     for (int i = 0; i < w; ++i) before += wsum[i];
     inc += before;
-    if (t < m && inc - x < k && k <= inc) {
-        *s_idx = t;
-        *s_before = inc - x;
+    if (j0 < j1 && inc - x < k && k <= inc) {
+        unsigned long long c = inc - x;
+        bool found = false;
+        for (int j = j0; j < j1 && !found; j += 8) {
+            uint32_t e[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) e[u] = ld(j + u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (!found && j + u < j1 && k <= c + e[u]) {
+                    *s_idx = j + u;
+                    *s_before = c;
+                    found = true;
+                }
+                c += e[u];
+            }
+        }
     }
     __syncthreads();
+    const int idx = *s_idx;
+    base = *s_before;
+    __syncthreads();
+    return idx;
 }
 
-// The whole k-th-score selection in ONE cooperative launch (grid = SMs):
-// per 16-bit digit pass, a grid-strided (column, |q|) histogram with
-// warp-aggregated atomics into u32 bins (n < 2^32), per-CTA slice sums, and
-// CTA 0 picks the slice and then the bin with block scans; the two histogram
-// buffers alternate so the next pass's zeroing overlaps the pick.  Then the
-// per-column |q| bounds of score < T and score == T.  Replaces 4 x (memset,
-// k_select_hist, k_select_pick2) + k_col_bounds (13 launches).
-constexpr int kSelThreads = 512;
+// exclusive prefix of a 0/1 flag over the CTA (in thread order) + total
+__device__ __forceinline__ uint32_t block_excl(bool f, uint32_t* wcnt, uint32_t& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t m = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wcnt[w] = __popc(m);
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
+    for (int i = 0; i < (int)blockDim.x / 32; ++i) {
+        before += i < w ? wcnt[i] : 0u;
+        tot += wcnt[i];
+    }
+    __syncthreads();
+    total = tot;
+    return before + __popc(m & ((1u << lane) - 1u));
+}
 
-__global__ void __launch_bounds__(kSelThreads) k_select_coop(const uint32_t* __restrict__ counts,
-                                                             const double* __restrict__ cm, int64_t cols,
-                                                             SelectState* __restrict__ st, uint32_t* __restrict__ hist2,
-                                                             uint32_t* __restrict__ psum2, uint8_t* __restrict__ lo,
-                                                             uint8_t* __restrict__ hi) {
-    // hist2 / psum2: two buffers each (pass parity), zeroed by the host before
-    // the launch; the buffer of pass p + 2 is re-zeroed during pass p + 1's pick
+constexpr int kCandCap = 1024;  // candidates cached in shared memory (else re-read from L2)
+constexpr int kEqCap = 4096;    // tie columns listed in shared memory (else whole rows are scanned)
+constexpr int kUnr = 8;
+
+__global__ void __launch_bounds__(kSelThreads) k_select4(const uint32_t* __restrict__ counts,
+                                                         const double* __restrict__ cm, const int8_t* __restrict__ q,
+                                                         int64_t rows, int64_t cols, unsigned long long k,
+                                                         SelectOut* __restrict__ so, uint32_t* __restrict__ hist,
+                                                         uint32_t* __restrict__ psum, uint32_t* __restrict__ cand,
+                                                         uint32_t* __restrict__ eqmask, uint8_t* __restrict__ bound,
+                                                         uint8_t* __restrict__ lo, uint8_t* __restrict__ hi) {
+    // hist (2 x 4096 u32), eqmask and so->n_cand are zeroed by k_colhist4_sum
     cg::grid_group grid = cg::this_grid();
     const int64_t n = cols * kBins;
-    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
-    const int slice = (65536 + gridDim.x - 1) / gridDim.x;
     __shared__ unsigned long long wsum[kSelThreads / 32], s_before;
+    __shared__ uint32_t wcnt[kSelThreads / 32], h[256], hs[kSelHBins];
     __shared__ int s_idx;
-    for (int pass = 0; pass < 4; ++pass) {
-        uint32_t* hist = hist2 + (pass & 1) * 65536;
-        uint32_t* psum = psum2 + (pass & 1) * 4096;
-        const int shift = 48 - 16 * pass, top = shift + 16;
-        // st / hist / psum are written by other CTAs between grid barriers: every
-        // read of them bypasses L1 (ld.cg), which is not coherent across SMs
-        const unsigned long long prefix = __ldcg(&st->prefix);
-        // histogram of this pass's digit; the slice totals accumulate alongside
-        for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += gs) {
-            const int64_t i = base + threadIdx.x;
-            uint32_t cnt = 0, bin = 0xFFFFFFFFu;
-            if (i < n) {
-                cnt = counts[i];
-                if (cnt) {
-                    const uint32_t col = (uint32_t)i / (uint32_t)kBins;
-                    const unsigned long long key = key_of(cm[col], (int)((uint32_t)i - col * (uint32_t)kBins));
-                    if (top >= 64 || (key >> top) == prefix) bin = (uint32_t)((key >> shift) & 0xFFFF);
-                }
-            }
-            const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-            const uint32_t sum = __reduce_add_sync(peers, bin == 0xFFFFFFFFu ? 0u : cnt);
-            if (bin != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], sum);
-        }
-        grid.sync();
-        {  // per-CTA slice sums (an atomic per slice would serialise: pass 0 sends
-           // nearly every key to a handful of bins)
-            __shared__ uint32_t red[kSelThreads / 32];
-            uint32_t v = 0;
-            const int b0 = blockIdx.x * slice;
-            for (int b = b0 + threadIdx.x; b < min(65536, b0 + slice); b += blockDim.x) v += __ldcg(hist + b);
-            v = __reduce_add_sync(0xffffffffu, v);
-            if (lane == 0) red[threadIdx.x >> 5] = v;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                uint32_t t = 0;
-                for (int k = 0; k < kSelThreads / 32; ++k) t += red[k];
-                psum[blockIdx.x] = t;
-            }
-        }
-        grid.sync();
-        if (blockIdx.x == 0) {
-            const unsigned long long k = __ldcg(&st->k);
-            // windows of kSelThreads entries: (index, count before) of the rank-k entry
-            auto find = [&](const uint32_t* v, int m, unsigned long long& base) -> int {
-                for (int c0 = 0; c0 < m; c0 += kSelThreads) {
-                    if (threadIdx.x == 0) s_idx = -1;
-                    __syncthreads();
-                    block_find(v + c0, min(kSelThreads, m - c0), k, base, &s_idx, &s_before, wsum);
-                    const int idx = s_idx;
-                    if (idx >= 0) {
-                        base = s_before;
-                        __syncthreads();
-                        return c0 + idx;
-                    }
-                    for (int i = 0; i < kSelThreads / 32; ++i) base += wsum[i];
-                    __syncthreads();
-                }
-                return m - 1;  // unreachable for 1 <= k <= total
-            };
-            unsigned long long base = 0;
-            const int sl = find(psum, (int)gridDim.x, base);  // slice holding rank k
-            const int b0 = sl * slice;
-            const int bin = b0 + find(hist + b0, min(65536, b0 + slice) - b0, base);  // bin inside it
-            if (threadIdx.x == 0) {
-                st->prefix = (__ldcg(&st->prefix) << 16) | (unsigned long long)bin;
-                st->k = k - base;
-                st->below = __ldcg(&st->below) + base;
-            }
-        }
-        // the buffers of pass - 1 were consumed by its pick: zero them for pass + 1
-        if (pass >= 1 && pass < 3 && (blockIdx.x != 0 || gridDim.x == 1)) {
-            uint32_t* h = hist2 + ((pass - 1) & 1) * 65536;
-            const bool solo = gridDim.x == 1;
-            const int64_t zt = solo ? threadIdx.x : (int64_t)(blockIdx.x - 1) * blockDim.x + threadIdx.x;
-            const int64_t zs = solo ? blockDim.x : (int64_t)(gridDim.x - 1) * blockDim.x;
-            for (int64_t i = zt; i < 65536; i += zs) h[i] = 0;
-        }
-        grid.sync();
-    }
-    const unsigned long long T = __ldcg(&st->prefix);
-    for (int64_t c = gt; c < cols; c += gs) {
-        int l = 0, h;
-        while (l < kBins && key_of(cm[c], l) < T) ++l;
-        h = l;
-        while (h < kBins && key_of(cm[c], h) == T) ++h;
-        lo[c] = (uint8_t)l;
-        hi[c] = (uint8_t)h;
-    }
-}
-
-// Single-pass tie ranks (decoupled look-back): tiles of kEqBlock2 elements
-// are claimed in order from a counter; a tile publishes its tie count (flag
-// A), then warp 0 looks back 32 predecessors at a time, adding counts until
-// a predecessor with an inclusive prefix (flag P), and publishes its own
-// inclusive prefix -- eq_count + scan + apply as one pass over q.
-constexpr unsigned long long kLbA = 1ull << 62, kLbP = 2ull << 62, kLbMask = (1ull << 62) - 1;
-
-__global__ void __launch_bounds__(kPrThreads) k_apply3(const int8_t* __restrict__ q, const uint8_t* __restrict__ lo,
-                                                        const uint8_t* __restrict__ hi, int64_t n, int64_t cols,
-                                                        bool vec, const SelectState* __restrict__ st,
-                                                        unsigned long long* __restrict__ look,
-                                                        uint32_t* __restrict__ tile_ctr, int8_t* __restrict__ out) {
-    __shared__ uint32_t s_tile;
-    __shared__ unsigned long long s_excl;
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __shared__ __align__(16) unsigned char pool[kCandCap * 12 > kEqCap * 4 ? kCandCap * 12 : kEqCap * 4];
+    auto* ckey = reinterpret_cast<unsigned long long*>(pool);
+    auto* ccnt = reinterpret_cast<uint32_t*>(pool + kCandCap * 8);
+    auto* elist = reinterpret_cast<uint32_t*>(pool);
+#ifdef DC_PRUNE_TIMING
+    unsigned long long tm[12];
+    int ntm = 0;
+#define TMARK() do { if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm[ntm++])); } while (0)
+#else
+#define TMARK() do {} while (0)
+#endif
+    TMARK();
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;  // contiguous items per CTA (A and D)
+    const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n, i0 + per);
+    auto item_key = [&](uint32_t i) {
+        const uint32_t col = i / (uint32_t)kBins;
+        return key_of(cm[col], (int)(i - col * (uint32_t)kBins));
+    };
+    // ---- A: (sign, exponent) histogram in shared memory, flushed to hist[0..4096)
+    for (int j = threadIdx.x; j < kSelHBins; j += blockDim.x) hs[j] = 0;
     __syncthreads();
-    const int64_t tile = s_tile;
-    const unsigned long long r_keep = st->k;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int8_t v[kEqSub][16];
-    uint32_t ltm[kEqSub], eqm[kEqSub];
+    auto hist_pass = [&](int pass, uint32_t want) {
+        for (int64_t ib = i0 + threadIdx.x; ib < i1; ib += kUnr * blockDim.x) {
+            uint32_t c[kUnr];
 #pragma unroll
-    for (int r = 0; r < kEqSub; ++r)
-        flags16(q, lo, hi, n, cols, tile * kEqBlock2 + r * kEqBlock + threadIdx.x * 16, vec, v[r], ltm[r], eqm[r]);
-    __shared__ uint32_t ws[kEqSub][kPrThreads / 32];
-    uint32_t inc[kEqSub];
+            for (int u = 0; u < kUnr; ++u) {
+                const int64_t i = ib + (int64_t)u * blockDim.x;
+                c[u] = i < i1 ? counts[i] : 0u;
+            }
 #pragma unroll
-    for (int r = 0; r < kEqSub; ++r) {
-        inc[r] = __popc(eqm[r]);
+            for (int u = 0; u < kUnr; ++u) {
+                if (!c[u]) continue;
+                const unsigned long long key = item_key((uint32_t)(ib + (int64_t)u * blockDim.x));
+                if (pass == 0)
+                    atomicAdd(&hs[key >> 52], c[u]);
+                else if ((uint32_t)(key >> 52) == want)
+                    atomicAdd(&hs[(key >> 40) & 0xFFF], c[u]);
+            }
+        }
+        __syncthreads();
+        uint32_t* g = hist + pass * kSelHBins;
+        for (int j = threadIdx.x; j < kSelHBins; j += blockDim.x) {
+            const uint32_t v = hs[j];
+            if (v) atomicAdd(g + j, v);
+            hs[j] = 0;
+        }
+    };
+    hist_pass(0, 0);
+    TMARK();
+    grid.sync();
+    unsigned long long base = 0;
+    const uint32_t e0 = (uint32_t)block_find_all(hist, true, kSelHBins, k, base, &s_idx, &s_before, wsum);
+    // ---- A2: the next 12 bits inside that exponent
+    hist_pass(1, e0);
+    TMARK();
+    grid.sync();
+    const uint32_t bin = (e0 << 12) |
+                         (uint32_t)block_find_all(hist + kSelHBins, true, kSelHBins, k, base, &s_idx, &s_before, wsum);
+    TMARK();
+    // ---- D: candidates = items whose top 24 key bits are `bin`
+    for (int64_t ib = i0; ib < i1; ib += kUnr * blockDim.x) {
+        uint32_t c[kUnr];
+#pragma unroll
+        for (int u = 0; u < kUnr; ++u) {
+            const int64_t i = ib + (int64_t)u * blockDim.x + threadIdx.x;
+            c[u] = i < i1 ? counts[i] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnr; ++u) {
+            const int64_t i = ib + (int64_t)u * blockDim.x + threadIdx.x;
+            const bool f = c[u] && (item_key((uint32_t)i) >> 40) == bin;
+            const uint32_t m = __ballot_sync(0xffffffffu, f);
+            if (m) {
+                uint32_t pos = 0;
+                if (lane == 0) pos = atomicAdd(&so->n_cand, (uint32_t)__popc(m));
+                pos = __shfl_sync(0xffffffffu, pos, 0);
+                if (f) cand[pos + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+            }
+        }
+    }
+    TMARK();
+    grid.sync();
+    // ---- E (every CTA, same answer): the k-th key among the candidates
+    const uint32_t nc = __ldcg(&so->n_cand);
+    unsigned long long kk = k - base, T;
+    uint32_t eq_total = 0;
+    if (nc <= (uint32_t)kCandCap) {
+        // cached: each candidate's rank range [below, below + eq) by direct
+        // comparison with all others (nc is small: 24 key bits are fixed)
+        __shared__ unsigned long long s_T, s_kk;
+        __shared__ uint32_t s_eq;
+        for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
+            const uint32_t i = __ldcg(cand + j);
+            ckey[j] = item_key(i);
+            ccnt[j] = counts[i];
+        }
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
+            const unsigned long long kj = ckey[j];
+            unsigned long long below = 0;
+            uint32_t eq = 0;
+            for (uint32_t i = 0; i < nc; ++i) {
+                const unsigned long long ki = ckey[i];
+                const uint32_t ci = ccnt[i];
+                below += ki < kj ? ci : 0u;
+                eq += ki == kj ? ci : 0u;
+            }
+            if (below < kk && kk <= below + eq) {  // every candidate with key T writes the same values
+                s_T = kj;
+                s_kk = kk - below;
+                s_eq = eq;
+            }
+        }
+        __syncthreads();
+        T = s_T;
+        kk = s_kk;
+        eq_total = s_eq;
+        __syncthreads();
+    } else {  // many candidates: 8-bit radix passes over the other 40 bits, from L2
+        unsigned long long prefix = bin;
+        for (int shift = 32; shift >= 0; shift -= 8) {
+            for (int j = threadIdx.x; j < 256; j += blockDim.x) h[j] = 0;
+            __syncthreads();
+            for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
+                const uint32_t i = __ldcg(cand + j);
+                const unsigned long long key = item_key(i);
+                if ((key >> (shift + 8)) == prefix) atomicAdd(&h[(key >> shift) & 0xFFu], counts[i]);
+            }
+            __syncthreads();
+            unsigned long long b2 = 0;
+            const int d = block_find_all(h, false, 256, kk, b2, &s_idx, &s_before, wsum);
+            prefix = (prefix << 8) | (unsigned long long)d;
+            kk -= b2;
+            eq_total = h[d];
+            __syncthreads();
+        }
+        T = prefix;
+    }
+    const bool all_ties = kk == eq_total;
+    TMARK();
+    // ---- F: bounds of this CTA's columns (lo = #|q| with score < T, hi = ... <= T)
+    {
+        const int64_t cper = (cols + gridDim.x - 1) / gridDim.x;
+        const int64_t c1 = min(cols, ((int64_t)blockIdx.x + 1) * cper);
+        for (int64_t c = (int64_t)blockIdx.x * cper + threadIdx.x; c < c1; c += blockDim.x) {
+            const double w = cm[c];
+            int a = 0, b = kBins;  // first a with key >= T
+            while (a < b) {
+                const int mid = (a + b) >> 1;
+                if (key_of(w, mid) < T) a = mid + 1; else b = mid;
+            }
+            const int l = a;
+            b = kBins;  // first a with key > T
+            while (a < b) {
+                const int mid = (a + b) >> 1;
+                if (key_of(w, mid) <= T) a = mid + 1; else b = mid;
+            }
+            lo[c] = (uint8_t)l;
+            hi[c] = (uint8_t)a;
+            bound[c] = (uint8_t)(all_ties ? a : l);
+            if (l < a) atomicOr(&eqmask[c >> 5], 1u << (c & 31));
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            so->T = T;
+            so->kk = kk;
+            so->eq_total = eq_total;
+            so->bin = bin;
+            so->cut = all_ties ? ~0ull : 0ull;
+        }
+    }
+    TMARK();
+#ifdef DC_PRUNE_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        printf("select4 nc=%u all_ties=%d:", nc, (int)all_ties);
+        for (int i = 1; i < ntm; ++i) printf(" %.2f", (tm[i] - tm[i - 1]) * 1e-3);
+        printf(" us\n");
+    }
+#endif
+    if (all_ties) return;  // grid-uniform; k_apply4 runs after this launch
+    grid.sync();
+    TMARK();
+    // ---- G: the tie columns in ascending order (shared list), ties per CTA
+    const int nw = (int)((cols + 31) >> 5);
+    uint32_t E;
+    {
+        const int per_w = (nw + blockDim.x - 1) / blockDim.x;
+        const int w0 = threadIdx.x * per_w, w1 = min(nw, w0 + per_w);
+        uint32_t c = 0;
+        for (int j = w0; j < w1; ++j) c += __popc(__ldcg(eqmask + j));
+        uint32_t inc = c;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, inc[r], d);
-            if (lane >= d) inc[r] += o;
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
         }
-        if (lane == 31) ws[r][w] = inc[r];
+        if (lane == 31) wcnt[threadIdx.x >> 5] = inc;
+        __syncthreads();
+        uint32_t before = 0, tot = 0;
+        for (int i = 0; i < kSelThreads / 32; ++i) {
+            before += i < (int)(threadIdx.x >> 5) ? wcnt[i] : 0u;
+            tot += wcnt[i];
+        }
+        E = tot;
+        if (E <= (uint32_t)kEqCap) {
+            uint32_t pos = before + inc - c;
+            for (int j = w0; j < w1; ++j)
+                for (uint32_t m = __ldcg(eqmask + j); m; m &= m - 1) elist[pos++] = (uint32_t)j * 32 + __ffs(m) - 1;
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    if (w == 0) {
-        uint32_t tot = 0;
+    const bool listed = E <= (uint32_t)kEqCap;
+    const uint32_t width = listed ? E : (uint32_t)cols;  // unlisted: whole rows (non-tie columns never match)
+    const int64_t rper = (rows + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = min(rows, (int64_t)blockIdx.x * rper), r1 = min(rows, r0 + rper);
+    const uint32_t np = (uint32_t)((r1 - r0) * (int64_t)width);
+    auto tie_at = [&](uint32_t p, int64_t& idx) -> bool {
+        const uint32_t rr = p / width, j = p - rr * width;
+        const uint32_t c = listed ? elist[j] : j;
+        idx = (r0 + rr) * cols + c;
+        const int a = absq(q[idx]);
+        return a >= __ldcg(lo + c) && a < __ldcg(hi + c);
+    };
+    {
+        uint32_t cnt = 0;
+        for (uint32_t pb = threadIdx.x; pb < np; pb += kUnr * blockDim.x) {
 #pragma unroll
-        for (int r = 0; r < kEqSub; ++r) tot += lane < kPrThreads / 32 ? ws[r][lane] : 0u;
-        tot = __reduce_add_sync(0xffffffffu, tot);
-        unsigned long long excl = 0;
-        if (tile == 0) {
-            if (lane == 0) atomicExch(&look[0], kLbP | tot);
-        } else {
-            if (lane == 0) atomicExch(&look[tile], kLbA | tot);
-            int64_t j = tile - 1;  // window [j - 31, j], lane l reads j - l
-            while (true) {
-                unsigned long long f = kLbP;  // before tile 0: an empty inclusive prefix
-                if (j - lane >= 0) {
-                    do f = *((volatile unsigned long long*)&look[j - lane]);
-                    while ((f & ~kLbMask) == 0);
-                }
-                const uint32_t pm = __ballot_sync(0xffffffffu, (f & ~kLbMask) == kLbP);
-                const int stop = pm ? __ffs(pm) - 1 : 32;  // nearest predecessor with a prefix
-                const unsigned long long add = lane <= stop ? (f & kLbMask) : 0ull;
-                unsigned long long sum = add;
-#pragma unroll
-                for (int d = 16; d; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
-                excl += sum;
-                if (pm) break;
-                j -= 32;
+            for (int u = 0; u < kUnr; ++u) {
+                const uint32_t p = pb + u * blockDim.x;
+                int64_t idx;
+                if (p < np) cnt += tie_at(p, idx);
             }
-            if (lane == 0) atomicExch(&look[tile], kLbP | (excl + tot));
         }
-        if (lane == 0) s_excl = excl;
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) wcnt[threadIdx.x >> 5] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int j = 0; j < kSelThreads / 32; ++j) t += wcnt[j];
+            psum[blockIdx.x] = t;
+        }
     }
-    __syncthreads();
-    unsigned long long base = s_excl;
+    TMARK();
+    grid.sync();
+    TMARK();
+    // ---- H: the CTA holding the kk-th tie finds its flat index
+    unsigned long long before = 0;
+    {
+        uint32_t v = 0;  // ties before this CTA's rows (parallel loads, block sum)
+        for (int j = threadIdx.x; j < (int)blockIdx.x; j += blockDim.x) v += __ldcg(psum + j);
+        v = __reduce_add_sync(0xffffffffu, v);
+        __syncthreads();
+        if (lane == 0) wcnt[threadIdx.x >> 5] = v;
+        __syncthreads();
+        for (int j = 0; j < kSelThreads / 32; ++j) before += wcnt[j];
+        __syncthreads();
+    }
+    const unsigned long long mine = __ldcg(psum + blockIdx.x);
+    if (!(before < kk && kk <= before + mine)) return;
+    for (uint32_t pb = 0; pb < np; pb += blockDim.x) {
+        const uint32_t p = pb + threadIdx.x;
+        int64_t idx = 0;
+        const bool t = p < np && tie_at(p, idx);
+        uint32_t tot;
+        const uint32_t r = block_excl(t, wcnt, tot);
+        if (t && before + r + 1 == kk) so->cut = (unsigned long long)idx;
+        before += tot;
+        if (before >= kk) break;  // block-uniform
+    }
+#ifdef DC_PRUNE_TIMING
+    TMARK();
+    if (threadIdx.x == 0) {
+        printf("select4 G/H (CTA %d holds the cut):", (int)blockIdx.x);
+        for (int i = 1; i < ntm; ++i) printf(" %.2f", (tm[i] - tm[i - 1]) * 1e-3);
+        printf(" us\n");
+    }
+#endif
+}
+
+// out = q with |q| < bound[c] zeroed, and the ties (bound <= |q| in [lo, hi))
+// at flat index <= cut: one streaming pass, 16 B per thread step, four in flight.
+constexpr int kApThreads = 256, kApVec = 4;
+
+__device__ __forceinline__ uint32_t zero_mask4(uint32_t qw, uint32_t bw, uint32_t lw, uint32_t hw, uint32_t cw) {
+    const uint32_t a = __vabs4(qw);
+    const uint32_t lt = __vcmpltu4(a, bw);
+    const uint32_t tie = __vcmpltu4(a, hw) & ~__vcmpltu4(a, lw) & cw;
+    return qw & ~(lt | tie);
+}
+
+__global__ void __launch_bounds__(kApThreads) k_apply4(const int8_t* __restrict__ q, const uint8_t* __restrict__ bound,
+                                                       const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi,
+                                                       int64_t n, int64_t cols, bool vec,
+                                                       const SelectOut* __restrict__ so, int8_t* __restrict__ out) {
+    const unsigned long long cut = so->cut;
+    const int64_t stride = (int64_t)gridDim.x * kApThreads * 16 * kApVec;
+    if (vec) {  // cols % 16 == 0, 16-B aligned: each vector lies in one row
+        for (int64_t base = ((int64_t)blockIdx.x * kApThreads * kApVec + threadIdx.x) * 16; base < n; base += stride) {
+            uint4 v[kApVec];
 #pragma unroll
-    for (int r = 0; r < kEqSub; ++r) {
-        uint32_t before = 0, total = 0;
-        for (int k = 0; k < kPrThreads / 32; ++k) {
-            const uint32_t x = ws[r][k];
-            before += k < w ? x : 0u;
-            total += x;
-        }
-        unsigned long long rank = base + before + inc[r] - __popc(eqm[r]);
-        base += total;
-        uint32_t zero = ltm[r];
-        for (uint32_t e = eqm[r]; e; e &= e - 1) {  // ties (few): the first r_keep in row-major order
-            if (rank < r_keep) zero |= e & (0u - e);
-            ++rank;
-        }
-        const int64_t i0 = tile * kEqBlock2 + r * kEqBlock + threadIdx.x * 16;
-        if (vec && i0 + 16 <= n) {
-            uint32_t o[4];
-            memcpy(o, v[r], 16);
+            for (int u = 0; u < kApVec; ++u) {
+                const int64_t i0 = base + (int64_t)u * kApThreads * 16;
+                v[u] = i0 < n ? __ldcs(reinterpret_cast<const uint4*>(q + i0)) : make_uint4(0, 0, 0, 0);
+            }
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                o[k] &= ~((((zero >> (4 * k)) & 15u) * 0x00204081u & 0x01010101u) * 0xFFu);
-            *reinterpret_cast<uint4*>(out + i0) = make_uint4(o[0], o[1], o[2], o[3]);
-        } else {
+            for (int u = 0; u < kApVec; ++u) {
+                const int64_t i0 = base + (int64_t)u * kApThreads * 16;
+                if (i0 >= n) break;
+                const uint32_t c0 = (uint32_t)((uint64_t)i0 % (uint64_t)cols);
+                const uint4 b = *reinterpret_cast<const uint4*>(bound + c0);
+                const uint4 l = *reinterpret_cast<const uint4*>(lo + c0);
+                const uint4 h = *reinterpret_cast<const uint4*>(hi + c0);
+                // ties at index <= cut: byte j of word w is element 4w + j
+                uint32_t cw[4];
+                const long long ck = (long long)cut - i0;  // cut = ~0: every tie (ck < 0 as signed, handled)
+                if (cut == ~0ull || ck >= 15) {
+                    cw[0] = cw[1] = cw[2] = cw[3] = 0xFFFFFFFFu;
+                } else if (ck < 0) {
+                    cw[0] = cw[1] = cw[2] = cw[3] = 0u;
+                } else {
 #pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if ((zero >> k) & 1) v[r][k] = 0;
-            for (int k = 0; k < 16; ++k)
-                if (i0 + k < n) out[i0 + k] = v[r][k];
+                    for (int w = 0; w < 4; ++w)
+                        cw[w] = __vcmpleu4(0x03020100u + 0x04040404u * w, 0x01010101u * (uint32_t)ck);
+                }
+                uint4 o;
+                o.x = zero_mask4(v[u].x, b.x, l.x, h.x, cw[0]);
+                o.y = zero_mask4(v[u].y, b.y, l.y, h.y, cw[1]);
+                o.z = zero_mask4(v[u].z, b.z, l.z, h.z, cw[2]);
+                o.w = zero_mask4(v[u].w, b.w, l.w, h.w, cw[3]);
+                __stcs(reinterpret_cast<uint4*>(out + i0), o);
+            }
         }
+        return;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * kApThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kApThreads) {
+        const int64_t c = i % cols;
+        const int8_t v = q[i];
+        const int a = absq(v);
+        const bool z = a < bound[c] || (a >= lo[c] && a < hi[c] && (cut == ~0ull || (unsigned long long)i <= cut));
+        out[i] = z ? (int8_t)0 : v;
     }
 }
 
@@ -658,24 +939,36 @@ extern "C" int dc_prune_scores(const int8_t* q, const double* cm, int64_t rows, 
     return DC_OK;
 }
 
-static int64_t colhist3_rb(int64_t rows, int64_t cols) {
-    const int64_t n_cb = (cols + kH3Cols - 1) / kH3Cols;
-    int64_t n_rb = (2 * (int64_t)sm_count_pr() + n_cb - 1) / n_cb;
+static int64_t colhist4_rb(int64_t rows, int64_t cols) {
+    const int64_t n_cb = (cols + kH4Cols - 1) / kH4Cols;
+    int64_t n_rb = 3 * (int64_t)sm_count_pr() / n_cb;  // 3 CTAs per SM, one wave
     n_rb = n_rb < 1 ? 1 : (n_rb > 64 ? 64 : n_rb);
-    return n_rb > rows ? (rows > 0 ? rows : 1) : n_rb;
+    if (n_rb > rows) n_rb = rows > 0 ? rows : 1;
+    const int64_t need = (rows + 65534) / 65535;  // u16 partial counts
+    return n_rb < need ? need : n_rb;
+}
+
+static int64_t colhist5_rb(int64_t rows, int64_t cols) {
+    const int64_t n_cb = (cols + kH5Cols - 1) / kH5Cols;
+    int64_t n_rb = (int64_t)sm_count_pr() / n_cb;  // one CTA per SM, one wave
+    n_rb = n_rb < 1 ? 1 : (n_rb > 64 ? 64 : n_rb);
+    if (n_rb > rows) n_rb = rows > 0 ? rows : 1;
+    const int64_t need = (rows + 65534) / 65535;  // u16 partial counts
+    return n_rb < need ? need : n_rb;
 }
 
 extern "C" int dc_prune_scratch_bytes(int64_t rows, int64_t cols, uint64_t* out) {
-    const int64_t n = rows * cols;
-    const uint64_t n_cb = (uint64_t)((cols + kH3Cols - 1) / kH3Cols);
-    const uint64_t tiles = (uint64_t)((n + kEqBlock2 - 1) / kEqBlock2);
-    *out = 4ull * 2 * 65536 + 4ull * 2 * 4096 + 64 + 256 + 8ull * tiles + 256 + 4ull * (uint64_t)cols * kBins + 256 +
-           2ull * (uint64_t)cols + 256 + 4ull * kH3Cols * kBins * n_cb * (uint64_t)colhist3_rb(rows, cols) + 256;
+    const uint64_t n_cb = (uint64_t)((cols + kH4Cols - 1) / kH4Cols);
+    const uint64_t items = (uint64_t)cols * kBins;
+    *out = 8ull * kSelHBins + 256 + 4ull * 4096 + 256 + sizeof(SelectOut) + 256 + 4ull * items + 256 + 4ull * cols +
+           256 + 4ull * items + 256 + 3ull * (uint64_t)cols + 256 +
+           2ull * kH4Words * n_cb * (uint64_t)colhist4_rb(rows, cols) +
+           4ull * kH5Words * (uint64_t)((cols + kH5Cols - 1) / kH5Cols) * (uint64_t)colhist5_rb(rows, cols) + 256;
     return DC_OK;
 }
 
-// Per tensor: (column, |q|) histogram -> one cooperative selection launch ->
-// one look-back apply pass (5 launches + 2 memsets, was 20).
+// Per tensor: (column, |q|) histogram (+ sum) -> one cooperative selection
+// launch -> one streaming apply pass (4 launches, was 20 in round 1).
 extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, int64_t cols, int64_t k,
                                int8_t* out, uint8_t* scratch, void* stream) {
     if (rows < 0 || cols < 0 || k < 0 || k > rows * cols) return DC_ERR_ARG;
@@ -697,75 +990,86 @@ extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, 
     auto align = [](uint8_t* p) {
         return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255);
     };
-    uint8_t* p = scratch;
-    auto* hist2 = reinterpret_cast<uint32_t*>(p);
-    p += 4ull * 2 * 65536;
+    const int64_t items = cols * kBins;
+    uint8_t* p = align(scratch);
+    auto* hist = reinterpret_cast<uint32_t*>(p);
+    p = align(p + 8ull * kSelHBins);
     auto* psum = reinterpret_cast<uint32_t*>(p);
-    p += 4ull * 2 * 4096;
-    auto* sel = reinterpret_cast<SelectState*>(p);
-    p += 64;
-    auto* tile_ctr = reinterpret_cast<uint32_t*>(p);
-    p = align(p + 4);
-    const int64_t tiles = (n + kEqBlock2 - 1) / kEqBlock2;
-    auto* look = reinterpret_cast<unsigned long long*>(p);
-    p = align(p + 8ull * tiles);
+    p = align(p + 4ull * 4096);
+    auto* so = reinterpret_cast<SelectOut*>(p);
+    p = align(p + sizeof(SelectOut));
+    auto* cand = reinterpret_cast<uint32_t*>(p);
+    p = align(p + 4ull * items);
+    auto* eqmask = reinterpret_cast<uint32_t*>(p);
+    p = align(p + 4ull * ((cols + 31) / 32));
     auto* counts = reinterpret_cast<uint32_t*>(p);
-    p = align(p + 4ull * cols * kBins);
-    uint8_t* lo = p;
-    uint8_t* hi = p + cols;
-    p = align(p + 2ull * cols);
-    auto* partial = reinterpret_cast<uint32_t*>(p);
+    p = align(p + 4ull * items);
+    uint8_t* bound = p;
+    uint8_t* lo = p + cols;
+    uint8_t* hi = p + 2 * cols;
+    p = align(p + 3ull * cols);
+    auto* partial = reinterpret_cast<uint16_t*>(p);
     const bool vec = cols % 16 == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
                      (reinterpret_cast<uintptr_t>(out) & 15) == 0;
 
-    k_sel_init<<<1, 1, 0, st>>>(sel, (unsigned long long)k);  // (a pageable H2D copy would synchronize)
-    DC_CHECK_LAUNCH("k_sel_init");
-    const int64_t n_cb = (cols + kH3Cols - 1) / kH3Cols;
-    int64_t n_rb = colhist3_rb(rows, cols);
-    const int64_t rows_per = (rows + n_rb - 1) / n_rb;
-    n_rb = (rows + rows_per - 1) / rows_per;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_colhist3, cudaFuncAttributeMaxDynamicSharedMemorySize, kH3Cols * kBins * 4);
-        attr = true;
-    }
-    k_colhist3<<<dim3((unsigned)n_rb, (unsigned)n_cb), kH3Threads, kH3Cols * kBins * 4, st>>>(q, rows, cols, rows_per,
-                                                                                           vec, partial);
-    DC_CHECK_LAUNCH("k_colhist3");
-    const int64_t sb = (cols * kBins + 255) / 256;
-    k_colhist3_sum<<<(unsigned)(sb < 1184 ? sb : 1184), 256, 0, st>>>(partial, n_rb, n_cb, cols, counts);
-    DC_CHECK_LAUNCH("k_colhist3_sum");
-    {  // the k-th score and the per-column bounds: one cooperative launch
-        cudaError_t ez = cudaMemsetAsync(hist2, 0, 4ull * 2 * 65536 + 4ull * 2 * 4096, st);  // hist2 + psum2
-        if (ez != cudaSuccess) {
-            set_error("prune memset", ez);
-            return DC_ERR_CUDA;
+    if (vec) {  // 16-B path
+        const int64_t n_cb = (cols + kH5Cols - 1) / kH5Cols;
+        int64_t n_rb = colhist5_rb(rows, cols);
+        const int64_t rows_per = (rows + n_rb - 1) / n_rb;
+        n_rb = (rows + rows_per - 1) / rows_per;
+        static bool attr5 = false;
+        if (!attr5) {
+            cudaFuncSetAttribute(k_colhist5, cudaFuncAttributeMaxDynamicSharedMemorySize, kH5Smem);
+            attr5 = true;
         }
+        auto* part = reinterpret_cast<uint32_t*>(partial);
+        k_colhist5<<<dim3((unsigned)n_rb, (unsigned)n_cb), kH5Threads, kH5Smem, st>>>(q, rows, cols, rows_per, part);
+        DC_CHECK_LAUNCH("k_colhist5");
+        k_colhist5_sum<<<(unsigned)(sm_count_pr() * 8), 256, 0, st>>>(part, n_rb, n_cb, cols, counts, hist, eqmask,
+                                                                       so);
+        DC_CHECK_LAUNCH("k_colhist5_sum");
+    } else {
+        const int64_t n_cb = (cols + kH4Cols - 1) / kH4Cols;
+        int64_t n_rb = colhist4_rb(rows, cols);
+        const int64_t rows_per = (rows + n_rb - 1) / n_rb;
+        n_rb = (rows + rows_per - 1) / rows_per;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_colhist4, cudaFuncAttributeMaxDynamicSharedMemorySize, kH4Smem);
+            attr = true;
+        }
+        const bool vec4 = cols % 4 == 0 && (reinterpret_cast<uintptr_t>(q) & 3) == 0;
+        k_colhist4<<<dim3((unsigned)n_rb, (unsigned)n_cb), kH4Threads, kH4Smem, st>>>(q, rows, cols, rows_per, vec4,
+                                                                                      partial);
+        DC_CHECK_LAUNCH("k_colhist4");
+        k_colhist4_sum<<<(unsigned)(sm_count_pr() * 8), 256, 0, st>>>(partial, n_rb, n_cb, cols, counts, hist, eqmask,
+                                                                       so);
+        DC_CHECK_LAUNCH("k_colhist4_sum");
+    }
+    {  // the k-th score, the per-column bounds and the tie cut: one cooperative launch
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_coop, kSelThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select4, kSelThreads, 0);
         if (per_sm < 1) {
-            set_error_msg("k_select_coop: not resident");
+            set_error_msg("k_select4: not resident");
             return DC_ERR_CUDA;
         }
         int grid = sm_count_pr();
-        if (grid > 4096) grid = 4096;
-        void* args[] = {(void*)&counts, (void*)&cm, (void*)&cols, (void*)&sel, (void*)&hist2, (void*)&psum,
-                        (void*)&lo, (void*)&hi};
-        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_select_coop, dim3((unsigned)grid), dim3(kSelThreads),
+        if (grid > 4096) grid = 4096;  // psum slots
+        unsigned long long kk = (unsigned long long)k;
+        void* args[] = {(void*)&counts, (void*)&cm, (void*)&q, (void*)&rows, (void*)&cols, (void*)&kk, (void*)&so,
+                        (void*)&hist, (void*)&psum, (void*)&cand, (void*)&eqmask, (void*)&bound, (void*)&lo, (void*)&hi};
+        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_select4, dim3((unsigned)grid), dim3(kSelThreads),
                                                     args, 0, st);
         if (e != cudaSuccess) {
-            set_error("k_select_coop", e);
+            set_error("k_select4", e);
             return DC_ERR_CUDA;
         }
     }
-    cudaError_t e = cudaMemsetAsync(tile_ctr, 0, 4, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(look, 0, 8ull * tiles, st);
-    if (e != cudaSuccess) {
-        set_error("prune memset", e);
-        return DC_ERR_CUDA;
-    }
-    k_apply3<<<(unsigned)tiles, kPrThreads, 0, st>>>(q, lo, hi, n, cols, vec, sel, look, tile_ctr, out);
-    DC_CHECK_LAUNCH("k_apply3");
+    const int64_t want = (n + (int64_t)kApThreads * 16 * kApVec - 1) / ((int64_t)kApThreads * 16 * kApVec);
+    const int64_t cap = (int64_t)sm_count_pr() * 8;
+    const int64_t g = vec ? (want < cap ? want : cap) : cap;
+    k_apply4<<<(unsigned)g, kApThreads, 0, st>>>(q, bound, lo, hi, n, cols, vec, so, out);
+    DC_CHECK_LAUNCH("k_apply4");
     return DC_OK;
 }
 

@@ -115,6 +115,22 @@ def test_prune_per_row_wide_rows_match_oracle(cuda, oracle):
             assert np.array_equal(got, oracle.prune(q, c_vec, sp, True)), (cols, sp)
 
 
+def test_prune_per_tensor_ties_match_oracle(cuda, oracle):
+    """Per-tensor selection where the k-th score is shared by many entries:
+    constant cm (every column holds ties: the tie cut scans whole rows), a
+    few cm levels, zero channel maxima (score-0 keys), 16-aligned and ragged
+    widths (vector and scalar apply) -- zero sets equal the reference's."""
+    rng = np.random.default_rng(66)
+    for rows, cols in ((300, 1024), (257, 777), (64, 4096)):
+        q = np.clip(np.round(rng.normal(0, 9, (rows, cols))), -127, 127).astype(np.int8)
+        for cm in (np.full(cols, 0.75), rng.choice([0.0, 0.5, 1.0, 2.0], cols), rng.lognormal(-1, 1, cols)):
+            for sp in (0.013, 0.2, 0.5, 0.93):
+                qt = cuda.QuantizedTensor("t", q, 0.1, cuda.ScaleVector.identity(cols))
+                st = cuda.ActivationStats("t", cm)
+                got = cuda.prune(qt, st, cuda.PruneConfig(sp)).qvalues
+                assert np.array_equal(got, oracle.prune(q, cm, sp, False)), (rows, cols, sp, cm[:3])
+
+
 def test_prune_properties(cuda):
     rng = np.random.default_rng(44)
     q = np.clip(np.round(rng.normal(0, 20, (256, 512))), -127, 127).astype(np.int8)
