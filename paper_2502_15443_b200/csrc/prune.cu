@@ -25,13 +25,15 @@ constexpr int kPrThreads = 256;
 constexpr int kBins = 129;  // |q| in 0..128
 
 constexpr int kSelThreads = 512;
-constexpr int kSelHBins = 4096;  // 12-bit digit passes (two), in shared memory
+constexpr int kSelHBins = 4096;  // selection histogram bins (shared memory)
 
 struct SelectOut {
     unsigned long long T;         // the k-th smallest score's bits
     unsigned long long kk;        // ties (score == T) to zero, the first kk in row-major order
     unsigned long long eq_total;  // elements with score == T
     unsigned long long cut;       // flat index of the last tie to zero (~0: every tie goes)
+    unsigned long long kmin;      // key of the smallest positive score (min cm > 0, |q| = 1); ~0 if none
+    unsigned long long kmax;      // key bound of the largest score (max cm, |q| = 128)
     uint32_t n_cand, n_eqc, bin, pad;
 };
 
@@ -42,84 +44,59 @@ __device__ __forceinline__ unsigned long long key_of(double cm, int a) {
 __device__ __forceinline__ int absq(int8_t v) { return v < 0 ? -(int)v : (int)v; }
 
 // ------------------------------------------------------------ per tensor
-// (column, |q|) histogram, conflict-free: a CTA covers 128 columns, each warp
-// one row per step with lane L loading the 4 bytes of columns 4L..4L+3; the
-// shared bins are laid out [|q|][e][lane] so the atomic for byte e of every
-// lane lands in bank L whatever the |q| values (the round-1 column-major bins
-// took random-bank conflicts and same-address collisions: ~2.5x slower).
-// Row blocks (<= 65535 rows, so u16 counts) write partial histograms in the
-// same layout; k_colhist4_sum adds them up.
-constexpr int kH4Cols = 128;
-constexpr int kH4Threads = 512;
-constexpr int kH4Unr = 8;
-constexpr int kH4Words = kBins * kH4Cols;  // [a][e][lane]
-constexpr int kH4Smem = kH4Words * 4;
-
-__global__ void __launch_bounds__(kH4Threads, 3) k_colhist4(const int8_t* __restrict__ q, int64_t rows, int64_t cols,
-                                                             int64_t rows_per, bool vec4,
-                                                             uint16_t* __restrict__ partial) {
-    extern __shared__ __align__(16) uint32_t hb[];
-    for (int i = threadIdx.x; i < kH4Words / 4; i += blockDim.x) reinterpret_cast<uint4*>(hb)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = kH4Threads / 32;
-    const int64_t c0 = (int64_t)blockIdx.y * kH4Cols + lane * 4;
-    const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(rows, r0 + rows_per);
-    uint32_t* hl = hb + lane;
-#ifdef DC_PRUNE_NOATOMS
-    uint32_t sink = 0;
-#endif
-    if (vec4) {  // cols % 4 == 0, q 4-byte aligned
-        if (c0 < cols) {
-            const int8_t* p = q + c0;
-            for (int64_t r = r0 + warp; r < r1; r += nwarp * kH4Unr) {
-                uint32_t w[kH4Unr];
-#pragma unroll
-                for (int u = 0; u < kH4Unr; ++u) {
-                    const int64_t rr = r + u * nwarp;
-                    w[u] = rr < r1 ? __ldg(reinterpret_cast<const uint32_t*>(p + rr * cols)) : 0u;
-                }
-#pragma unroll
-                for (int u = 0; u < kH4Unr; ++u) {
-                    if (r + u * nwarp >= r1) break;
-                    const uint32_t a4 = __vabs4(w[u]);  // 0x80 -> 128 (unsigned)
-#ifdef DC_PRUNE_NOATOMS
-                    sink += a4;
-#else
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) atomicAdd(hl + ((a4 >> (8 * e)) & 0xFFu) * kH4Cols + e * 32, 1u);
-#endif
-                }
-            }
-        }
-    } else {
-        for (int64_t r = r0 + warp; r < r1; r += nwarp)
-            for (int e = 0; e < 4; ++e)
-                if (c0 + e < cols) atomicAdd(hl + absq(q[r * cols + c0 + e]) * kH4Cols + e * 32, 1u);
-    }
-#ifdef DC_PRUNE_NOATOMS
-    hl[0] += sink;
-#endif
-    __syncthreads();
-    uint32_t* out = reinterpret_cast<uint32_t*>(partial + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * kH4Words);
-    for (int i = threadIdx.x; i < kH4Words / 2; i += blockDim.x) {
-        const uint2 v = reinterpret_cast<const uint2*>(hb)[i];
-        out[i] = v.x | (v.y << 16);
-    }
-}
-
-// Same with 16-byte loads: lane L holds columns 16L..16L+15 of a row (a warp
-// reads 512 contiguous bytes), counters are u16 pairs (even / odd column of
-// the lane's 16) in words laid out [|q|][e / 2][lane]: still bank L for every
-// lane, 132 KB of shared bins for 512 columns, one CTA of 32 warps per SM.
+// (column, |q|) histogram, conflict-free: a CTA covers 512 columns, each warp
+// one row per step with lane L loading the 16 bytes of columns 16L..16L+15
+// (a warp reads 512 contiguous bytes); counters are u16 pairs (even / odd
+// column of the lane's 16) in words laid out [|q|][e / 2][lane], so the
+// atomic for byte e of every lane lands in bank L whatever the |q| values
+// (column-major bins took random-bank conflicts and same-address collisions:
+// 2.3x slower).  132 KB of shared bins, one CTA of 32 warps per SM, one wave;
+// row blocks of <= 65535 rows (u16) write partial histograms in the same
+// layout, summed by k_select4's first phase.  CTA (0, 0) also zeroes the
+// selection's histograms, tie-column bits and candidate counter.
 constexpr int kH5Cols = 512;
 constexpr int kH5Threads = 1024;
 constexpr int kH5Unr = 4;
 constexpr int kH5Words = kBins * kH5Cols / 2;  // [a][e/2 (8)][lane (32)], u16 pairs
 constexpr int kH5Smem = kH5Words * 4;
 
-__global__ void __launch_bounds__(kH5Threads, 1) k_colhist5(const int8_t* __restrict__ q, int64_t rows, int64_t cols,
-                                                             int64_t rows_per, uint32_t* __restrict__ partial) {
+__global__ void __launch_bounds__(kH5Threads, 1) k_colhist5(const int8_t* __restrict__ q, const double* __restrict__ cm,
+                                                             int64_t rows, int64_t cols, int64_t rows_per, bool vec,
+                                                             uint32_t* __restrict__ partial,
+                                                             uint32_t* __restrict__ hist, uint32_t* __restrict__ eqmask,
+                                                             SelectOut* __restrict__ so) {
     extern __shared__ __align__(16) uint32_t hb[];
+    if (blockIdx.x == 0 && blockIdx.y == 0) {
+        for (int i = threadIdx.x; i < 2 * kSelHBins; i += blockDim.x) hist[i] = 0;
+        for (int64_t i = threadIdx.x; i < (cols + 31) / 32; i += blockDim.x) eqmask[i] = 0;
+        // the key range of the selection's bins: smallest positive cm, largest cm
+        __shared__ double rmin[kH5Threads / 32], rmax[kH5Threads / 32];
+        double mn = INFINITY, mx = 0.0;
+        for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+            const double v = cm[c];
+            if (v > 0.0) mn = fmin(mn, v);
+            mx = fmax(mx, v);
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            rmin[threadIdx.x >> 5] = mn;
+            rmax[threadIdx.x >> 5] = mx;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int i = 1; i < kH5Threads / 32; ++i) {
+                mn = fmin(mn, rmin[i]);
+                mx = fmax(mx, rmax[i]);
+            }
+            so->n_cand = 0;
+            so->kmin = mn == INFINITY ? ~0ull : (unsigned long long)__double_as_longlong(mn);
+            so->kmax = key_of(mx, 128);
+        }
+    }
     for (int i = threadIdx.x; i < kH5Words / 4; i += blockDim.x) reinterpret_cast<uint4*>(hb)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = kH5Threads / 32;
@@ -129,7 +106,7 @@ __global__ void __launch_bounds__(kH5Threads, 1) k_colhist5(const int8_t* __rest
 #ifdef DC_PRUNE_NOATOMS
     uint32_t sink = 0;
 #endif
-    if (c0 < cols) {  // cols % 16 == 0, q 16-byte aligned (caller)
+    if (vec && c0 < cols) {  // cols % 16 == 0, q 16-byte aligned
         const int8_t* p = q + c0;
         for (int64_t r = r0 + warp; r < r1; r += nwarp * kH5Unr) {
             uint4 v[kH5Unr];
@@ -153,6 +130,12 @@ __global__ void __launch_bounds__(kH5Threads, 1) k_colhist5(const int8_t* __rest
             }
         }
     }
+    if (!vec) {  // ragged widths / unaligned: byte loads
+        for (int64_t r = r0 + warp; r < r1; r += nwarp)
+            for (int e = 0; e < 16; ++e)
+                if (c0 + e < cols)
+                    atomicAdd(hl + absq(q[r * cols + c0 + e]) * (kH5Cols / 2) + (e >> 1) * 32, (e & 1) ? 0x10000u : 1u);
+    }
 #ifdef DC_PRUNE_NOATOMS
     hl[0] += sink & 1;
 #endif
@@ -161,71 +144,13 @@ __global__ void __launch_bounds__(kH5Threads, 1) k_colhist5(const int8_t* __rest
     for (int i = threadIdx.x; i < kH5Words / 4; i += blockDim.x) out[i] = reinterpret_cast<const uint4*>(hb)[i];
 }
 
-// counts[c * 129 + a] from the k_colhist5 partials (u16 pairs)
-__global__ void k_colhist5_sum(const uint32_t* __restrict__ partial, int64_t n_rb, int64_t n_cb, int64_t cols,
-                               uint32_t* __restrict__ counts, uint32_t* __restrict__ hist,
-                               uint32_t* __restrict__ eqmask, SelectOut* __restrict__ so) {
-    const int64_t per_rb = n_cb * kH5Words;
-    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = gt; i < per_rb; i += gs) {
-        const uint32_t cb = (uint32_t)(i / kH5Words), rem = (uint32_t)(i - (int64_t)cb * kH5Words);
-        const uint32_t a = rem / (kH5Cols / 2), slot = rem % (kH5Cols / 2);  // slot = (e/2) * 32 + lane
-        const int64_t c = (int64_t)cb * kH5Cols + (slot & 31) * 16 + (slot >> 5) * 2;
-        uint32_t s0 = 0, s1 = 0;
-        for (int64_t rb = 0; rb < n_rb; rb += 8) {
-            uint32_t v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = rb + u < n_rb ? partial[(rb + u) * per_rb + i] : 0u;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                s0 += v[u] & 0xFFFFu;
-                s1 += v[u] >> 16;
-            }
-        }
-        if (c < cols) counts[c * kBins + a] = s0;
-        if (c + 1 < cols) counts[(c + 1) * kBins + a] = s1;
-    }
-    for (int64_t i = gt; i < 2 * kSelHBins / 4; i += gs) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0, 0, 0, 0);
-    for (int64_t i = gt; i < (cols + 31) / 32; i += gs) eqmask[i] = 0;
-    if (gt == 0) so->n_cand = 0;
-}
-
-// counts[c * 129 + a] = sum over row blocks of the k_colhist4 partials (read
-// in their layout, coalesced; n_rb loads in flight); also zeroes k_select4's
-// histograms, tie-column bits and candidate counter.
-__global__ void k_colhist4_sum(const uint16_t* __restrict__ partial, int64_t n_rb, int64_t n_cb, int64_t cols,
-                               uint32_t* __restrict__ counts, uint32_t* __restrict__ hist,
-                               uint32_t* __restrict__ eqmask, SelectOut* __restrict__ so) {
-    const int64_t per_rb = n_cb * kH4Words;
-    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = gt; i < per_rb; i += gs) {
-        const uint32_t cb = (uint32_t)(i / kH4Words), rem = (uint32_t)(i - (int64_t)cb * kH4Words);
-        const uint32_t a = rem / kH4Cols, slot = rem % kH4Cols;
-        const int64_t c = (int64_t)cb * kH4Cols + (slot & 31) * 4 + (slot >> 5);
-        uint32_t s = 0;
-        for (int64_t rb = 0; rb < n_rb; rb += 8) {
-            uint32_t v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = rb + u < n_rb ? partial[(rb + u) * per_rb + i] : 0u;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) s += v[u];
-        }
-        if (c < cols) counts[c * kBins + a] = s;
-    }
-    for (int64_t i = gt; i < 2 * kSelHBins / 4; i += gs) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0, 0, 0, 0);
-    for (int64_t i = gt; i < (cols + 31) / 32; i += gs) eqmask[i] = 0;
-    if (gt == 0) so->n_cand = 0;
-}
-
 // The whole k-th-score selection and the tie cut in ONE cooperative launch
-// (grid = SMs, 4 grid barriers, 6 when only some ties stay):
-//   A  every CTA: histogram of the top 12 key bits (sign + exponent) of its
-//      (column, |q|) items in shared memory, flushed with one global atomic
-//      per non-empty bin; every CTA then picks the bin holding rank k;
-//   A2 the same for the next 12 bits, over the items inside that exponent
-//      (global atomics on a few thousand hot bins of a flat 2^20-bin table
-//      were 20 us of L2 atomic serialization);
-//   D  every CTA appends the items whose top 24 key bits match to a list;
+// (grid = SMs, 3 grid barriers, 5 when only some ties stay):
+//   A  every CTA sums the row-block partials of its item slice (the counts
+//      are kept for D) into a 4096-bin shared histogram over the keys' actual
+//      range (bin_of below), flushed with one global atomic per non-empty
+//      bin; every CTA then picks the bin holding rank k;
+//   D  every CTA appends the (key, count) of that bin's items to a list;
 //   E  every CTA redundantly: the k-th key among those (few) candidates by
 //      direct rank comparison in shared memory (8-bit radix passes from L2
 //      when there are many) -> T, the ties to zero (kk), the entries == T;
@@ -237,7 +162,9 @@ __global__ void k_colhist4_sum(const uint16_t* __restrict__ partial, int64_t n_r
 //      records its flat index as the cut.
 // Loops over global data batch their loads (the serial L2 round trips of a
 // plain loop dominated).  Replaces a 4 x 16-bit grid-wide radix select (12
-// grid barriers) and the look-back tie scan of the round-1 apply pass.
+// grid barriers, hot-bin global atomics) and the look-back tie scan of the
+// round-1 apply pass.  (One cluster of 16 CTAs with DSMEM reductions instead
+// of grid barriers was tried: 98 us -- the item passes need all SMs.)
 // rank-k entry of v[0..m) for any m: thread t sums a contiguous run of
 // ceil(m / blockDim) entries (independent loads), one block scan picks the run,
 // its owner walks it.  Returns the index; `base` becomes the count before it.
@@ -246,8 +173,13 @@ __device__ int block_find_all(const uint32_t* v, bool gmem, int m, unsigned long
     const int per = (m + blockDim.x - 1) / blockDim.x;
     const int j0 = threadIdx.x * per, j1 = min(m, j0 + per);
     auto ld = [&](int j) -> uint32_t { return j < j1 ? (gmem ? __ldcg(v + j) : v[j]) : 0u; };
+    uint32_t e0[8];  // the first 8 entries of the run stay in registers for the walk
+#pragma unroll
+    for (int u = 0; u < 8; ++u) e0[u] = ld(j0 + u);
     unsigned long long x = 0;
-    for (int j = j0; j < j1; j += 8) {  // 8 independent loads in flight
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x += e0[u];
+    for (int j = j0 + 8; j < j1; j += 8) {  // 8 independent loads in flight
         uint32_t e[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) e[u] = ld(j + u);
@@ -273,7 +205,7 @@ __device__ int block_find_all(const uint32_t* v, bool gmem, int m, unsigned long
         for (int j = j0; j < j1 && !found; j += 8) {
             uint32_t e[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) e[u] = ld(j + u);
+            for (int u = 0; u < 8; ++u) e[u] = j == j0 ? e0[u] : ld(j + u);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 if (!found && j + u < j1 && k <= c + e[u]) {
@@ -312,16 +244,17 @@ constexpr int kCandCap = 1024;  // candidates cached in shared memory (else re-r
 constexpr int kEqCap = 4096;    // tie columns listed in shared memory (else whole rows are scanned)
 constexpr int kUnr = 8;
 
-__global__ void __launch_bounds__(kSelThreads) k_select4(const uint32_t* __restrict__ counts,
+__global__ void __launch_bounds__(kSelThreads) k_select4(const uint32_t* __restrict__ partial, int64_t n_rb,
+                                                         int64_t n_cb, uint32_t* __restrict__ counts,
                                                          const double* __restrict__ cm, const int8_t* __restrict__ q,
                                                          int64_t rows, int64_t cols, unsigned long long k,
                                                          SelectOut* __restrict__ so, uint32_t* __restrict__ hist,
                                                          uint32_t* __restrict__ psum, uint32_t* __restrict__ cand,
                                                          uint32_t* __restrict__ eqmask, uint8_t* __restrict__ bound,
                                                          uint8_t* __restrict__ lo, uint8_t* __restrict__ hi) {
-    // hist (2 x 4096 u32), eqmask and so->n_cand are zeroed by k_colhist4_sum
+    // hist (2 x 4096 u32), eqmask and so->n_cand are zeroed by k_colhist5
     cg::grid_group grid = cg::this_grid();
-    const int64_t n = cols * kBins;
+    const int64_t nw = n_cb * kH5Words;  // partial words = item pairs
     const int lane = threadIdx.x & 31;
     __shared__ unsigned long long wsum[kSelThreads / 32], s_before;
     __shared__ uint32_t wcnt[kSelThreads / 32], h[256], hs[kSelHBins];
@@ -338,71 +271,94 @@ __global__ void __launch_bounds__(kSelThreads) k_select4(const uint32_t* __restr
 #define TMARK() do {} while (0)
 #endif
     TMARK();
-    const int64_t per = (n + gridDim.x - 1) / gridDim.x;  // contiguous items per CTA (A and D)
-    const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n, i0 + per);
-    auto item_key = [&](uint32_t i) {
-        const uint32_t col = i / (uint32_t)kBins;
-        return key_of(cm[col], (int)(i - col * (uint32_t)kBins));
+    // items follow the k_colhist5 layout: item j = 2 * word + half, word =
+    // (cb * 129 + a) * 256 + (e / 2) * 32 + lane, column cb * 512 + 16 lane +
+    // e (e = 2 (e / 2) + half); counts[j] is written by phase A
+    const int64_t per = ((nw + gridDim.x - 1) / gridDim.x + 3) & ~3ll;  // contiguous words per CTA (A, A2, D)
+    const int64_t w0 = min(nw, (int64_t)blockIdx.x * per), w1 = min(nw, w0 + per);  // nw % 4 == 0
+    auto item_col_a = [&](uint32_t j, uint32_t& col) -> uint32_t {
+        const uint32_t w = j >> 1, cb = w / (uint32_t)kH5Words, rem = w - cb * (uint32_t)kH5Words;
+        const uint32_t a = rem / (kH5Cols / 2), slot = rem % (kH5Cols / 2);
+        col = cb * kH5Cols + (slot & 31) * 16 + (slot >> 5) * 2 + (j & 1);
+        return a;
     };
-    // ---- A: (sign, exponent) histogram in shared memory, flushed to hist[0..4096)
+    auto item_key = [&](uint32_t j) {
+        uint32_t col;
+        const uint32_t a = item_col_a(j, col);
+        return key_of(cm[col], (int)a);
+    };
+    // ---- A: one histogram of 4096 bins over the keys' actual range: bin 0
+    // holds score 0, bins 1.. the positive keys >> sh, offset so that the
+    // smallest positive key (min cm > 0 at |q| = 1) is bin 1 and sh is the
+    // least shift that fits the largest (max cm at |q| = 128) -- for cm
+    // spanning <= 2^8 that is 2^-8-octave resolution, so few items share the
+    // chosen bin.  Keys are monotone in the bin, so the rank-k bin is exact.
+    const unsigned long long kmin = __ldcg(&so->kmin), kmax = __ldcg(&so->kmax);
+    int sh = 0;
+    while (sh < 63 && kmin != ~0ull && (kmax >> sh) - (kmin >> sh) > (unsigned long long)(kSelHBins - 2)) ++sh;
+    auto bin_of = [&](unsigned long long key) -> uint32_t {
+        return key == 0 ? 0u : 1u + (uint32_t)((key >> sh) - (kmin >> sh));
+    };
     for (int j = threadIdx.x; j < kSelHBins; j += blockDim.x) hs[j] = 0;
     __syncthreads();
-    auto hist_pass = [&](int pass, uint32_t want) {
-        for (int64_t ib = i0 + threadIdx.x; ib < i1; ib += kUnr * blockDim.x) {
-            uint32_t c[kUnr];
+    for (int64_t w = w0 + 4 * threadIdx.x; w < w1; w += 4 * blockDim.x) {
+        // sum the row-block partials, 4 words per thread (16-B loads, 6 in flight)
+        uint32_t s0[4] = {0, 0, 0, 0}, s1[4] = {0, 0, 0, 0};
+        for (int64_t rb = 0; rb < n_rb; rb += 6) {
+            uint4 v[6];
 #pragma unroll
-            for (int u = 0; u < kUnr; ++u) {
-                const int64_t i = ib + (int64_t)u * blockDim.x;
-                c[u] = i < i1 ? counts[i] : 0u;
-            }
+            for (int u = 0; u < 6; ++u)
+                v[u] = rb + u < n_rb ? *reinterpret_cast<const uint4*>(partial + (rb + u) * nw + w) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int u = 0; u < kUnr; ++u) {
-                if (!c[u]) continue;
-                const unsigned long long key = item_key((uint32_t)(ib + (int64_t)u * blockDim.x));
-                if (pass == 0)
-                    atomicAdd(&hs[key >> 52], c[u]);
-                else if ((uint32_t)(key >> 52) == want)
-                    atomicAdd(&hs[(key >> 40) & 0xFFF], c[u]);
+            for (int u = 0; u < 6; ++u) {
+                const uint32_t x[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    s0[t] += x[t] & 0xFFFFu;
+                    s1[t] += x[t] >> 16;
+                }
             }
         }
-        __syncthreads();
-        uint32_t* g = hist + pass * kSelHBins;
-        for (int j = threadIdx.x; j < kSelHBins; j += blockDim.x) {
-            const uint32_t v = hs[j];
-            if (v) atomicAdd(g + j, v);
-            hs[j] = 0;
+        reinterpret_cast<uint4*>(counts)[w >> 1] = make_uint4(s0[0], s1[0], s0[1], s1[1]);
+        reinterpret_cast<uint4*>(counts)[(w >> 1) + 1] = make_uint4(s0[2], s1[2], s0[3], s1[3]);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const uint32_t c = (t & 1) ? s1[t >> 1] : s0[t >> 1];
+            if (c) atomicAdd(&hs[bin_of(item_key((uint32_t)(2 * (w + (t >> 1)) + (t & 1))))], c);
         }
-    };
-    hist_pass(0, 0);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < kSelHBins; j += blockDim.x) {
+        const uint32_t v = hs[j];
+        if (v) atomicAdd(hist + j, v);
+    }
     TMARK();
     grid.sync();
     unsigned long long base = 0;
-    const uint32_t e0 = (uint32_t)block_find_all(hist, true, kSelHBins, k, base, &s_idx, &s_before, wsum);
-    // ---- A2: the next 12 bits inside that exponent
-    hist_pass(1, e0);
+    const uint32_t bin = (uint32_t)block_find_all(hist, true, kSelHBins, k, base, &s_idx, &s_before, wsum);
     TMARK();
-    grid.sync();
-    const uint32_t bin = (e0 << 12) |
-                         (uint32_t)block_find_all(hist + kSelHBins, true, kSelHBins, k, base, &s_idx, &s_before, wsum);
-    TMARK();
-    // ---- D: candidates = items whose top 24 key bits are `bin`
-    for (int64_t ib = i0; ib < i1; ib += kUnr * blockDim.x) {
-        uint32_t c[kUnr];
+    // ---- D: candidates = the items of that bin
+    for (int64_t wb = w0; wb < w1; wb += kUnr * blockDim.x) {
+        uint2 c[kUnr];
 #pragma unroll
         for (int u = 0; u < kUnr; ++u) {
-            const int64_t i = ib + (int64_t)u * blockDim.x + threadIdx.x;
-            c[u] = i < i1 ? counts[i] : 0u;
+            const int64_t w = wb + (int64_t)u * blockDim.x + threadIdx.x;
+            c[u] = w < w1 ? reinterpret_cast<const uint2*>(counts)[w] : make_uint2(0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < kUnr; ++u) {
-            const int64_t i = ib + (int64_t)u * blockDim.x + threadIdx.x;
-            const bool f = c[u] && (item_key((uint32_t)i) >> 40) == bin;
+        for (int u = 0; u < 2 * kUnr; ++u) {
+            const int64_t j = 2 * (wb + (int64_t)(u >> 1) * blockDim.x + threadIdx.x) + (u & 1);
+            const uint32_t cnt = (u & 1) ? c[u >> 1].y : c[u >> 1].x;
+            const unsigned long long key = cnt ? item_key((uint32_t)j) : 0ull;
+            const bool f = cnt && bin_of(key) == bin;
             const uint32_t m = __ballot_sync(0xffffffffu, f);
             if (m) {
                 uint32_t pos = 0;
                 if (lane == 0) pos = atomicAdd(&so->n_cand, (uint32_t)__popc(m));
                 pos = __shfl_sync(0xffffffffu, pos, 0);
-                if (f) cand[pos + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+                if (f)  // (key, count) so that the ranking needs one load per candidate
+                    reinterpret_cast<ulonglong2*>(cand)[pos + __popc(m & ((1u << lane) - 1u))] =
+                        make_ulonglong2(key, cnt);
             }
         }
     }
@@ -414,13 +370,13 @@ __global__ void __launch_bounds__(kSelThreads) k_select4(const uint32_t* __restr
     uint32_t eq_total = 0;
     if (nc <= (uint32_t)kCandCap) {
         // cached: each candidate's rank range [below, below + eq) by direct
-        // comparison with all others (nc is small: 24 key bits are fixed)
+        // comparison with all others (nc is small at 2^-8-octave bins)
         __shared__ unsigned long long s_T, s_kk;
         __shared__ uint32_t s_eq;
         for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
-            const uint32_t i = __ldcg(cand + j);
-            ckey[j] = item_key(i);
-            ccnt[j] = counts[i];
+            const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(cand) + j);
+            ckey[j] = e.x;
+            ccnt[j] = (uint32_t)e.y;
         }
         __syncthreads();
         for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
@@ -444,15 +400,15 @@ __global__ void __launch_bounds__(kSelThreads) k_select4(const uint32_t* __restr
         kk = s_kk;
         eq_total = s_eq;
         __syncthreads();
-    } else {  // many candidates: 8-bit radix passes over the other 40 bits, from L2
-        unsigned long long prefix = bin;
-        for (int shift = 32; shift >= 0; shift -= 8) {
+    } else {  // many candidates: 8-bit radix passes over the whole key, from L2
+        unsigned long long prefix = 0;
+        for (int shift = 56; shift >= 0; shift -= 8) {
             for (int j = threadIdx.x; j < 256; j += blockDim.x) h[j] = 0;
             __syncthreads();
             for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
-                const uint32_t i = __ldcg(cand + j);
-                const unsigned long long key = item_key(i);
-                if ((key >> (shift + 8)) == prefix) atomicAdd(&h[(key >> shift) & 0xFFu], counts[i]);
+                const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(cand) + j);
+                if (shift == 56 || (e.x >> (shift + 8)) == prefix)
+                    atomicAdd(&h[(e.x >> shift) & 0xFFu], (uint32_t)e.y);
             }
             __syncthreads();
             unsigned long long b2 = 0;
@@ -508,13 +464,13 @@ __global__ void __launch_bounds__(kSelThreads) k_select4(const uint32_t* __restr
     grid.sync();
     TMARK();
     // ---- G: the tie columns in ascending order (shared list), ties per CTA
-    const int nw = (int)((cols + 31) >> 5);
+    const int nmw = (int)((cols + 31) >> 5);
     uint32_t E;
     {
-        const int per_w = (nw + blockDim.x - 1) / blockDim.x;
-        const int w0 = threadIdx.x * per_w, w1 = min(nw, w0 + per_w);
+        const int per_w = (nmw + blockDim.x - 1) / blockDim.x;
+        const int m0 = threadIdx.x * per_w, m1 = min(nmw, m0 + per_w);
         uint32_t c = 0;
-        for (int j = w0; j < w1; ++j) c += __popc(__ldcg(eqmask + j));
+        for (int j = m0; j < m1; ++j) c += __popc(__ldcg(eqmask + j));
         uint32_t inc = c;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -531,7 +487,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select4(const uint32_t* __restr
         E = tot;
         if (E <= (uint32_t)kEqCap) {
             uint32_t pos = before + inc - c;
-            for (int j = w0; j < w1; ++j)
+            for (int j = m0; j < m1; ++j)
                 for (uint32_t m = __ldcg(eqmask + j); m; m &= m - 1) elist[pos++] = (uint32_t)j * 32 + __ffs(m) - 1;
         }
         __syncthreads();
@@ -604,9 +560,11 @@ __global__ void __launch_bounds__(kSelThreads) k_select4(const uint32_t* __restr
 #endif
 }
 
-// out = q with |q| < bound[c] zeroed, and the ties (bound <= |q| in [lo, hi))
-// at flat index <= cut: one streaming pass, 16 B per thread step, four in flight.
-constexpr int kApThreads = 256, kApVec = 4;
+// out = q with |q| < bound[c] zeroed, and the ties (|q| in [lo, hi)) at flat
+// index <= cut.  16-B path: a thread owns 16 columns (bounds in registers,
+// loaded once) and streams rows, a warp covering 512 contiguous bytes of a
+// row, kApUnr rows in flight.
+constexpr int kApThreads = 256, kApUnr = 4;
 
 __device__ __forceinline__ uint32_t zero_mask4(uint32_t qw, uint32_t bw, uint32_t lw, uint32_t hw, uint32_t cw) {
     const uint32_t a = __vabs4(qw);
@@ -615,50 +573,58 @@ __device__ __forceinline__ uint32_t zero_mask4(uint32_t qw, uint32_t bw, uint32_
     return qw & ~(lt | tie);
 }
 
-__global__ void __launch_bounds__(kApThreads) k_apply4(const int8_t* __restrict__ q, const uint8_t* __restrict__ bound,
+__global__ void __launch_bounds__(kApThreads) k_apply5(const int8_t* __restrict__ q, const uint8_t* __restrict__ bound,
                                                        const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi,
-                                                       int64_t n, int64_t cols, bool vec,
-                                                       const SelectOut* __restrict__ so, int8_t* __restrict__ out) {
+                                                       int64_t rows, int64_t cols, const SelectOut* __restrict__ so,
+                                                       int8_t* __restrict__ out) {
+    const int64_t c0 = ((int64_t)blockIdx.x * kApThreads + threadIdx.x) * 16;
+    if (c0 >= cols) return;
     const unsigned long long cut = so->cut;
-    const int64_t stride = (int64_t)gridDim.x * kApThreads * 16 * kApVec;
-    if (vec) {  // cols % 16 == 0, 16-B aligned: each vector lies in one row
-        for (int64_t base = ((int64_t)blockIdx.x * kApThreads * kApVec + threadIdx.x) * 16; base < n; base += stride) {
-            uint4 v[kApVec];
+    const uint4 b = *reinterpret_cast<const uint4*>(bound + c0);
+    const uint4 l = *reinterpret_cast<const uint4*>(lo + c0);
+    const uint4 h = *reinterpret_cast<const uint4*>(hi + c0);
+    const int64_t G = gridDim.y;
+    for (int64_t r = blockIdx.y; r < rows; r += G * kApUnr) {
+        uint4 v[kApUnr];
 #pragma unroll
-            for (int u = 0; u < kApVec; ++u) {
-                const int64_t i0 = base + (int64_t)u * kApThreads * 16;
-                v[u] = i0 < n ? __ldcs(reinterpret_cast<const uint4*>(q + i0)) : make_uint4(0, 0, 0, 0);
-            }
-#pragma unroll
-            for (int u = 0; u < kApVec; ++u) {
-                const int64_t i0 = base + (int64_t)u * kApThreads * 16;
-                if (i0 >= n) break;
-                const uint32_t c0 = (uint32_t)((uint64_t)i0 % (uint64_t)cols);
-                const uint4 b = *reinterpret_cast<const uint4*>(bound + c0);
-                const uint4 l = *reinterpret_cast<const uint4*>(lo + c0);
-                const uint4 h = *reinterpret_cast<const uint4*>(hi + c0);
-                // ties at index <= cut: byte j of word w is element 4w + j
-                uint32_t cw[4];
-                const long long ck = (long long)cut - i0;  // cut = ~0: every tie (ck < 0 as signed, handled)
-                if (cut == ~0ull || ck >= 15) {
-                    cw[0] = cw[1] = cw[2] = cw[3] = 0xFFFFFFFFu;
-                } else if (ck < 0) {
-                    cw[0] = cw[1] = cw[2] = cw[3] = 0u;
-                } else {
-#pragma unroll
-                    for (int w = 0; w < 4; ++w)
-                        cw[w] = __vcmpleu4(0x03020100u + 0x04040404u * w, 0x01010101u * (uint32_t)ck);
-                }
-                uint4 o;
-                o.x = zero_mask4(v[u].x, b.x, l.x, h.x, cw[0]);
-                o.y = zero_mask4(v[u].y, b.y, l.y, h.y, cw[1]);
-                o.z = zero_mask4(v[u].z, b.z, l.z, h.z, cw[2]);
-                o.w = zero_mask4(v[u].w, b.w, l.w, h.w, cw[3]);
-                __stcs(reinterpret_cast<uint4*>(out + i0), o);
-            }
+        for (int u = 0; u < kApUnr; ++u) {
+            const int64_t rr = r + u * G;
+            v[u] = rr < rows ? __ldcs(reinterpret_cast<const uint4*>(q + rr * cols + c0)) : make_uint4(0, 0, 0, 0);
         }
-        return;
+#pragma unroll
+        for (int u = 0; u < kApUnr; ++u) {
+            const int64_t rr = r + u * G;
+            if (rr >= rows) break;
+            const int64_t i0 = rr * cols + c0;
+            // ties at index <= cut: byte j of word w is element 4w + j
+            uint32_t cw[4];
+            const long long ck = (long long)cut - i0;
+            if (cut == ~0ull || ck >= 15) {
+                cw[0] = cw[1] = cw[2] = cw[3] = 0xFFFFFFFFu;
+            } else if (ck < 0) {
+                cw[0] = cw[1] = cw[2] = cw[3] = 0u;
+            } else {
+#pragma unroll
+                for (int w = 0; w < 4; ++w) cw[w] = __vcmpleu4(0x03020100u + 0x04040404u * w, 0x01010101u * (uint32_t)ck);
+            }
+            uint4 o;
+            o.x = zero_mask4(v[u].x, b.x, l.x, h.x, cw[0]);
+            o.y = zero_mask4(v[u].y, b.y, l.y, h.y, cw[1]);
+            o.z = zero_mask4(v[u].z, b.z, l.z, h.z, cw[2]);
+            o.w = zero_mask4(v[u].w, b.w, l.w, h.w, cw[3]);
+            __stcs(reinterpret_cast<uint4*>(out + i0), o);
+        }
     }
+}
+
+// scalar path (ragged widths / unaligned buffers)
+__global__ void __launch_bounds__(kApThreads) k_apply_bytes(const int8_t* __restrict__ q,
+                                                            const uint8_t* __restrict__ bound,
+                                                            const uint8_t* __restrict__ lo,
+                                                            const uint8_t* __restrict__ hi, int64_t n, int64_t cols,
+                                                            const SelectOut* __restrict__ so,
+                                                            int8_t* __restrict__ out) {
+    const unsigned long long cut = so->cut;
     for (int64_t i = (int64_t)blockIdx.x * kApThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kApThreads) {
         const int64_t c = i % cols;
         const int8_t v = q[i];
@@ -939,15 +905,6 @@ extern "C" int dc_prune_scores(const int8_t* q, const double* cm, int64_t rows, 
     return DC_OK;
 }
 
-static int64_t colhist4_rb(int64_t rows, int64_t cols) {
-    const int64_t n_cb = (cols + kH4Cols - 1) / kH4Cols;
-    int64_t n_rb = 3 * (int64_t)sm_count_pr() / n_cb;  // 3 CTAs per SM, one wave
-    n_rb = n_rb < 1 ? 1 : (n_rb > 64 ? 64 : n_rb);
-    if (n_rb > rows) n_rb = rows > 0 ? rows : 1;
-    const int64_t need = (rows + 65534) / 65535;  // u16 partial counts
-    return n_rb < need ? need : n_rb;
-}
-
 static int64_t colhist5_rb(int64_t rows, int64_t cols) {
     const int64_t n_cb = (cols + kH5Cols - 1) / kH5Cols;
     int64_t n_rb = (int64_t)sm_count_pr() / n_cb;  // one CTA per SM, one wave
@@ -957,18 +914,19 @@ static int64_t colhist5_rb(int64_t rows, int64_t cols) {
     return n_rb < need ? need : n_rb;
 }
 
+// items of the selection = u16 counters of one row block's partial histogram
+static int64_t prune_items(int64_t cols) { return 2 * ((cols + kH5Cols - 1) / kH5Cols) * (int64_t)kH5Words; }
+
 extern "C" int dc_prune_scratch_bytes(int64_t rows, int64_t cols, uint64_t* out) {
-    const uint64_t n_cb = (uint64_t)((cols + kH4Cols - 1) / kH4Cols);
-    const uint64_t items = (uint64_t)cols * kBins;
-    *out = 8ull * kSelHBins + 256 + 4ull * 4096 + 256 + sizeof(SelectOut) + 256 + 4ull * items + 256 + 4ull * cols +
-           256 + 4ull * items + 256 + 3ull * (uint64_t)cols + 256 +
-           2ull * kH4Words * n_cb * (uint64_t)colhist4_rb(rows, cols) +
-           4ull * kH5Words * (uint64_t)((cols + kH5Cols - 1) / kH5Cols) * (uint64_t)colhist5_rb(rows, cols) + 256;
+    const uint64_t items = (uint64_t)prune_items(cols);
+    *out = 8ull * kSelHBins + 256 + 4ull * 4096 + 256 + sizeof(SelectOut) + 256 + 16ull * items + 256 +
+           4ull * (uint64_t)((cols + 31) / 32) + 256 + 4ull * items + 256 + 3ull * (uint64_t)cols + 256 +
+           2ull * items * (uint64_t)colhist5_rb(rows, cols) + 256;
     return DC_OK;
 }
 
-// Per tensor: (column, |q|) histogram (+ sum) -> one cooperative selection
-// launch -> one streaming apply pass (4 launches, was 20 in round 1).
+// Per tensor: (column, |q|) partial histograms -> one cooperative selection
+// launch (sums them) -> one streaming apply pass (3 launches, 20 in round 1).
 extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, int64_t cols, int64_t k,
                                int8_t* out, uint8_t* scratch, void* stream) {
     if (rows < 0 || cols < 0 || k < 0 || k > rows * cols) return DC_ERR_ARG;
@@ -990,7 +948,7 @@ extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, 
     auto align = [](uint8_t* p) {
         return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255);
     };
-    const int64_t items = cols * kBins;
+    const int64_t items = prune_items(cols);
     uint8_t* p = align(scratch);
     auto* hist = reinterpret_cast<uint32_t*>(p);
     p = align(p + 8ull * kSelHBins);
@@ -998,8 +956,8 @@ extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, 
     p = align(p + 4ull * 4096);
     auto* so = reinterpret_cast<SelectOut*>(p);
     p = align(p + sizeof(SelectOut));
-    auto* cand = reinterpret_cast<uint32_t*>(p);
-    p = align(p + 4ull * items);
+    auto* cand = reinterpret_cast<uint32_t*>(p);  // 16-B (key, count) entries
+    p = align(p + 16ull * items);
     auto* eqmask = reinterpret_cast<uint32_t*>(p);
     p = align(p + 4ull * ((cols + 31) / 32));
     auto* counts = reinterpret_cast<uint32_t*>(p);
@@ -1008,44 +966,22 @@ extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, 
     uint8_t* lo = p + cols;
     uint8_t* hi = p + 2 * cols;
     p = align(p + 3ull * cols);
-    auto* partial = reinterpret_cast<uint16_t*>(p);
+    auto* partial = reinterpret_cast<uint32_t*>(p);
     const bool vec = cols % 16 == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
                      (reinterpret_cast<uintptr_t>(out) & 15) == 0;
 
-    if (vec) {  // 16-B path
-        const int64_t n_cb = (cols + kH5Cols - 1) / kH5Cols;
-        int64_t n_rb = colhist5_rb(rows, cols);
-        const int64_t rows_per = (rows + n_rb - 1) / n_rb;
-        n_rb = (rows + rows_per - 1) / rows_per;
-        static bool attr5 = false;
-        if (!attr5) {
-            cudaFuncSetAttribute(k_colhist5, cudaFuncAttributeMaxDynamicSharedMemorySize, kH5Smem);
-            attr5 = true;
-        }
-        auto* part = reinterpret_cast<uint32_t*>(partial);
-        k_colhist5<<<dim3((unsigned)n_rb, (unsigned)n_cb), kH5Threads, kH5Smem, st>>>(q, rows, cols, rows_per, part);
-        DC_CHECK_LAUNCH("k_colhist5");
-        k_colhist5_sum<<<(unsigned)(sm_count_pr() * 8), 256, 0, st>>>(part, n_rb, n_cb, cols, counts, hist, eqmask,
-                                                                       so);
-        DC_CHECK_LAUNCH("k_colhist5_sum");
-    } else {
-        const int64_t n_cb = (cols + kH4Cols - 1) / kH4Cols;
-        int64_t n_rb = colhist4_rb(rows, cols);
-        const int64_t rows_per = (rows + n_rb - 1) / n_rb;
-        n_rb = (rows + rows_per - 1) / rows_per;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_colhist4, cudaFuncAttributeMaxDynamicSharedMemorySize, kH4Smem);
-            attr = true;
-        }
-        const bool vec4 = cols % 4 == 0 && (reinterpret_cast<uintptr_t>(q) & 3) == 0;
-        k_colhist4<<<dim3((unsigned)n_rb, (unsigned)n_cb), kH4Threads, kH4Smem, st>>>(q, rows, cols, rows_per, vec4,
-                                                                                      partial);
-        DC_CHECK_LAUNCH("k_colhist4");
-        k_colhist4_sum<<<(unsigned)(sm_count_pr() * 8), 256, 0, st>>>(partial, n_rb, n_cb, cols, counts, hist, eqmask,
-                                                                       so);
-        DC_CHECK_LAUNCH("k_colhist4_sum");
+    int64_t n_cb = (cols + kH5Cols - 1) / kH5Cols;
+    int64_t n_rb = colhist5_rb(rows, cols);
+    const int64_t rows_per = (rows + n_rb - 1) / n_rb;
+    n_rb = (rows + rows_per - 1) / rows_per;
+    static bool attr5 = false;
+    if (!attr5) {
+        cudaFuncSetAttribute(k_colhist5, cudaFuncAttributeMaxDynamicSharedMemorySize, kH5Smem);
+        attr5 = true;
     }
+    k_colhist5<<<dim3((unsigned)n_rb, (unsigned)n_cb), kH5Threads, kH5Smem, st>>>(q, cm, rows, cols, rows_per, vec,
+                                                                                  partial, hist, eqmask, so);
+    DC_CHECK_LAUNCH("k_colhist5");
     {  // the k-th score, the per-column bounds and the tie cut: one cooperative launch
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select4, kSelThreads, 0);
@@ -1056,8 +992,9 @@ extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, 
         int grid = sm_count_pr();
         if (grid > 4096) grid = 4096;  // psum slots
         unsigned long long kk = (unsigned long long)k;
-        void* args[] = {(void*)&counts, (void*)&cm, (void*)&q, (void*)&rows, (void*)&cols, (void*)&kk, (void*)&so,
-                        (void*)&hist, (void*)&psum, (void*)&cand, (void*)&eqmask, (void*)&bound, (void*)&lo, (void*)&hi};
+        void* args[] = {(void*)&partial, (void*)&n_rb, (void*)&n_cb, (void*)&counts, (void*)&cm, (void*)&q,
+                        (void*)&rows, (void*)&cols, (void*)&kk, (void*)&so, (void*)&hist, (void*)&psum,
+                        (void*)&cand, (void*)&eqmask, (void*)&bound, (void*)&lo, (void*)&hi};
         cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_select4, dim3((unsigned)grid), dim3(kSelThreads),
                                                     args, 0, st);
         if (e != cudaSuccess) {
@@ -1065,11 +1002,16 @@ extern "C" int dc_prune_tensor(const int8_t* q, const double* cm, int64_t rows, 
             return DC_ERR_CUDA;
         }
     }
-    const int64_t want = (n + (int64_t)kApThreads * 16 * kApVec - 1) / ((int64_t)kApThreads * 16 * kApVec);
-    const int64_t cap = (int64_t)sm_count_pr() * 8;
-    const int64_t g = vec ? (want < cap ? want : cap) : cap;
-    k_apply4<<<(unsigned)g, kApThreads, 0, st>>>(q, bound, lo, hi, n, cols, vec, so, out);
-    DC_CHECK_LAUNCH("k_apply4");
+    if (vec) {
+        const int64_t gx = (cols / 16 + kApThreads - 1) / kApThreads;
+        int64_t gy = (int64_t)sm_count_pr() * 8 / gx;
+        gy = gy < 1 ? 1 : (gy > rows ? rows : gy);
+        k_apply5<<<dim3((unsigned)gx, (unsigned)gy), kApThreads, 0, st>>>(q, bound, lo, hi, rows, cols, so, out);
+        DC_CHECK_LAUNCH("k_apply5");
+    } else {
+        k_apply_bytes<<<(unsigned)(sm_count_pr() * 8), kApThreads, 0, st>>>(q, bound, lo, hi, n, cols, so, out);
+        DC_CHECK_LAUNCH("k_apply_bytes");
+    }
     return DC_OK;
 }
 
