@@ -274,44 +274,104 @@ __global__ void __launch_bounds__(kQThreads) k_absmax_v(const typename In<T>::ty
     }
 }
 
+#ifndef DC_QUANT_MINB
+#define DC_QUANT_MINB 4  // <= 64 registers: 4 CTAs per SM (fewer registers spill, measured slower)
+#endif
+
+// f32 product path for 8 elements: q bytes packed in (lo, hi), and whether any
+// of them lies within 1e-4 of a half-integer (then the caller redoes the 8
+// exactly).  Branch-free: one test per 8 elements instead of a convergence
+// barrier per element.
+__device__ __forceinline__ uint32_t q8_fast_byte(float wf, float cf, bool& near) {
+    const float xf = wf * cf;
+    const float a = fabsf(xf);
+    const float t = __fadd_rn(a, 8388608.0f);  // 2^23: the nearest integer lands in the mantissa
+    const float d = __fsub_rn(a, __fsub_rn(t, 8388608.0f));
+    near |= fabsf(fabsf(d) - 0.5f) < 1e-4f;
+    const int r = min((int)(__float_as_uint(t) & 0x7FFFFFu), 127);
+    return (uint32_t)(uint8_t)(int8_t)(xf < 0.0f ? -r : r);
+}
+
+// q of 8 elements by the reference's exact f64 formula (re-reads w and s)
 template <int T>
-__global__ void __launch_bounds__(kQThreads) k_quantize_v(const typename In<T>::type* __restrict__ w,
+__device__ __noinline__ void exact8(const typename In<T>::type* __restrict__ w, const double* __restrict__ s, int64_t e,
+                                    int64_t c, double w_scale, uint32_t& lo, uint32_t& hi) {
+    Raw8<T> v;
+    load_raw8<T>(w, e, v);
+    double sc[8];
+    load_s8(s, c, sc);
+    lo = hi = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t b = (uint8_t)q_of(__dmul_rn(raw_at<T>(v, k), sc[k]), w_scale);
+        if (k < 4)
+            lo |= b << (8 * k);
+        else
+            hi |= b << (8 * (k - 4));
+    }
+}
+
+template <int T>
+__global__ void __launch_bounds__(kQThreads, DC_QUANT_MINB) k_quantize_v(const typename In<T>::type* __restrict__ w,
                                                            const double* __restrict__ s, int64_t rows, int64_t cols,
                                                            int64_t rows_par, double w_scale, int8_t* __restrict__ q) {
     const int64_t gpr = cols / 8, t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t cg = t % gpr, rp = t / gpr;
-    double sc[8];
-    load_s8(s, cg * 8, sc);
-    float cf[8];  // s[col] / w_scale in f32 (see q_of_f32)
+    {
+        // only cf stays in registers (the f64 scales are re-read in the rare
+        // exact path); kQR rows of raw loads are in flight per thread
+        float cf[8];
+        {
+            double sc[8];
+            load_s8(s, cg * 8, sc);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) cf[k] = __double2float_rn(sc[k] / w_scale);
-    // kQR rows per iteration, raw (un-widened) loads all issued before any use:
-    // the kernel is memory-latency bound with one row in flight per thread
+            for (int k = 0; k < 8; ++k) cf[k] = __double2float_rn(sc[k] / w_scale);
+        }
 #ifndef DC_QUANT_ROWS
 #define DC_QUANT_ROWS 1
 #endif
-    constexpr int kQR = T == kF64 ? 1 : DC_QUANT_ROWS;
-    for (int64_t r0 = rp; r0 < rows && rp < rows_par; r0 += kQR * rows_par) {
-        Raw8<T> v[kQR];
-#pragma unroll
-        for (int j = 0; j < kQR; ++j) {
-            const int64_t r = r0 + j * rows_par;
-            if (r < rows) load_raw8<T>(w, r * cols + cg * 8, v[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < kQR; ++j) {
-            const int64_t r = r0 + j * rows_par;
-            if (r >= rows) break;
-            uint32_t lo = 0, hi = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t b = (uint8_t)q_of_f32(raw_at_f32<T>(v[j], k), cf[k], raw_at<T>(v[j], k), sc[k], w_scale);
-                if (k < 4)
-                    lo |= b << (8 * k);
-                else
-                    hi |= b << (8 * (k - 4));
+#ifndef DC_QUANT_PF
+#define DC_QUANT_PF 1  // rows ahead whose warp span is bulk-prefetched into L2 (0: off)
+#endif
+        constexpr int kQR = DC_QUANT_ROWS;
+        // the warp's 32 consecutive 8-column groups are one contiguous span of
+        // a row (when they do not wrap): lane 0 bulk-prefetches the span
+        // DC_QUANT_PF rows ahead into L2, so more bytes are in flight than the
+        // registers of 4 resident CTAs can hold
+        const int64_t cg0 = __shfl_sync(0xffffffffu, cg, 0);
+        const bool span = DC_QUANT_PF > 0 && (threadIdx.x & 31) == 0 && cg0 + 32 <= gpr;
+        constexpr uint32_t kSpan = 32 * 8 * sizeof(typename In<T>::type);
+        for (int64_t r0 = rp; r0 < rows && rp < rows_par; r0 += kQR * rows_par) {
+            if (span) {
+                const int64_t rf = r0 + (int64_t)DC_QUANT_PF * kQR * rows_par;
+                if (rf < rows)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(w + rf * cols + cg0 * 8), "r"(kSpan)
+                                 : "memory");
             }
-            *reinterpret_cast<uint2*>(q + r * cols + cg * 8) = make_uint2(lo, hi);
+            Raw8<T> v[kQR];
+#pragma unroll
+            for (int j = 0; j < kQR; ++j) {
+                const int64_t r = r0 + j * rows_par;
+                if (r < rows) load_raw8<T>(w, r * cols + cg * 8, v[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < kQR; ++j) {
+                const int64_t r = r0 + j * rows_par;
+                if (r >= rows) break;
+                uint32_t lo = 0, hi = 0;
+                bool near = false;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t b = q8_fast_byte(raw_at_f32<T>(v[j], k), cf[k], near);
+                    if (k < 4)
+                        lo |= b << (8 * k);
+                    else
+                        hi |= b << (8 * (k - 4));
+                }
+                if (near)  // rare: the exact f64 rounding for these 8 (out of line)
+                    exact8<T>(w, s, r * cols + cg * 8, cg * 8, w_scale, lo, hi);
+                *reinterpret_cast<uint2*>(q + r * cols + cg * 8) = make_uint2(lo, hi);
+            }
         }
     }
 }

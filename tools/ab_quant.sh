@@ -1,2 +1,2 @@
 #!/bin/bash
-for lib in ab/*.so; do echo "== $lib"; DCOMP_LIB=$lib python tools/profile_quant.py 2>&1 | grep quantize; done
+for lib in ab/*.so; do echo "== $lib"; DCOMP_LIB=$lib python tools/profile_quant.py 2>&1 | grep -E "quantize|absmax"; done
