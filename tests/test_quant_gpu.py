@@ -53,6 +53,28 @@ def test_device_dtypes_match_f64(cuda):
         assert torch.equal(q1, q2) and s1 == s2
 
 
+def test_vector_path_half_integers_match_oracle(cuda, oracle):
+    """The 8-column vector kernels (cols % 8 == 0) on every input dtype, with
+    values placed on, just below and just above half-integers of w*s/w_scale,
+    so the branch-free f32-product rounding hands those groups to the exact
+    f64 path; q must equal the reference's rounding of the widened values."""
+    from paper_2502_15443_b200.scaling import quantize_device
+    rng = np.random.default_rng(77)
+    rows, cols = 96, 256
+    base = rng.integers(-126, 126, (rows, cols)).astype(np.float64)
+    frac = rng.choice([0.5, 0.5 - 2 ** -14, 0.5 + 2 ** -14, 0.49999, 0.50001, 0.25, 0.0], (rows, cols))
+    w = (base + np.sign(base + 0.1) * frac) / 127.0
+    w[0, 0] = 1.0  # max |w| = 1 -> w_scale = 1/127
+    for dt in (torch.float64, torch.float32, torch.bfloat16, torch.float16):
+        wd = torch.from_numpy(w).to(dt).cuda()
+        wide = wd.to(torch.float64).cpu().numpy()
+        for s in (None, rng.uniform(0.5, 2.0, cols)):
+            q, ws = quantize_device(wd, None if s is None else torch.from_numpy(s))
+            qo, wso = oracle.quantize(wide, s)
+            assert ws == wso, dt
+            assert np.array_equal(q.cpu().numpy(), qo), (dt, s is None)
+
+
 def test_dequantize_and_scale(cuda):
     rng = np.random.default_rng(8)
     w, st = cuda.synth_ensemble(cuda.SynthSpec(rows=64, cols=96), 3)
