@@ -14,6 +14,7 @@
 // Non-negative doubles order like their u64 bit patterns, so keys are bits.
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -650,6 +651,8 @@ static int sm_count_pr() {
 // computed once; 8 x 8-bit radix passes over a shared 256-bin histogram with a
 // block-scan bucket pick; then the ordered tie pass.
 constexpr int kRowMax = kPrThreads * 16;
+constexpr int kRowBins = 2048;  // per-row key-range histogram
+constexpr int kRowCand = 512;   // candidates ranked directly (else radix over the bin)
 
 __device__ __forceinline__ void block_pick256(const uint32_t* hist, unsigned long long& prefix, unsigned long long& kk,
                                               unsigned long long* s_prefix, unsigned long long* s_k,
@@ -683,22 +686,28 @@ __global__ void __launch_bounds__(kPrThreads) k_prune_rows2(const int8_t* __rest
                                                              int8_t* __restrict__ out) {
     // persistent over rows: thread t owns columns [16t, 16t + 16) of every row,
     // their channel maxima stay in registers (one load per CTA, not per row)
-    __shared__ uint32_t hist[256];
-    __shared__ uint32_t wsum[kPrThreads / 32];
+    __shared__ uint32_t hist[256], rbins[kRowBins];
+    __shared__ uint32_t wsum[kPrThreads / 32], s_nc, s_bin;
     __shared__ unsigned long long s_prefix, s_k[2], s_min[kPrThreads / 32], s_max[kPrThreads / 32];
+    __shared__ unsigned long long cand[kRowCand];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int c0 = t * 16;
     double cmr[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) cmr[j] = c0 + j < cols ? cm[c0 + j] : 0.0;
     const bool vec = (cols & 15) == 0 && ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    // the next row's 16 bytes are loaded before this row is processed (the
+    // load latency was the largest stall: one row per CTA at a time)
+    uint4 qnext = make_uint4(0, 0, 0, 0);
+    if (vec && c0 < cols && blockIdx.x < rows) qnext = *reinterpret_cast<const uint4*>(q + (int64_t)blockIdx.x * cols + c0);
     for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
         const int8_t* qr = q + row * cols;
         int8_t* orow = out + row * cols;
         int8_t v[16];
         if (vec) {
-            uint4 qv = make_uint4(0, 0, 0, 0);
-            if (c0 < cols) qv = *reinterpret_cast<const uint4*>(qr + c0);
+            const uint4 qv = qnext;
+            if (c0 < cols && row + gridDim.x < rows)
+                qnext = *reinterpret_cast<const uint4*>(q + (row + gridDim.x) * cols + c0);
             memcpy(v, &qv, 16);
         } else {
 #pragma unroll
@@ -710,12 +719,17 @@ __global__ void __launch_bounds__(kPrThreads) k_prune_rows2(const int8_t* __rest
         for (int j = 0; j < 16; ++j) {
             key[j] = c0 + j < cols ? key_of(cmr[j], absq(v[j])) : ~0ull;
             if (c0 + j < cols) {
-                kmin = min(kmin, key[j]);
+                if (key[j]) kmin = min(kmin, key[j]);  // smallest POSITIVE key (0 has its own bin)
                 kmax = max(kmax, key[j]);
             }
         }
-        // the row's keys share their leading bytes (scores span a few binades):
-        // start the radix passes at the first byte where min and max differ
+        unsigned long long prefix, kk;
+        {
+        // One histogram pass over the row's key range (kRowBins bins: bin 0 =
+        // score 0, then positive keys >> sh offset to the smallest), the
+        // rank-k bin by a block scan, then the exact k-th key among that bin's
+        // (few) candidates by direct ranking -- instead of up to eight 8-bit
+        // radix passes of 64-bit compares and shifts per element (ALU-bound).
 #pragma unroll
         for (int d = 16; d; d >>= 1) {
             kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, d));
@@ -726,32 +740,98 @@ __global__ void __launch_bounds__(kPrThreads) k_prune_rows2(const int8_t* __rest
             s_min[w] = kmin;
             s_max[w] = kmax;
         }
+        for (int i = t; i < kRowBins; i += kPrThreads) rbins[i] = 0;
+        if (t == 0) s_nc = 0;
         __syncthreads();
         for (int i = 0; i < kPrThreads / 32; ++i) {
             kmin = min(kmin, s_min[i]);
             kmax = max(kmax, s_max[i]);
         }
-        const int p0 = kmin == kmax ? 8 : __clzll(kmin ^ kmax) / 8;
-        unsigned long long prefix = p0 == 0 ? 0ull : p0 == 8 ? kmin : kmin >> (64 - 8 * p0);
-        unsigned long long kk = (unsigned long long)k;
-        for (int pass = p0; pass < 8; ++pass) {
-            const int shift = 56 - 8 * pass;
-            hist[t] = 0;
-            __syncthreads();
+        // kmin here is the smallest positive key (zero keys were excluded below)
+        // (kmax >> sh) - (kmin >> sh) <= ((kmax - kmin) >> sh) + 1 < 1025 bins
+        const unsigned long long span = kmin == ~0ull ? 0ull : kmax - kmin;
+        const int sh = max(0, 64 - __clzll(span) - 10);
+        auto rbin = [&](unsigned long long key) -> uint32_t {
+            return key == 0 ? 0u : 1u + (uint32_t)((key >> sh) - (kmin >> sh));
+        };
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < cols && (pass == 0 || (key[j] >> (shift + 8)) == prefix))
-                    atomicAdd(&hist[(key[j] >> shift) & 0xFF], 1u);
+        for (int j = 0; j < 16; ++j)
+            if (c0 + j < cols) atomicAdd(&rbins[rbin(key[j])], 1u);
+        __syncthreads();
+        // block scan over the bins: kRowBins / kPrThreads consecutive bins per thread
+        constexpr int kPer = kRowBins / kPrThreads;
+        uint32_t loc[kPer], tot = 0;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            loc[i] = rbins[t * kPer + i];
+            tot += loc[i];
+        }
+        uint32_t inc = tot;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        uint32_t before = 0;
+        for (int i = 0; i < w; ++i) before += wsum[i];
+        uint32_t c = before + inc - tot;
+        const unsigned long long kq = (unsigned long long)k;
+        if (c < kq && kq <= c + tot) {
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                if (c < kq && kq <= c + loc[i]) {
+                    s_bin = (uint32_t)(t * kPer + i);
+                    s_k[0] = kq - c;  // rank inside the bin (1-based)
+                }
+                c += loc[i];
+            }
+        }
+        __syncthreads();
+        const uint32_t bsel = s_bin;
+        kk = s_k[0];
+        // candidates: the keys of the chosen bin
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (c0 + j < cols && rbin(key[j]) == bsel) {
+                const uint32_t pos = atomicAdd(&s_nc, 1u);
+                if (pos < kRowCand) cand[pos] = key[j];
+            }
+        }
+        __syncthreads();
+        const uint32_t nc = s_nc;
+        if (nc <= kRowCand) {
+            for (uint32_t i = t; i < nc; i += kPrThreads) {
+                const unsigned long long ki = cand[i];
+                uint32_t lt = 0, eq = 0;
+                for (uint32_t m = 0; m < nc; ++m) {
+                    lt += cand[m] < ki;
+                    eq += cand[m] == ki;
+                }
+                if (lt < kk && kk <= lt + eq) {  // every candidate equal to T writes the same
+                    s_prefix = ki;
+                    s_k[1] = kk - lt;
+                }
+            }
             __syncthreads();
-            block_pick256(hist, prefix, kk, &s_prefix, s_k, wsum);
-            if (s_k[1] == 1 && shift > 0) {  // one key in the bucket: it is the threshold
+            prefix = s_prefix;
+            kk = s_k[1];
+        } else {  // many equal-bin keys (e.g. constant channel maxima): 8-bit radix over the bin's keys
+            prefix = 0;
+            for (int pass = 0; pass < 8; ++pass) {
+                const int shift = 56 - 8 * pass;
+                hist[t] = 0;
+                __syncthreads();
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
-                    if (c0 + j < cols && (key[j] >> shift) == prefix) s_prefix = key[j];
+                    if (c0 + j < cols && rbin(key[j]) == bsel && (pass == 0 || (key[j] >> (shift + 8)) == prefix))
+                        atomicAdd(&hist[(key[j] >> shift) & 0xFF], 1u);
                 __syncthreads();
-                prefix = s_prefix;
-                break;
+                block_pick256(hist, prefix, kk, &s_prefix, s_k, wsum);
             }
+        }
+        __syncthreads();
         }
         // ordered ties: zero key < T, and the first kk entries with key == T
         const unsigned long long T = prefix;
@@ -794,6 +874,301 @@ __global__ void __launch_bounds__(kPrThreads) k_prune_rows2(const int8_t* __rest
             for (int j = 0; j < 16; ++j)
                 if (c0 + j < cols) orow[c0 + j] = v[j];
         }
+    }
+}
+
+// Per row, one WARP per row (no block barriers): lane L holds the 16-byte
+// pieces at columns 512 m + 16 L (m = 0..7: up to 4096 columns, 16-aligned)
+// in registers; the channel maxima sit in shared memory in the matching
+// order (column 512 m + 16 L + e at index 512 m + 32 e + L: conflict-free
+// LDS.64 for every lane).  Keys are recomputed per pass (one DMUL each)
+// rather than stored.  The histogram bins are fixed for the whole tensor:
+// the high words of the keys between those of (min cm > 0) x 1 and
+// (max cm) x 128, >> s so they fit kRwBins (bin 0: high word 0, i.e. score 0
+// or subnormal) -- no per-row min / max pass, 32-bit bin arithmetic.  Then
+// the rank-k bin by a warp scan, the (few) candidates of that bin ranked
+// directly on their full keys (8-bit radix passes if there are many), and the
+// apply pass, with the tie ranks in column order by per-chunk warp scans only
+// when some ties stay.
+constexpr int kRwWarps = 16;
+constexpr int kRwBins = 1056;  // 33 per lane
+constexpr int kRwCand = 64;
+
+struct RwSmem {
+    double cm[kRowMax];  // permuted channel maxima
+    uint32_t hist[kRwWarps][kRwBins];
+    unsigned long long cand[kRwWarps][kRwCand];
+    uint16_t ccol[kRwWarps][kRwCand];
+    double red[2][kRwWarps];
+};
+
+template <bool FULL>  // cols % 512 == 0: every lane holds every chunk
+__global__ void __launch_bounds__(kRwWarps * 32, 2) k_prune_rowsw(const int8_t* __restrict__ q,
+                                                                  const double* __restrict__ cm, int64_t rows,
+                                                                  int64_t cols, int64_t k, int8_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t rw_raw[];
+    RwSmem& S = *reinterpret_cast<RwSmem*>(rw_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double mn = INFINITY, mx = 0.0;
+    for (int c = threadIdx.x; c < kRowMax; c += blockDim.x) {
+        const int m = c >> 9, L = (c >> 4) & 31, e = c & 15;
+        const double v = c < cols ? cm[c] : 0.0;
+        S.cm[(m << 9) + (e << 5) + L] = v;
+        if (c < cols) {
+            if (v > 0.0) mn = fmin(mn, v);
+            mx = fmax(mx, v);
+        }
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+    }
+    if (lane == 0) {
+        S.red[0][warp] = mn;
+        S.red[1][warp] = mx;
+    }
+    __syncthreads();
+    for (int i = 0; i < kRwWarps; ++i) {
+        mn = fmin(mn, S.red[0][i]);
+        mx = fmax(mx, S.red[1][i]);
+    }
+    // bin(key) = hi == 0 ? 0 : 1 + ((hi - hmin) >> s), hi = key's high word
+    const uint32_t hmin = mn == INFINITY ? 0xFFFFFFFFu : (uint32_t)(__double_as_longlong(mn) >> 32);
+    const uint32_t hmax = (uint32_t)(key_of(mx, 128) >> 32);
+    const uint32_t hspan = hmin == 0xFFFFFFFFu || hmax < hmin ? 0u : hmax - hmin;
+    const int s = max(0, 32 - __clz(hspan) - 10);  // (hspan >> s) < 1024
+    // = hi == 0 ? 0 : 1 + ((hi - hmin) >> s): no positive key has 0 < hi < hmin,
+    // and hi - hmin2 < 2^31 (hi <= 0x7FF00000, hmin2 >= -2^22), so one signed
+    // shift and a clamp at 0 give it
+    const int32_t hmin2 = (int32_t)hmin - (1 << s);
+    auto bin_of = [&](unsigned long long key) -> uint32_t {
+        const int32_t hi = (int32_t)(key >> 32);
+        return (uint32_t)max(0, (hi - hmin2) >> s);
+    };
+    const int nm = (int)((cols + 511) >> 9);  // 512-column chunks
+    uint32_t* H = S.hist[warp];
+    unsigned long long* C = S.cand[warp];
+    uint16_t* CC = S.ccol[warp];
+    const unsigned long long kq = (unsigned long long)k;
+    const int64_t nwarp = (int64_t)gridDim.x * kRwWarps;
+    auto valid = [&](int m) { return FULL || (int64_t)((m << 9) + (lane << 4)) < cols; };
+    auto keyat = [&](const uint4 (&qv)[8], int m, int e) -> unsigned long long {
+        const uint32_t w = (&qv[m].x)[e >> 2];
+        const uint32_t a = __byte_perm(__vabs4(w), 0, 0x4440 + (e & 3));
+        return key_of(S.cm[(m << 9) + (e << 5) + lane], (int)a);
+    };
+    for (int64_t row = (int64_t)blockIdx.x * kRwWarps + warp; row < rows; row += nwarp) {
+        const int8_t* qr = q + row * cols;
+        uint4 qv[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+            qv[m] = (m < nm && valid(m)) ? *reinterpret_cast<const uint4*>(qr + (m << 9) + (lane << 4))
+                                         : make_uint4(0, 0, 0, 0);
+        for (int i = lane; i < kRwBins; i += 32) H[i] = 0;
+        __syncwarp();
+        // ---- histogram
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            if (m >= nm || !valid(m)) continue;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) atomicAdd(&H[bin_of(keyat(qv, m, e))], 1u);
+        }
+        __syncwarp();
+        // ---- rank-k bin: lane L sums bins [33 L, 33 L + 33)
+        constexpr int kPer = kRwBins / 32;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) tot += H[lane * kPer + i];
+        uint32_t inc = tot;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        uint32_t bsel = 0, kin = 0;  // chosen bin, rank inside it
+        {
+            uint32_t c = inc - tot;
+            const bool mine = c < kq && kq <= (unsigned long long)inc;
+            if (mine) {
+                for (int i = 0; i < kPer; ++i) {
+                    const uint32_t h = H[lane * kPer + i];
+                    if (kq <= (unsigned long long)c + h) {
+                        bsel = (uint32_t)(lane * kPer + i);
+                        kin = (uint32_t)(kq - c);
+                        break;
+                    }
+                    c += h;
+                }
+            }
+            const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+            bsel = __shfl_sync(0xffffffffu, bsel, src);
+            kin = __shfl_sync(0xffffffffu, kin, src);
+        }
+        // ---- one pass: bins below the chosen one are zeroed now, bins above
+        // kept, the chosen bin's entries (key + column) listed
+        uint32_t nc = 0;
+        int8_t* orow = out + row * cols;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            if (m >= nm) continue;
+            uint32_t zm = 0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const unsigned long long key = valid(m) ? keyat(qv, m, e) : ~0ull;
+                const uint32_t bn = valid(m) ? bin_of(key) : 0xFFFFFFFFu;
+                zm |= (uint32_t)(bn < bsel) << e;
+                const bool f = bn == bsel;
+                const uint32_t msk = __ballot_sync(0xffffffffu, f);
+                if (msk) {  // warp-uniform and rare (a dozen of 128 steps)
+                    const uint32_t pos = nc + __popc(msk & ((1u << lane) - 1u));
+                    if (f && pos < (uint32_t)kRwCand) {
+                        C[pos] = key;
+                        CC[pos] = (uint16_t)((m << 9) + (lane << 4) + e);
+                    }
+                    nc += __popc(msk);
+                }
+            }
+            uint32_t* w4 = &qv[m].x;
+#pragma unroll
+            for (int b4 = 0; b4 < 4; ++b4)
+                w4[b4] &= ~((((zm >> (4 * b4)) & 15u) * 0x00204081u & 0x01010101u) * 0xFFu);
+        }
+        __syncwarp();
+        if (nc <= (uint32_t)kRwCand) {
+            // rank the candidates: T = the kin-th smallest key; zero those < T and
+            // the first kk (column order) of those == T, in their owners' registers
+            unsigned long long T = 0, kk = 0;
+            for (uint32_t i = lane; i < nc; i += 32) {
+                const unsigned long long ki = C[i];
+                uint32_t lt = 0, eq = 0;
+                for (uint32_t j = 0; j < nc; ++j) {
+                    lt += C[j] < ki;
+                    eq += C[j] == ki;
+                }
+                if (lt < kin && kin <= lt + eq) {
+                    T = ki;
+                    kk = kin - lt;
+                }
+            }
+            const int src = __ffs(__ballot_sync(0xffffffffu, kk != 0)) - 1;
+            T = __shfl_sync(0xffffffffu, T, src);
+            kk = __shfl_sync(0xffffffffu, kk, src);
+            for (uint32_t i = 0; i < nc; ++i) {  // uniform loop; the owner lane applies
+                const uint32_t col = CC[i];
+                if ((int)((col >> 4) & 31) != lane) continue;
+                const unsigned long long ki = C[i];
+                bool z = ki < T;
+                if (ki == T) {  // tie: its rank among the ties in column order
+                    uint32_t r = 0;
+                    for (uint32_t j = 0; j < nc; ++j) r += C[j] == T && CC[j] < col;
+                    z = r < kk;
+                }
+                if (z) {
+                    const int m = col >> 9, e = col & 15;
+                    (&qv[m].x)[e >> 2] &= ~(0xFFu << (8 * (e & 3)));
+                }
+            }
+        } else {  // many keys in one bin (e.g. equal channel maxima): 8-bit radix passes over the bin
+            unsigned long long prefix = 0, kr = kin;
+            for (int pass = 0; pass < 8; ++pass) {
+                const int shift = 56 - 8 * pass;
+                for (int i = lane; i < 256; i += 32) H[i] = 0;
+                __syncwarp();
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    if (m >= nm || !valid(m)) continue;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const unsigned long long key = keyat(qv, m, e);
+                        if (bin_of(key) == bsel && (pass == 0 || (key >> (shift + 8)) == prefix))
+                            atomicAdd(&H[(key >> shift) & 0xFF], 1u);
+                    }
+                }
+                __syncwarp();
+                uint32_t hv[8], ht = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    hv[i] = H[lane * 8 + i];
+                    ht += hv[i];
+                }
+                uint32_t hi2 = ht;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, hi2, d);
+                    if (lane >= d) hi2 += o;
+                }
+                uint32_t c = hi2 - ht, dsel = 0, kn = 0;
+                const bool mine = c < kr && kr <= (unsigned long long)hi2;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (mine && c < kr && kr <= (unsigned long long)c + hv[i]) {
+                        dsel = (uint32_t)(lane * 8 + i);
+                        kn = (uint32_t)(kr - c);
+                    }
+                    c += hv[i];
+                }
+                const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+                dsel = __shfl_sync(0xffffffffu, dsel, src);
+                kr = __shfl_sync(0xffffffffu, kn, src);
+                prefix = (prefix << 8) | dsel;
+                __syncwarp();
+            }
+            const unsigned long long T = prefix, kk = kr;
+            // the chosen bin's entries: < T zeroed, ties in column order
+            uint32_t eqm[8];
+            uint32_t myeq = 0;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                eqm[m] = 0;
+                if (m >= nm || !valid(m)) continue;
+                uint32_t ltm = 0;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const unsigned long long key = keyat(qv, m, e);
+                    if (bin_of(key) != bsel) continue;
+                    ltm |= (uint32_t)(key < T) << e;
+                    eqm[m] |= (uint32_t)(key == T) << e;
+                }
+                myeq += __popc(eqm[m]);
+                uint32_t* w4 = &qv[m].x;
+#pragma unroll
+                for (int b4 = 0; b4 < 4; ++b4)
+                    w4[b4] &= ~((((ltm >> (4 * b4)) & 15u) * 0x00204081u & 0x01010101u) * 0xFFu);
+            }
+            const uint32_t eq_total = __reduce_add_sync(0xffffffffu, myeq);
+            const bool some = (unsigned long long)eq_total > kk;
+            unsigned long long before = 0;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                if (m >= nm) continue;
+                uint32_t z = eqm[m];
+                if (some) {
+                    const uint32_t cnt = __popc(eqm[m]);
+                    uint32_t ic = cnt;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t o = __shfl_up_sync(0xffffffffu, ic, d);
+                        if (lane >= d) ic += o;
+                    }
+                    unsigned long long r = before + ic - cnt;
+                    z = 0;
+                    for (uint32_t e = eqm[m]; e; e &= e - 1) {
+                        if (r < kk) z |= e & (0u - e);
+                        ++r;
+                    }
+                    before += __shfl_sync(0xffffffffu, ic, 31);
+                }
+                uint32_t* w4 = &qv[m].x;
+#pragma unroll
+                for (int b4 = 0; b4 < 4; ++b4)
+                    w4[b4] &= ~((((z >> (4 * b4)) & 15u) * 0x00204081u & 0x01010101u) * 0xFFu);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+            if (m < nm && valid(m)) *reinterpret_cast<uint4*>(orow + (m << 9) + (lane << 4)) = qv[m];
+        __syncwarp();  // the candidate list is rewritten by the next row
     }
 }
 
@@ -1019,6 +1394,24 @@ extern "C" int dc_prune_rows(const int8_t* q, const double* cm, int64_t rows, in
                              void* stream) {
     if (rows < 0 || cols < 0 || k < 0 || k > cols) return DC_ERR_ARG;
     if (rows == 0 || cols == 0) return DC_OK;
+    const bool vec = (cols & 15) == 0 && ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (k > 0 && cols <= kRowMax && vec && !getenv("DC_PRUNE_ROWS_CTA")) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_prune_rowsw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RwSmem));
+            cudaFuncSetAttribute(k_prune_rowsw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RwSmem));
+            attr = true;
+        }
+        const int64_t need = (rows + kRwWarps - 1) / kRwWarps, cap = (int64_t)sm_count_pr() * 2;
+        if (cols % 512 == 0)
+            k_prune_rowsw<true><<<(unsigned)(need < cap ? need : cap), kRwWarps * 32, sizeof(RwSmem),
+                                  (cudaStream_t)stream>>>(q, cm, rows, cols, k, out);
+        else
+            k_prune_rowsw<false><<<(unsigned)(need < cap ? need : cap), kRwWarps * 32, sizeof(RwSmem),
+                                   (cudaStream_t)stream>>>(q, cm, rows, cols, k, out);
+        DC_CHECK_LAUNCH("k_prune_rowsw");
+        return DC_OK;
+    }
     if (k > 0 && cols <= kRowMax) {
         const int64_t cap = (int64_t)sm_count_pr() * 2;  // resident CTAs (123 regs x 256 threads)
         k_prune_rows2<<<(unsigned)(rows < cap ? rows : cap), kPrThreads, 0, (cudaStream_t)stream>>>(q, cm, rows,
