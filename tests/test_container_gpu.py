@@ -178,10 +178,16 @@ def test_structural_errors_with_sidecar(cuda):
         mutants.append(bytes(b))
     mutants += [data[:-1], data + b"\x00", data[:prefix + 5]]
     raised = 0
-    for m in mutants:
+    pside = torch.empty(len(side), dtype=torch.uint8, pin_memory=True)
+    pside.numpy()[:] = np.frombuffer(side, np.uint8)
+    for i, m in enumerate(mutants):
         want = outcome(lambda: container.unpack(m))
         got = outcome(lambda: container.unpack(m, index=side))
         assert got == want
+        if i % 4 == 0:  # the pinned-tensor input parses a zero-copy view of the prefix
+            pin = torch.empty(len(m), dtype=torch.uint8, pin_memory=True)
+            pin.numpy()[:] = np.frombuffer(m, np.uint8)
+            assert outcome(lambda: container.unpack(pin, index=pside)) == want
         raised += want is not None
     assert raised >= 70
 
