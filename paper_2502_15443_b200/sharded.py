@@ -223,3 +223,62 @@ def unpack_shard(src, rank: int, world: int, index=None, device=None, group=None
         key = int(k.item())
     _raise_verdict(key)
     return ShardResult(sh, out, directory, chunk_size)
+
+
+# ----------------------------------------------------- quantize + prune by tensor
+def plan_tensor_shards(sizes, world: int) -> list[tuple[int, int]]:
+    """Contiguous tensor ranges per rank, balanced by element count (SURVEY
+    §8(e): absmax, threshold and k are tensor-local -- no collective on the
+    data path)."""
+    return shard_ranges(np.asarray(sizes, dtype=np.int64), world)
+
+
+def _gpu_quantize_prune(w, st, alpha, prune_cfg):
+    from .pruning import prune
+    from .scaling import quantize_scaled
+    q = quantize_scaled(w, st, alpha)
+    return prune(q, st, prune_cfg) if prune_cfg is not None and prune_cfg.sparsity > 0 else q
+
+
+def quantize_prune_shard(weights, stats, alpha: float, prune_cfg=None, rank: int = 0, world: int = 1,
+                         group=None, fn=None, gather: bool = True):
+    """This rank's share of ``quantize_scaled`` (+ ``prune``) over a model
+    (the reference's per-tensor transforms, scaling.py:107-111 and
+    pruning.py:43-64, applied to each tensor independently): rank r takes the
+    contiguous tensor range ``plan_tensor_shards(sizes, world)[r]`` on its own
+    GPU.  ``gather=True``: every rank then receives every rank's
+    QuantizedTensors in model order (one all-gather of the metadata and one
+    of the int8 payload bytes), so any rank can ``pack`` the container --
+    byte-identical to the single-process pipeline.  ``fn(w, stats, alpha,
+    prune_cfg) -> QuantizedTensor`` is injectable (CPU tests use the oracle)."""
+    import torch
+    import torch.distributed as dist
+
+    from .scaling import QuantizedTensor, ScaleVector
+    fn = fn or _gpu_quantize_prune
+    sizes = [w.values.size for w in weights]
+    t0, t1 = plan_tensor_shards(sizes, world)[rank]
+    mine = [fn(weights[i], stats[weights[i].name], alpha, prune_cfg) for i in range(t0, t1)]
+    if not gather or world == 1:
+        return mine
+    meta = [(q.name, q.qvalues.shape, q.w_scale, q.scale_vec.alpha, np.asarray(q.scale_vec.s)) for q in mine]
+    payload = np.concatenate([np.ascontiguousarray(q.qvalues).view(np.uint8).ravel() for q in mine]) if mine \
+        else np.zeros(0, np.uint8)
+    metas = [None] * world
+    dist.all_gather_object(metas, meta, group=group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    lens = [sum(int(np.prod(m[1])) for m in ms) for ms in metas]
+    buf = torch.zeros(max(lens) if lens else 0, dtype=torch.uint8, device=dev)
+    buf[:payload.size] = torch.from_numpy(payload).to(dev)
+    outs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf, group=group)
+    res = []
+    for ms, o, n in zip(metas, outs, lens):
+        flat = o[:n].cpu().numpy()
+        pos = 0
+        for name, shape, w_scale, a, s in ms:
+            k = int(np.prod(shape))
+            qv = flat[pos:pos + k].view(np.int8).reshape(shape).copy()
+            pos += k
+            res.append(QuantizedTensor(name, qv, w_scale, ScaleVector(a, s)))
+    return res

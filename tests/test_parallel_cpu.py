@@ -216,3 +216,64 @@ def test_sharded_unpack_gloo_world2(tmp_path):
         raise AssertionError("oracle accepted a corrupt stream")
     except O.OracleError as e:
         assert e.chunk == ans[-1] or f"chunk {ans[-1]}" in e.msg
+
+
+def _oracle_qp(w, st, alpha, cfg):
+    from oracle import oracle as O
+    from paper_2502_15443_b200.pruning import PruneScope
+    from paper_2502_15443_b200.scaling import QuantizedTensor, ScaleVector
+    s = O.compute_scale(np.asarray(st.channel_max), alpha)
+    q, ws = O.quantize(w.values, s)
+    if cfg is not None and cfg.sparsity > 0:
+        q = O.prune(q, np.asarray(st.channel_max), cfg.sparsity, cfg.scope is PruneScope.PER_ROW)
+    return QuantizedTensor(w.name, q, ws, ScaleVector(alpha, s))
+
+
+def _qp_model():
+    from paper_2502_15443_b200 import tensors
+    ws, st = [], {}
+    for i, (r, c) in enumerate([(64, 96), (128, 64), (40, 200), (96, 96), (17, 33)]):
+        w, s = tensors.synth_ensemble(tensors.SynthSpec(rows=r, cols=c, name=f"t{i}"), 100 + i)
+        ws.append(w)
+        st[w.name] = s
+    return ws, st
+
+
+def _qp_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_15443_b200 import sharded
+        from paper_2502_15443_b200.pruning import PruneConfig
+        ws, st = _qp_model()
+        out = sharded.quantize_prune_shard(ws, st, 0.5, PruneConfig(0.2), rank, world, fn=_oracle_qp)
+        q.put((rank, [(t.name, t.qvalues.copy(), t.w_scale, t.scale_vec.s.copy()) for t in out]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_quantize_prune_sharded_by_tensor_gloo_world2():
+    """Quantize + prune sharded by tensor over two ranks (no data-path
+    collective; one all-gather so every rank holds the whole model): every
+    rank's gathered tensors equal the single-process result, in model order."""
+    from paper_2502_15443_b200 import sharded
+    from paper_2502_15443_b200.pruning import PruneConfig
+    ws, st = _qp_model()
+    want = [_oracle_qp(w, st[w.name], 0.5, PruneConfig(0.2)) for w in ws]
+    plan = sharded.plan_tensor_shards([w.values.size for w in ws], 2)
+    assert plan[0][0] == 0 and plan[0][1] == plan[1][0] and plan[1][1] == len(ws)
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_qp_worker, args=(r, 2, port, qu)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(qu.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in (0, 1):
+        got = res[r]
+        assert [g[0] for g in got] == [t.name for t in want]
+        for (name, qv, wsc, s), t in zip(got, want):
+            assert np.array_equal(qv, t.qvalues) and wsc == t.w_scale and np.array_equal(s, t.scale_vec.s), name

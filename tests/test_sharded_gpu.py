@@ -79,3 +79,21 @@ def test_shard_world2_gpu(cuda, tmp_path):
     assert a0 == 0 and a1 == c0 and c1 == payload.size
     assert np.frombuffer(b0, np.uint8).tobytes() == payload[a0:a1].tobytes()
     assert np.frombuffer(d0, np.uint8).tobytes() == payload[c0:c1].tobytes()
+
+
+def test_quantize_prune_shard_world1_equals_api(cuda, oracle):
+    """world 1, the default GPU per-tensor function: the shard is the whole
+    model and equals quantize_scaled + prune through the API (and the oracle)."""
+    from paper_2502_15443_b200 import sharded, tensors
+    from paper_2502_15443_b200.pruning import PruneConfig
+    ws, st = [], {}
+    for i, (r, c) in enumerate([(64, 96), (128, 64), (40, 200)]):
+        w, s = tensors.synth_ensemble(tensors.SynthSpec(rows=r, cols=c, name=f"t{i}"), 300 + i)
+        ws.append(w)
+        st[w.name] = s
+    got = sharded.quantize_prune_shard(ws, st, 0.5, PruneConfig(0.2), 0, 1)
+    for g, w in zip(got, ws):
+        s = oracle.compute_scale(np.asarray(st[w.name].channel_max), 0.5)
+        q, wsc = oracle.quantize(w.values, s)
+        q = oracle.prune(q, np.asarray(st[w.name].channel_max), 0.2, False)
+        assert np.array_equal(g.qvalues, q) and g.w_scale == wsc
