@@ -222,8 +222,11 @@ __device__ __forceinline__ void fwin_advance(Chain& c, uint32_t s, const FmaK& k
         : "r"(c.rb), "r"(s), "r"(k.c1));
 }
 
+#ifndef DC_FUSED_CLAMP
+#define DC_FUSED_CLAMP 1  // never request stream bytes past the chain's end (+ the window's 8-byte look-ahead)
+#endif
 __device__ __forceinline__ void ring_refill(Chain& c, uint32_t ring_base) {
-    if (c.mode <= 1 && ring_avail(c) < 96u) {
+    if (c.mode <= 1 && ring_avail(c) < 96u && (!DC_FUSED_CLAMP || c.gfill < c.gend + 8)) {
         cp_async16(ring_base + ((uint32_t)c.gfill & 127u), reinterpret_cast<const void*>(c.gfill));
         cp_async16(ring_base + ((uint32_t)(c.gfill + 16) & 127u), reinterpret_cast<const void*>(c.gfill + 16));
         c.gfill += 32;
@@ -372,6 +375,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_fused_ring(
             if (c.mode <= 1) {  // prime the ring with 112 B: buffered bytes stay < 128, so
                                 // (gfill - read) & 127 never aliases a full ring to empty
                 for (int k = 0; k < 7; ++k) {
+                    if (DC_FUSED_CLAMP && c.gfill >= c.gend + 8) break;
                     cp_async16(ring_base[u] + ((uint32_t)c.gfill & 127u), reinterpret_cast<const void*>(c.gfill));
                     c.gfill += 16;
                 }
