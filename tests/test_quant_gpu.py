@@ -153,6 +153,26 @@ def test_prune_per_tensor_ties_match_oracle(cuda, oracle):
                 assert np.array_equal(got, oracle.prune(q, cm, sp, False)), (rows, cols, sp, cm[:3])
 
 
+def test_prune_per_row_warp_kernel_shapes_match_oracle(cuda, oracle):
+    """The warp-per-row kernel (16-aligned widths up to 4096, full and ragged
+    512-column chunks) on continuous, few-level and constant channel maxima,
+    zero columns, heavy ties and sparsities from 1/cols to 1: zero sets equal
+    the reference's stable-argsort result."""
+    rng = np.random.default_rng(88)
+    for cols in (16, 48, 512, 1040, 2064, 4096):
+        rows = 37
+        q = np.clip(np.round(rng.normal(0, 12, (rows, cols))), -127, 127).astype(np.int8)
+        q[0, :] = 5
+        q[1, :] = rng.choice([-2, 2, 9], cols)
+        q[2, : cols // 2] = 0
+        for cm in (rng.lognormal(-1, 1, cols), rng.choice([0.0, 0.25, 1.0, 4.0], cols), np.full(cols, 0.3)):
+            for sp in (1.0 / cols, 0.2, 0.5, 0.97, 1.0):
+                qt = cuda.QuantizedTensor("r", q, 0.1, cuda.ScaleVector.identity(cols))
+                st = cuda.ActivationStats("r", cm)
+                got = cuda.prune(qt, st, cuda.PruneConfig(sp, cuda.PruneScope.PER_ROW)).qvalues
+                assert np.array_equal(got, oracle.prune(q, cm, sp, True)), (cols, sp, cm[:2])
+
+
 def test_prune_properties(cuda):
     rng = np.random.default_rng(44)
     q = np.clip(np.round(rng.normal(0, 20, (256, 512))), -127, 127).astype(np.int8)
