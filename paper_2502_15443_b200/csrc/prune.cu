@@ -14,7 +14,6 @@
 // Non-negative doubles order like their u64 bit patterns, so keys are bits.
 #include <cooperative_groups.h>
 #include <cstdio>
-#include <cstdlib>
 
 #include "common.cuh"
 
@@ -1395,7 +1394,7 @@ extern "C" int dc_prune_rows(const int8_t* q, const double* cm, int64_t rows, in
     if (rows < 0 || cols < 0 || k < 0 || k > cols) return DC_ERR_ARG;
     if (rows == 0 || cols == 0) return DC_OK;
     const bool vec = (cols & 15) == 0 && ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
-    if (k > 0 && cols <= kRowMax && vec && !getenv("DC_PRUNE_ROWS_CTA")) {
+    if (k > 0 && cols <= kRowMax && vec) {
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k_prune_rowsw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RwSmem));
