@@ -263,6 +263,21 @@ __device__ __forceinline__ void win_advance_g(Win& w, uint32_t s) {
         : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
         : "r"(s), "n"(32u + (J + 1) * 0x10820u));
 }
+// Same with the word move as a predicated IMAD by an opaque 1 (FMA pipe)
+// instead of SEL (ALU pipe).
+template <int J>
+__device__ __forceinline__ void win_advance_gf(Win& w, uint32_t s, uint32_t one) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "mad.lo.u32 %3, %4, 8, %3;\n\t"
+        "setp.ge.u32 q, %3, %5;\n\t"
+        "@q mad.lo.u32 %0, %1, %6, 0;\n\t"
+        "@q ld.shared.u32 %1, [%2+4];\n\t"
+        "@q add.u32 %2, %2, 4;\n\t"
+        "@q add.u32 %3, %3, -32;\n\t}"
+        : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
+        : "r"(s), "n"(32u + (J + 1) * 0x10820u), "r"(one));
+}
 __device__ __forceinline__ void win_rebase(Win& w) { w.o -= 8u * 0x10820u; }
 
 // Same inside a 128-byte ring (fused kernel): the word address wraps.

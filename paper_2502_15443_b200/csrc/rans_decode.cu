@@ -320,8 +320,9 @@ constexpr int kOutWarpBytes = kDecIlp * 32 * kOutStride;
 // 2 CTAs/SM -- the large-chunk configuration.  Narrow: 4 warps, 256-segment
 // tasks, 45 KB staging, 3 CTAs/SM -- a 64 KiB chunk (256 segments) then
 // still gives every lane two interleaved chains instead of one.
-template <int TH, int MINB, uint32_t STAGE>
+template <int TH, int MINB, uint32_t STAGE, int DESC>
 struct DecCfg {
+    static constexpr int kDescBatch = DESC;
     static constexpr int kThreads = TH;
     static constexpr int kMinBlocks = MINB;
     static constexpr int kWarps = TH / 32;
@@ -332,11 +333,12 @@ struct DecCfg {
     static constexpr uint32_t kOffStage = ((sizeof(TableSmem) + 127) / 128) * 128;
     static constexpr uint32_t kOffOut = kOffStage + kStageCap + kStageSlack;
     static constexpr uint32_t kOffBar = kOffOut + kWarps * kOutWarpBytes;
-    static constexpr size_t kSmem = kOffBar + 16;
+    static constexpr uint32_t kOffDesc = kOffBar + 64;
+    static constexpr size_t kSmem = kOffDesc + DESC * 64;
     static_assert(kOffStage % 128 == 0 && kOffOut % 16 == 0 && kOffBar % 8 == 0, "smem carve-up alignment");
 };
-using WideCfg = DecCfg<256, 2, 72 * 1024>;
-using NarrowCfg = DecCfg<128, 3, 45 * 1024>;
+using WideCfg = DecCfg<256, 2, 72 * 1024, 32>;
+using NarrowCfg = DecCfg<128, 3, 44 * 1024, 16>;
 static_assert(WideCfg::kSmem * 2 + 2048 <= 228 * 1024 && NarrowCfg::kSmem * 3 + 3072 <= 228 * 1024,
               "CTAs per SM must fit in shared memory");
 
@@ -347,13 +349,18 @@ __device__ __forceinline__ uint32_t swz(int ls, int h) { return (uint32_t)(ls * 
 
 // One warp decodes NU segments per lane (segment r = warp*32 + lane + u*TH
 // of the task) and writes them out through its staging buffer `ob`.
+// Split points of a lane's (up to) two segments, loaded before the task's
+// stream staging completes so the load latency hides behind the bulk copy.
+struct LaneSplits {
+    uint32_t x[2], so[2], xe[2], pe[2];
+};
+
 template <int NU, int TH>
-__device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, int64_t sb, uint32_t lo,
-                                            uint32_t hi, uint32_t delta, uint32_t plen, uint64_t olen, uint32_t nseg_chunk,
-                                            const uint32_t* __restrict__ seg_state,
-                                            const uint32_t* __restrict__ seg_off, const uint32_t* tab_ptr,
-                                            const uint8_t* stage_ptr, uint8_t* ob, uint8_t* __restrict__ obase,
-                                            bool out_aligned, int32_t* st, const FmaK& fk) {
+__device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, uint32_t lo, uint32_t hi,
+                                            uint32_t delta, uint64_t olen, const LaneSplits& L,
+                                            const uint32_t* tab_ptr, const uint8_t* stage_ptr, uint8_t* ob,
+                                            uint8_t* __restrict__ obase, bool out_aligned, int32_t* st,
+                                            const FmaK& fk) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tab = smem_u32(tab_ptr), stage = smem_u32(stage_ptr);
     const uint32_t tabm = tab - (1u << 26);
@@ -366,15 +373,12 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
     for (int u = 0; u < NU; ++u) {
         const int r = warp * 32 + lane + u * TH;
         const uint32_t rel = (uint32_t)(s0 + r);
-        // the chain check's targets (the next split point), loaded now so the
-        // loads' latency hides behind the decode instead of the task tail
-        const bool inner = rel + 1 < nseg_chunk;
-        xe[u] = (r < ns && inner) ? seg_state[sb + rel + 1] : kStateLower;
-        pe[u] = (r < ns && inner) ? seg_off[sb + rel + 1] : plen;
+        xe[u] = L.xe[u];
+        pe[u] = L.pe[u];
         uint32_t p;
         if (r < ns) {
-            x[u] = seg_state[sb + rel];
-            const uint32_t so = seg_off[sb + rel];
+            x[u] = L.x[u];
+            const uint32_t so = L.so[u];
             wild = wild || so < lo || so > hi;
             p = (so < lo || so > hi) ? stage : stage + so - lo + delta;
             const uint64_t rem = olen - ((uint64_t)rel << seg_shift);
@@ -424,16 +428,18 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
                     const uint32_t t = __byte_perm(e0[u], dec_sym_fa(x[u], sel[u], wv[u], tabm, fk), 0x0040);
                     w[u][v >> 2] = (v & 2) ? __byte_perm(w[u][v >> 2], t, 0x5410) : t;
                 }
+#define WADV(J) win_advance_gf<J>(W[u], sel[u], fk.c1)
                 switch (v >> 1) {  // compile-time after unrolling
-                    case 0: for (int u = 0; u < NU; ++u) win_advance_g<0>(W[u], sel[u]); break;
-                    case 1: for (int u = 0; u < NU; ++u) win_advance_g<1>(W[u], sel[u]); break;
-                    case 2: for (int u = 0; u < NU; ++u) win_advance_g<2>(W[u], sel[u]); break;
-                    case 3: for (int u = 0; u < NU; ++u) win_advance_g<3>(W[u], sel[u]); break;
-                    case 4: for (int u = 0; u < NU; ++u) win_advance_g<4>(W[u], sel[u]); break;
-                    case 5: for (int u = 0; u < NU; ++u) win_advance_g<5>(W[u], sel[u]); break;
-                    case 6: for (int u = 0; u < NU; ++u) win_advance_g<6>(W[u], sel[u]); break;
-                    default: for (int u = 0; u < NU; ++u) win_advance_g<7>(W[u], sel[u]); break;
+                    case 0: for (int u = 0; u < NU; ++u) WADV(0); break;
+                    case 1: for (int u = 0; u < NU; ++u) WADV(1); break;
+                    case 2: for (int u = 0; u < NU; ++u) WADV(2); break;
+                    case 3: for (int u = 0; u < NU; ++u) WADV(3); break;
+                    case 4: for (int u = 0; u < NU; ++u) WADV(4); break;
+                    case 5: for (int u = 0; u < NU; ++u) WADV(5); break;
+                    case 6: for (int u = 0; u < NU; ++u) WADV(6); break;
+                    default: for (int u = 0; u < NU; ++u) WADV(7); break;
                 }
+#undef WADV
             }
 #pragma unroll
             for (int u = 0; u < NU; ++u) win_rebase(W[u]);
@@ -504,6 +510,19 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
     }
 }
 
+// Per-task header, filled for kDescBatch tasks at a time by warp 0 (one lane
+// per task, the dependent task -> chunk -> split-point loads all in flight at
+// once) so a task starts its stream copy without a global-load round trip.
+struct alignas(16) TaskDesc {
+    uint64_t blob;   // blob address (table | state | stream)
+    uint64_t obase;  // chunk output address
+    int64_t sb;      // first segment of the chunk in the index
+    uint64_t olen;   // chunk output bytes
+    uint32_t plen, lo, hi, nseg;
+    int32_t c, s0, ns, st0;
+};
+static_assert(sizeof(TaskDesc) == 64, "TaskDesc layout");
+
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segments(
     const uint8_t* __restrict__ base, const uint64_t* __restrict__ blob_off, const uint64_t* __restrict__ blob_len,
@@ -516,8 +535,9 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segme
     TableSmem& T = *reinterpret_cast<TableSmem*>(smem + Cfg::kOffTab);
     uint8_t* stage = smem + Cfg::kOffStage;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::kOffBar);
+    TaskDesc* desc = reinterpret_cast<TaskDesc*>(smem + Cfg::kOffDesc);
 
-    const int warp = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t* ob = smem + Cfg::kOffOut + warp * kOutWarpBytes;
     const uint32_t K = 1u << seg_shift;
 
@@ -527,26 +547,41 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segme
         mbar_init(bar, 1);
         fence_mbar_init();
     }
-    __syncthreads();
     int cur_chunk = -1;
     uint32_t phase = 0;
 
     for (int64_t ti = t_begin; ti < t_end; ++ti) {
-        const int4 task = tasks[ti];
-        const int c = task.x, s0 = task.y, ns = task.z;
-        {  // prologue errors (k_validate, same stream) are never decoded
-            const int32_t st0 = status[c];
-            if (st0 >= DC_CHUNK_TRUNC_TABLE && st0 <= DC_CHUNK_EMPTY_BAD) continue;
+        const int bi = (int)((ti - t_begin) % Cfg::kDescBatch);
+        if (bi == 0) {
+            __syncthreads();  // the previous batch's descriptors are no longer read
+            if (warp == 0 && lane < Cfg::kDescBatch && ti + lane < t_end) {
+                const int4 task = tasks[ti + lane];
+                TaskDesc d;
+                d.c = task.x;
+                d.s0 = task.y;
+                d.ns = task.z;
+                d.st0 = status[d.c];
+                d.blob = reinterpret_cast<uint64_t>(base + blob_off[d.c]);
+                d.obase = reinterpret_cast<uint64_t>(out + out_off[d.c]);
+                d.plen = (uint32_t)(blob_len[d.c] - kHeaderBytes);
+                d.olen = out_len[d.c];
+                d.nseg = (uint32_t)((d.olen + K - 1) >> seg_shift);
+                d.sb = seg_base[d.c];
+                d.lo = seg_off[d.sb + d.s0];
+                d.hi = ((uint32_t)(d.s0 + d.ns) < d.nseg) ? seg_off[d.sb + d.s0 + d.ns] : d.plen;
+                desc[lane] = d;
+            }
         }
-        const uint8_t* blob = base + blob_off[c];
-        const uint8_t* gstream = blob + kHeaderBytes;
-        const uint32_t plen = (uint32_t)(blob_len[c] - kHeaderBytes);
-        const uint64_t olen = out_len[c];
-        const uint32_t nseg_chunk = (uint32_t)((olen + K - 1) >> seg_shift);
-        const int64_t sb = seg_base[c];
-        const uint32_t lo = seg_off[sb + s0];
-        const uint32_t hi = ((uint32_t)(s0 + ns) < nseg_chunk) ? seg_off[sb + s0 + ns] : plen;
-        const uintptr_t gsrc = reinterpret_cast<uintptr_t>(gstream) + lo;
+        __syncthreads();  // previous task done with stage[] and T; descriptors visible
+        const TaskDesc& D = desc[bi];
+        const int c = D.c, s0 = D.s0, ns = D.ns;
+        // prologue errors (k_validate, same stream) are never decoded
+        if (D.st0 >= DC_CHUNK_TRUNC_TABLE && D.st0 <= DC_CHUNK_EMPTY_BAD) continue;
+        const uint8_t* blob = reinterpret_cast<const uint8_t*>(D.blob);
+        const uint32_t plen = D.plen, lo = D.lo, hi = D.hi, nseg_chunk = D.nseg;
+        const uint64_t olen = D.olen;
+        const int64_t sb = D.sb;
+        const uintptr_t gsrc = reinterpret_cast<uintptr_t>(blob) + kHeaderBytes + lo;
         const uintptr_t a16 = gsrc & ~(uintptr_t)15;
         const uint32_t delta = (uint32_t)(gsrc - a16);
         // a damaged index (hi < lo, or past the stream) is never staged: the
@@ -554,13 +589,25 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segme
         const uint32_t bytes = (hi >= lo && hi <= plen) ? ((hi - lo + delta + 15u) & ~15u) : 0xFFFFFFFFu;
         const bool stage_ok = bytes <= Cfg::kStageCap;
 
-        __syncthreads();  // previous task done with stage[] and T
         if (threadIdx.x == 0) {
             fence_proxy_async_smem();
             const uint32_t nbytes = stage_ok ? bytes : 0u;
             mbar_arrive_expect_tx(bar, nbytes);
             for (uint32_t off = 0; off < nbytes; off += 16384u)
                 bulk_g2s(stage + off, reinterpret_cast<const void*>(a16 + off), min(16384u, nbytes - off), bar);
+        }
+        // this lane's split points (and the chain-check targets: the next
+        // split point), in flight while the stream is staged
+        LaneSplits L;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int r = warp * 32 + lane + u * Cfg::kThreads;
+            const uint32_t rel = (uint32_t)(s0 + r);
+            const bool valid = r < ns, inner = valid && rel + 1 < nseg_chunk;
+            L.x[u] = valid ? seg_state[sb + rel] : kStateLower;
+            L.so[u] = valid ? seg_off[sb + rel] : 0u;
+            L.xe[u] = inner ? seg_state[sb + rel + 1] : kStateLower;
+            L.pe[u] = inner ? seg_off[sb + rel + 1] : plen;
         }
         if (c != cur_chunk) {
             build_decode_table(blob, T);  // overlaps the bulk copy
@@ -573,7 +620,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segme
             continue;
         }
 
-        uint8_t* obase = out + out_off[c];
+        uint8_t* obase = reinterpret_cast<uint8_t*>(D.obase);
         const bool out_aligned = ((reinterpret_cast<uintptr_t>(obase) | (uintptr_t)K) & 15) == 0;
 
         if (T.single >= 0) {  // f = 4096: output is one repeated byte
@@ -590,11 +637,11 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks) k_decode_segme
         }
         if (warp * 32 >= ns) continue;  // idle warp in a short task
         if (warp * 32 + Cfg::kThreads < ns)
-            decode_warp<2, Cfg::kThreads>(seg_shift, s0, ns, sb, lo, hi, delta, plen, olen, nseg_chunk, seg_state,
-                                          seg_off, T.tab, stage, ob, obase, out_aligned, &status[c], fk);
+            decode_warp<2, Cfg::kThreads>(seg_shift, s0, ns, lo, hi, delta, olen, L, T.tab, stage, ob, obase,
+                                          out_aligned, &status[c], fk);
         else
-            decode_warp<1, Cfg::kThreads>(seg_shift, s0, ns, sb, lo, hi, delta, plen, olen, nseg_chunk, seg_state,
-                                          seg_off, T.tab, stage, ob, obase, out_aligned, &status[c], fk);
+            decode_warp<1, Cfg::kThreads>(seg_shift, s0, ns, lo, hi, delta, olen, L, T.tab, stage, ob, obase,
+                                          out_aligned, &status[c], fk);
     }
 }
 
