@@ -297,7 +297,12 @@ def workload_config(args, raw: int, file_bytes: int, digest: str) -> dict:
                         f"{args.chunk_size >> 20} MiB chunks; one step = unpack the container (validate + rANS "
                         f"decode + CRC32 verify of every chunk)",
             "weights_shape": args.model, "chunk_size": args.chunk_size, "raw_bytes": raw, "file_bytes": file_bytes,
-            "cr": raw / file_bytes, "container_digest": digest, "seed": args.seed}
+            "cr": raw / file_bytes, "container_digest": digest, "seed": args.seed,
+            "n_chunks": -(-raw // args.chunk_size),
+            "l2": "inputs (compressed) and outputs exceed the 126 MB L2",
+            "parallelism": (f"one container chunk-sharded over {args.gpus} GPUs (contiguous chunk ranges "
+                            f"balanced by decompressed bytes, no data-path collective)" if args.gpus > 1
+                            else "single GPU")}
 
 
 class DeviceUnpack:
@@ -517,6 +522,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    args.gpus = world  # the config names the ranks actually running
     # BENCH_DIST_BACKEND=gloo + BENCH_ONE_GPU=1: every rank on cuda:0 (a
     # functional check of the N > 1 path on a one-GPU box; never a measurement)
     if os.environ.get("BENCH_ONE_GPU") == "1":
@@ -751,22 +757,21 @@ def main():
             extra = {"model": args.extra_model, "error": repr(e)[:300]}
 
     if rank == 0:
+        # `config` is exactly the reference arm's (same workload, same container
+        # bytes); what only this arm has goes to `config_detail`
         cfg = workload_config(args, raw, file_bytes, digest)
-        cfg.update({"seg_len": 1 << args.seg_shift, "n_chunks": n_chunks, "n_tasks": n_tasks,
-                    "cr_resident": raw / (file_bytes + index_bytes), "index_bytes": index_bytes,
-                    "l2": "inputs (compressed) and outputs exceed the 126 MB L2",
-                    "parallelism": (f"chunk-sharded over {world} GPUs (one container, contiguous chunk ranges "
-                                    f"balanced by decompressed bytes, no data-path collective)" if world > 1
-                                    else "single GPU"),
-                    "shard": {"chunks": [shard.c0, shard.c1], "decompressed_bytes": shard_bytes},
-                    "build_s": t_build,
-                    "reference_arm": "bench.py --impl reference builds the same container from the same spec "
-                                     "(same container_digest) and unpacks whole-layer samples of it"})
+        assert cfg["n_chunks"] == n_chunks, (cfg["n_chunks"], n_chunks)
+        detail = {"seg_len": 1 << args.seg_shift, "n_tasks": n_tasks,
+                  "cr_resident": raw / (file_bytes + index_bytes), "index_bytes": index_bytes,
+                  "shard": {"chunks": [shard.c0, shard.c1], "decompressed_bytes": shard_bytes},
+                  "build_s": t_build,
+                  "reference_arm": "bench.py --impl reference builds the same container from the same spec "
+                                   "(same container_digest) and unpacks whole-layer samples of it"}
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong",
-            "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": cfg,
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": cfg, "config_detail": detail,
             "decode_kernel_gbs": shard_bytes / (kms / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "kernel": "k_decode_segments", "achieved": achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,

@@ -198,9 +198,12 @@ class SegmentIndex:
         return ok
 
     # ---- work decomposition -------------------------------------------------
-    def tasks(self, jobs: JobTable, ok: np.ndarray, max_segs: int | None = None) -> torch.Tensor:
+    def tasks(self, jobs: JobTable, ok: np.ndarray, max_segs: int | None = None,
+              seg_range: tuple[np.ndarray, np.ndarray] | None = None) -> torch.Tensor:
         """int32 [n_tasks, 4] = (chunk, first segment, count, 0): at most
-        ``max_segs`` segments and at most the kernel's staging capacity of stream bytes each."""
+        ``max_segs`` segments and at most the kernel's staging capacity of stream bytes each.
+        ``seg_range`` = (first, end) segment per job limits each chunk to that
+        segment range (decoding part of a chunk)."""
         mode = decode_mode(jobs)
         max_segs = max_segs or nv.call({"small": "dc_decode_small_segments", "narrow": "dc_decode_narrow_segments",
                                         "wide": "dc_decode_task_segments"}[mode])
@@ -208,12 +211,19 @@ class SegmentIndex:
         K = 1 << self.seg_shift
         sel = np.nonzero((jobs.codec == 1) & ok & (jobs.out_len > 0))[0]
         nseg = (jobs.out_len[sel].astype(np.int64) + K - 1) // K
-        ntask = (nseg + max_segs - 1) // max_segs
+        if seg_range is None:
+            lo_s, hi_s = np.zeros_like(nseg), nseg
+        else:
+            lo_s = np.asarray(seg_range[0], dtype=np.int64)[sel]
+            hi_s = np.minimum(np.asarray(seg_range[1], dtype=np.int64)[sel], nseg)
+            keep = hi_s > lo_s
+            sel, nseg, lo_s, hi_s = sel[keep], nseg[keep], lo_s[keep], hi_s[keep]
+        ntask = (hi_s - lo_s + max_segs - 1) // max_segs
         chunk = np.repeat(sel, ntask)
         first_task = np.repeat(np.cumsum(ntask) - ntask, ntask)
-        s0 = (np.arange(int(ntask.sum())) - first_task) * max_segs
+        s0 = np.repeat(lo_s, ntask) + (np.arange(int(ntask.sum())) - first_task) * max_segs
         nsg = np.repeat(nseg, ntask)
-        cnt = np.minimum(max_segs, nsg - s0)
+        cnt = np.minimum(max_segs, np.repeat(hi_s, ntask) - s0)
         # stream byte span per task: split the (rare) ones that overflow staging
         off = self.host_offsets()
         base = self.seg_base[chunk]

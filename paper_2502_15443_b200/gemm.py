@@ -93,18 +93,25 @@ class _LayerSet:
     """Per-layer activations and int32 accumulators shared by the grouped
     INT8 GEMM and the fused decode GEMM (one launch covers every layer)."""
 
-    def __init__(self, shapes, t_offs, xs, ntok: int):
+    def __init__(self, shapes, t_offs, xs, ntok: int, accs=None):
+        """``accs``: optional caller-owned int32 [ntok, rows] accumulators
+        (contiguous; the caller zeroes them) instead of one owned buffer."""
         assert _GT_DTYPE.itemsize == nv.call("dc_gemm_tensor_bytes")
         self.shapes = [(int(r), int(k)) for r, k in shapes]
         self.ntok = ntok
         self.xs = [x.contiguous() for x in xs]
         dev = self.xs[0].device
         sizes = [ntok * r for r, _ in self.shapes]
-        self.acc_flat = torch.zeros(sum(sizes), dtype=torch.int32, device=dev)
-        self.accs, pos = [], 0
-        for (r, _), n in zip(self.shapes, sizes):
-            self.accs.append(self.acc_flat[pos:pos + n].view(ntok, r))
-            pos += n
+        if accs is not None:
+            assert all(a.is_contiguous() and a.dtype == torch.int32 and tuple(a.shape) == (ntok, r)
+                       for a, (r, _) in zip(accs, self.shapes))
+            self.acc_flat, self.accs = None, list(accs)
+        else:
+            self.acc_flat = torch.zeros(sum(sizes), dtype=torch.int32, device=dev)
+            self.accs, pos = [], 0
+            for (r, _), n in zip(self.shapes, sizes):
+                self.accs.append(self.acc_flat[pos:pos + n].view(ntok, r))
+                pos += n
         gt = np.zeros(len(self.shapes), dtype=_GT_DTYPE)
         gt["x"] = [x.data_ptr() for x in self.xs]
         gt["acc"] = [a.data_ptr() for a in self.accs]
@@ -126,10 +133,10 @@ class _LayerSet:
 class GroupedInt8:
     """All linears of a model, uncompressed INT8 weights, one tcgen05 launch."""
 
-    def __init__(self, weights: list[torch.Tensor], xs: list[torch.Tensor], ntok: int):
+    def __init__(self, weights: list[torch.Tensor], xs: list[torch.Tensor], ntok: int, accs=None):
         if ntok > 16:
             raise ValueError("grouped GEMM handles <= 16 tokens per launch")
-        self.layers = _LayerSet([w.shape for w in weights], [0] * len(weights), xs, ntok)
+        self.layers = _LayerSet([w.shape for w in weights], [0] * len(weights), xs, ntok, accs)
         self.weights = [w.contiguous() for w in weights]
         n = len(weights)
         mb = nv.call("dc_tmap_bytes")
@@ -158,7 +165,8 @@ class GroupedInt8:
     def run(self, max_ctas: int | None = None) -> None:
         """One launch over every layer.  ``max_ctas`` selects the persistent
         kernel (one CTA per SM, grid capped at max_ctas; 0 = every SM)."""
-        self.layers.acc_flat.zero_()
+        if self.layers.acc_flat is not None:
+            self.layers.acc_flat.zero_()
         if max_ctas is None:
             nv.call("dc_w8a8_grouped", self.maps.data_ptr(), self.layers.tens.data_ptr(), self.unit_t.data_ptr(),
                     self.unit_t.shape[0], self.layers.ntok, nv.stream_ptr())
@@ -170,11 +178,13 @@ class GroupedInt8:
 class _StreamedDecodeGemm:
     """Layers whose 1024-row items the fused ring cannot serve (an item's rows
     spanning more than two chunks -- small chunks -- or a chunk size / layer
-    offset / K that is not a multiple of 256): per group of consecutive
-    layers, the split-point decoder writes the group's chunk range into an
-    L2-sized scratch slot and the grouped tcgen05 INT8 GEMM reads it back
-    while it is still L2-resident; the slots alternate so group g + 1 decodes
-    on a second stream while group g multiplies."""
+    offset / K that is not a multiple of 256): per group of layers, the
+    split-point decoder writes ONLY those layers' segments (chunk x segment
+    range tasks, so the native layers between them are not decoded twice)
+    into an L2-sized scratch slot, and the grouped tcgen05 INT8 GEMM reads
+    them back while still L2-resident, accumulating straight into the
+    caller's int32 outputs; the slots alternate so group g + 1 decodes on a
+    second stream while group g multiplies."""
 
     SLOT_BYTES = 48 << 20
 
@@ -183,72 +193,117 @@ class _StreamedDecodeGemm:
         from . import engine
         dev = image.device
         self.image, self.jobs, self.index = image, jobs, index
+        K = 1 << index.seg_shift
         out_off = jobs.out_off.astype(np.int64)
-        out_end = out_off + jobs.out_len.astype(np.int64)
-        groups, cur, span0 = [], [], None
+        out_len = jobs.out_len.astype(np.int64)
+        out_end = out_off + out_len
+        self.stored = []  # (slot index, slot byte offset, image byte offset, n) of stored-chunk pieces
+
+        def pieces(t, n):
+            """(chunk, first seg, end seg, payload start of first seg, payload end) per chunk of [t, t+n)."""
+            c0 = int(np.searchsorted(out_end, t, side="right"))
+            c1 = int(np.searchsorted(out_off, t + n, side="left"))
+            out = []
+            for c in range(c0, c1):
+                lo, hi = max(t, int(out_off[c])), min(t + n, int(out_end[c]))
+                s_lo, s_hi = (lo - int(out_off[c])) // K, -(-(hi - int(out_off[c])) // K)
+                a = int(out_off[c]) + s_lo * K
+                b = min(int(out_off[c]) + s_hi * K, int(out_end[c]))
+                out.append((c, s_lo, s_hi, a, b, lo, hi))
+            return out
+
+        # slot layout per group: each layer's decoded segment span [a, b) at slot
+        # position p, chosen so the layer's first weight byte is 16-B aligned
+        groups, cur, pos = [], [], 0
         for lay in layers:
             r, k, t, _, _ = lay
-            if cur and (t + r * k - span0 > self.SLOT_BYTES):
+            pcs = pieces(t, r * k)
+            a0, b1 = pcs[0][3], pcs[-1][4]
+            need = (b1 - a0) + 32
+            if cur and pos + need > self.SLOT_BYTES:
                 groups.append(cur)
-                cur = []
-            if not cur:
-                span0 = t
-            cur.append(lay)
+                cur, pos = [], 0
+            p = pos + ((a0 - t) - pos) % 16  # (p + t - a0) % 16 == 0
+            cur.append((lay, pcs, p, a0))
+            pos = p + (b1 - a0) + 16
         if cur:
             groups.append(cur)
         self.groups = []
-        slot = 0
-        for g in groups:
-            lo, hi = g[0][2], g[-1][2] + g[-1][0] * g[-1][1]
-            c0 = int(np.searchsorted(out_end, lo, side="right"))
-            c1 = int(np.searchsorted(out_off, hi, side="left"))
-            base_out = int(out_off[c0])
-            sl = slice(c0, c1)
-            lj = engine.JobTable.build(jobs.blob_off[sl], jobs.blob_len[sl], jobs.out_off[sl] - np.uint64(base_out),
-                                       jobs.out_len[sl], jobs.codec[sl], dev)
-            li = engine.SegmentIndex(index.seg_shift, index.seg_base[sl], index.n_segs,
-                                     index.d_seg_base[c0:c1].contiguous(), index.d_state, index.d_off,
-                                     h_off=index.host_offsets())
-            tasks = li.tasks(lj, np.ones(lj.n, bool))
-            span = int(out_end[c1 - 1]) - base_out
-            slot = max(slot, span + 16)
-            # decoded bytes land at slot + pad so that every layer view keeps its
-            # payload offset's 16-byte alignment (TMA maps of the INT8 GEMM)
-            pad = base_out % 16
-            self.groups.append((lj, li, tasks, base_out - pad, g, span, c0, pad))
-        self.slots = [nv.device_bytes(slot, dev) for _ in range(min(2, len(self.groups)))]
+        slot_bytes = 0
+        for gi, g in enumerate(groups):
+            jc, jo, s_lo, s_hi = [], [], [], []
+            for lay, pcs, p, a0 in g:
+                for c, sl, sh, a, b, lo, hi in pcs:
+                    if jobs.codec[c] == 0:  # stored chunk: plain copy of the layer's bytes
+                        self.stored.append((gi, p + lo - a0, int(jobs.blob_off[c]) + lo - int(out_off[c]), hi - lo))
+                        continue
+                    jc.append(c)
+                    jo.append(p + int(out_off[c]) - a0)  # may be negative: the kernel adds it mod 2^64
+                    s_lo.append(sl)
+                    s_hi.append(sh)
+            jc = np.asarray(jc, dtype=np.int64)
+            end = max(p + (pcs[-1][4] - a0) for _, pcs, p, a0 in g) + 16
+            slot_bytes = max(slot_bytes, end)
+            if len(jc):
+                lj = engine.JobTable.build(jobs.blob_off[jc], jobs.blob_len[jc],
+                                           np.asarray(jo, dtype=np.int64).view(np.uint64), jobs.out_len[jc],
+                                           jobs.codec[jc], dev)
+                li = engine.SegmentIndex(index.seg_shift, index.seg_base[jc], index.n_segs,
+                                         index.d_seg_base[torch.from_numpy(jc).to(dev)].contiguous(),
+                                         index.d_state, index.d_off, h_off=index.host_offsets())
+                tasks = li.tasks(lj, np.ones(lj.n, bool), seg_range=(np.asarray(s_lo), np.asarray(s_hi)))
+            else:
+                lj = li = tasks = None
+            self.groups.append((lj, li, tasks, jc, g))
+        self.slots = [nv.device_bytes(slot_bytes, dev) for _ in range(min(2, len(self.groups)))]
+        # one status word per (group, job): chunk ids kept for check()
+        n_jobs = [len(jc) for _, _, _, jc, _ in self.groups]
+        self.status = torch.zeros(max(sum(n_jobs), 1), dtype=torch.int32, device=dev)
+        self.status_chunks = np.concatenate([jc for _, _, _, jc, _ in self.groups]) if sum(n_jobs) else \
+            np.zeros(0, np.int64)
+        self.status_off = np.concatenate([[0], np.cumsum(n_jobs)[:-1]]).astype(np.int64)
         self.gemms = []
-        for gi, (lj, li, tasks, base_out, g, span, c0, pad) in enumerate(self.groups):
+        for gi, (lj, li, tasks, jc, g) in enumerate(self.groups):
             buf = self.slots[gi % len(self.slots)]
-            views = [buf[t - base_out:t - base_out + r * k].view(torch.int8).view(r, k) for r, k, t, _, _ in g]
-            self.gemms.append(GroupedInt8(views, [x for _, _, _, x, _ in g], ntok))
+            views = [buf[p + t - a0:p + t - a0 + r * k].view(torch.int8).view(r, k) for (r, k, t, _, _), _, p, a0
+                     in g]
+            self.gemms.append(GroupedInt8(views, [lay[3] for lay, _, _, _ in g], ntok,
+                                          accs=[lay[4] for lay, _, _, _ in g]))
         self.side = torch.cuda.Stream(dev)
         self.ev_free = [torch.cuda.Event() for _ in self.slots]
 
-    def run(self, status: torch.Tensor) -> None:
+    def chunk_status(self, n_chunks: int) -> np.ndarray:
+        """Per-chunk OR of this path's decode statuses."""
+        out = np.zeros(n_chunks, dtype=np.int32)
+        if len(self.status_chunks):
+            st = self.status[: len(self.status_chunks)].cpu().numpy()
+            np.maximum.at(out, self.status_chunks, np.abs(st))
+        return out
+
+    def run(self) -> None:
         from . import engine
         main = torch.cuda.current_stream()
+        self.status.zero_()
         self.side.wait_stream(main)
         n = len(self.slots)
-        for gi, ((lj, li, tasks, base_out, g, span, c0, pad), gemm) in enumerate(zip(self.groups, self.gemms)):
+        for gi, ((lj, li, tasks, jc, g), gemm) in enumerate(zip(self.groups, self.gemms)):
             slot = self.slots[gi % n]
             with torch.cuda.stream(self.side):  # decode group gi while group gi - 1 multiplies
                 if gi >= n:
                     self.side.wait_event(self.ev_free[gi % n])
-                out = slot[pad:]
-                if tasks.shape[0]:
+                if tasks is not None and tasks.shape[0]:
                     nv.call(engine.segment_kernel(lj), self.image.data_ptr(), lj.d_blob_off.data_ptr(),
                             lj.d_blob_len.data_ptr(), lj.d_out_off.data_ptr(), lj.d_out_len.data_ptr(),
                             li.seg_shift, li.d_seg_base.data_ptr(), li.d_state.data_ptr(), li.d_off.data_ptr(),
-                            tasks.data_ptr(), tasks.shape[0], out.data_ptr(), status.data_ptr() + 4 * c0,
-                            self.side.cuda_stream)
-                engine.store_copy(self.image, lj, out)
+                            tasks.data_ptr(), tasks.shape[0], slot.data_ptr(),
+                            self.status.data_ptr() + 4 * int(self.status_off[gi]), self.side.cuda_stream)
+                for sgi, so, io, nb in self.stored:
+                    if sgi == gi:
+                        slot[so:so + nb].copy_(self.image[io:io + nb])
                 ev = torch.cuda.Event()
                 ev.record(self.side)
             main.wait_event(ev)
             gemm.run()
-            for (_, _, _, _, acc), a in zip(g, gemm.accs):
-                acc.copy_(a)
             self.ev_free[gi % n].record(main)
 
 
@@ -364,7 +419,10 @@ class FusedRing:
 
     def check(self) -> np.ndarray:
         """Per-chunk status after run(); nonzero = chain broken / corrupt."""
-        return self.status[: self.jobs.n].cpu().numpy()
+        st = self.status[: self.jobs.n].cpu().numpy()
+        if self._fb is not None:
+            st = np.where(st != 0, st, self._fb.chunk_status(self.jobs.n))
+        return st
 
     def _fallback_epilogue(self) -> None:
         for li in self._fb_layers:
@@ -388,7 +446,7 @@ class FusedRing:
                     self.unit_t.shape[0], self.layers.ntok, self.status.data_ptr(),
                     self.epi.data_ptr() if self.epi is not None else None, int(max_ctas), nv.stream_ptr())
         if self._fb is not None:
-            self._fb.run(self.status)
+            self._fb.run()
             if self.ys is not None:
                 self._fallback_epilogue()
 
