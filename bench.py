@@ -766,7 +766,12 @@ def main():
                   "shard": {"chunks": [shard.c0, shard.c1], "decompressed_bytes": shard_bytes},
                   "build_s": t_build,
                   "reference_arm": "bench.py --impl reference builds the same container from the same spec "
-                                   "(same container_digest) and unpacks whole-layer samples of it"}
+                                   "(same container_digest) and unpacks whole-layer samples of it",
+                  "parity": "the decoded output is checked equal to the encoder's input payload after the "
+                            "warm-up, and every timed step checks every chunk's CRC32 against the container "
+                            "table (verdicts re-checked after the timed region); the workload's container bytes equal "
+                            "the oracle-packed container's (tests/test_bench_synth_gpu.py), whose codec is "
+                            "pinned to the reference's golden vectors (tests/test_oracle_golden.py)"}
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
