@@ -1,5 +1,7 @@
-"""Chunk-sharded unpack of ONE DCC1 container across GPUs (config C3 at
-1/2/4/8 GPUs).
+"""Chunk-sharded unpack (and pack) of ONE DCC1 container across GPUs
+(config C3 at 1/2/4/8 GPUs).  ``pack_shard`` is the encode
+side: each rank encodes its contiguous chunk range, rank 0 assembles the
+byte-identical file.
 
 DCC1 chunks are independent streams (reference container.py:20-21; the
 reference fans them out to worker threads, container.py:316-325), so the
@@ -282,3 +284,127 @@ def quantize_prune_shard(weights, stats, alpha: float, prune_cfg=None, rank: int
             pos += k
             res.append(QuantizedTensor(name, qv, w_scale, ScaleVector(a, s)))
     return res
+
+
+# ------------------------------------------------------------ pack by chunk
+def _payload_range(tensors, a: int, b: int) -> np.ndarray:
+    """Bytes [a, b) of the concatenated int8 payload (only the tensors that
+    overlap the range are touched)."""
+    out = np.empty(b - a, np.uint8)
+    pos = 0
+    for t in tensors:
+        n = t.qvalues.size
+        lo, hi = max(a, pos), min(b, pos + n)
+        if lo < hi:
+            flat = np.ascontiguousarray(t.qvalues).reshape(-1).view(np.uint8)
+            out[lo - a:hi - a] = flat[lo - pos:hi - pos]
+        pos += n
+        if pos >= b:
+            break
+    return out
+
+
+def gpu_encode(raw: np.ndarray, chunk_size: int, mask: np.ndarray, device=None):
+    """Default encoder: this rank's payload range -> its GPU, histogram /
+    normalize / rANS encode of its chunks (codec chosen as container.pack
+    does), blobs assembled back to back on the device.  Returns (codec u8,
+    comp_len u64, crc u32, blob bytes as a device uint8 tensor)."""
+    import torch
+
+    from . import engine
+    from . import native as nv
+    dev = device or nv.require_cuda()
+    payload = nv.to_device_bytes(raw, dev)[: raw.size]
+    enc = engine.encode_payload(payload, chunk_size, mask, None)
+    offs = np.zeros(enc.n, dtype=np.uint64)
+    if enc.n:
+        offs[1:] = np.cumsum(enc.comp_len)[:-1]
+    blobs = nv.device_bytes(int(enc.comp_len.sum()), dev)
+    engine.assemble(payload, enc, offs, blobs)
+    torch.cuda.current_stream(dev).synchronize()
+    return enc.codec.copy(), enc.comp_len.copy(), enc.crc.copy(), blobs
+
+
+def pack_shard(tensors, stats, chunk_size: int = container.DEFAULT_CHUNK_SIZE, plan=None, rank: int = 0,
+               world: int = 1, group=None, device=None, encode=None, dst: int = 0):
+    """``container.pack`` with the chunks sharded over ``world`` ranks (the
+    reference fans the same independent chunk encodes out to threads,
+    container.py:152-158): rank r encodes the contiguous chunk range
+    ``shard_ranges(chunk sizes, world)[r]`` of the payload on its own GPU;
+    rank ``dst`` gathers every rank's per-chunk (codec, length, CRC) and blob
+    bytes (point-to-point: over NCCL the blobs go GPU to GPU) and returns the
+    DCC1 bytes -- identical to single-process ``pack`` -- while the other
+    ranks return None.  ``encode(raw, chunk_size, mask) -> (codec, comp_len,
+    crc, blobs)`` is injectable (CPU tests use the oracle)."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+    if chunk_size < container.MIN_CHUNK_SIZE:
+        raise container.DcompError(f"chunk_size must be >= {container.MIN_CHUNK_SIZE}, got {chunk_size}")
+    names = [t.name for t in tensors]
+    if len(set(names)) != len(names):
+        raise container.DcompError("duplicate tensor names")
+    header = container._header(tensors, container._stats_map(stats), chunk_size)
+    total = sum(t.qvalues.size for t in tensors)
+    n = math.ceil(total / chunk_size) if total else 0
+    mask = container._mask_of(plan, n)
+    prefix = container.MAGIC + struct.pack("<HI", container.VERSION, len(header)) + header + struct.pack("<I", n)
+    if n == 0:
+        return prefix if rank == dst else None
+    ulen = np.minimum(chunk_size, total - np.arange(n, dtype=np.int64) * chunk_size)
+    ranges = shard_ranges(ulen, world)
+    c0, c1 = ranges[rank]
+    encode = encode or (lambda raw, cs, m: gpu_encode(raw, cs, m, device))
+    if c1 > c0:
+        raw = _payload_range(tensors, c0 * chunk_size, min(c1 * chunk_size, total))
+        codec, clen, crc, blobs = encode(raw, chunk_size, mask[c0:c1])
+    else:
+        codec, clen, crc, blobs = (np.zeros(0, np.uint8), np.zeros(0, np.uint64), np.zeros(0, np.uint32),
+                                   np.zeros(0, np.uint8))
+    if world == 1:
+        metas = [(codec, clen, crc)]
+    else:
+        metas = [None] * world
+        dist.all_gather_object(metas, (np.asarray(codec), np.asarray(clen), np.asarray(crc)), group=group)
+    codec_all = np.concatenate([m[0] for m in metas]).astype(np.uint8)
+    clen_all = np.concatenate([m[1] for m in metas]).astype(np.uint64)
+    crc_all = np.concatenate([m[2] for m in metas]).astype(np.uint32)
+    sizes = [int(np.asarray(m[1], np.uint64).sum()) for m in metas]
+    nccl = world > 1 and dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+
+    def as_tensor(b):
+        t = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(b, np.uint8))
+        return t.to(dev)
+
+    if rank != dst:
+        if sizes[rank]:
+            dist.send(as_tensor(blobs)[: sizes[rank]].contiguous(), dst, group=group)
+        return None
+    # dst: this rank's blobs and every other rank's, in chunk order
+    body = torch.empty(sum(sizes), dtype=torch.uint8, device=dev)
+    pos = 0
+    for r in range(world):
+        if sizes[r]:
+            if r == rank:
+                body[pos:pos + sizes[r]].copy_(as_tensor(blobs)[: sizes[r]])
+            else:
+                recv = body[pos:pos + sizes[r]]
+                dist.recv(recv, r, group=group)
+        pos += sizes[r]
+    first = len(prefix) + n * container._ENTRY.size
+    offs = np.zeros(n, dtype=np.uint64)
+    offs[1:] = np.cumsum(clen_all)[:-1]
+    entries = np.zeros(n, dtype=container.ENTRY_DTYPE)
+    entries["codec"] = codec_all
+    entries["file_offset"] = offs + np.uint64(first)
+    entries["comp_len"] = clen_all
+    entries["uncomp_len"] = ulen.astype(np.uint64)
+    entries["crc32"] = crc_all
+    out = bytearray(first + sum(sizes))
+    out[:len(prefix)] = prefix
+    out[len(prefix):first] = entries.tobytes()
+    if sizes and sum(sizes):
+        out[first:] = body.cpu().numpy().tobytes() if body.is_cuda else body.numpy().tobytes()
+    return bytes(out)

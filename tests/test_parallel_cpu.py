@@ -277,3 +277,73 @@ def test_quantize_prune_sharded_by_tensor_gloo_world2():
         assert [g[0] for g in got] == [t.name for t in want]
         for (name, qv, wsc, s), t in zip(got, want):
             assert np.array_equal(qv, t.qvalues) and wsc == t.w_scale and np.array_equal(s, t.scale_vec.s), name
+
+
+def _oracle_encode(raw, cs, mask):
+    """The reference's per-chunk codec choice (container.py:160-171) with the
+    oracle's encoder, in pack_shard's encode() shape."""
+    from oracle import oracle as O
+    codec, clen, crc, parts = [], [], [], []
+    for i in range(-(-raw.size // cs)):
+        ch = raw[i * cs:(i + 1) * cs]
+        blob = O.compress_blob(ch) if mask[i] else None
+        data = blob if blob is not None and len(blob) < ch.size else ch.tobytes()
+        codec.append(1 if data is blob else 0)
+        clen.append(len(data))
+        crc.append(O.crc32(ch))
+        parts.append(data)
+    return (np.array(codec, np.uint8), np.array(clen, np.uint64), np.array(crc, np.uint32),
+            np.frombuffer(b"".join(parts), np.uint8))
+
+
+def _pack_model():
+    from paper_2502_15443_b200.scaling import QuantizedTensor, ScaleVector
+    from paper_2502_15443_b200.tensors import ActivationStats
+    rng = np.random.default_rng(3)
+    ts, st, ents = [], {}, []
+    for i, (r, c) in enumerate([(300, 700), (128, 1024), (77, 513), (256, 600)]):
+        q = np.clip(np.round(rng.normal(0, 9, (r, c))), -127, 127).astype(np.int8)
+        s = rng.uniform(0.5, 2.0, c)
+        cm = rng.uniform(0.1, 3.0, c).astype(np.float32)
+        ts.append(QuantizedTensor(f"w{i}", q, 0.01 * (i + 1), ScaleVector(0.5, s)))
+        st[f"w{i}"] = ActivationStats(f"w{i}", cm)
+        ents.append((f"w{i}", q, 0.01 * (i + 1), 0.5, s, cm))
+    return ts, st, ents
+
+
+def _pack_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_15443_b200 import sharded
+        ts, st, _ = _pack_model()
+        n = -(-sum(t.qvalues.size for t in ts) // 16384)
+        mask = np.array([i % 5 != 3 for i in range(n)])  # some chunks stored by plan
+        out = sharded.pack_shard(ts, st, 16384, mask, rank, world, encode=_oracle_encode)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_pack_sharded_by_chunk_gloo_world2():
+    """container.pack with the chunks encoded on two ranks (each only its
+    contiguous chunk range), blobs sent to rank 0: byte-identical to the
+    single-process pack of the same tensors (the oracle's, which equals the
+    reference's); rank 1 returns None."""
+    from oracle import oracle as O
+    _, _, ents = _pack_model()
+    n = -(-sum(e[1].size for e in ents) // 16384)
+    mask = np.array([i % 5 != 3 for i in range(n)])
+    want = O.pack(ents, 16384, mask=mask)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pack_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[1] is None
+    assert res[0] == want

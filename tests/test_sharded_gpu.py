@@ -97,3 +97,56 @@ def test_quantize_prune_shard_world1_equals_api(cuda, oracle):
         q, wsc = oracle.quantize(w.values, s)
         q = oracle.prune(q, np.asarray(st[w.name].channel_max), 0.2, False)
         assert np.array_equal(g.qvalues, q) and g.w_scale == wsc
+
+
+def _pack_model(dc):
+    rng = np.random.default_rng(5)
+    ts, st = [], {}
+    for i, (r, c) in enumerate([(512, 1024), (300, 2048), (1000, 640), (7, 9)]):
+        q = np.clip(np.round(rng.normal(0, 9, (r, c))), -127, 127).astype(np.int8)
+        if i == 1:
+            q[:100] = rng.integers(-127, 128, (100, c))  # a chunk that does not compress: stored
+        ts.append(dc.QuantizedTensor(f"w{i}", q, 0.01, dc.ScaleVector.identity(c)))
+        st[f"w{i}"] = dc.ActivationStats(f"w{i}", np.ones(c))
+    return ts, st
+
+
+def test_pack_shard_world1_equals_pack(cuda):
+    from paper_2502_15443_b200 import container, sharded
+    ts, st = _pack_model(cuda)
+    for cs in (1 << 16, 1 << 18):
+        assert sharded.pack_shard(ts, st, cs) == container.pack(ts, st, cs)
+
+
+def _pack_worker(rank, world, port, q, cs):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2502_15443_b200 as dc
+        from paper_2502_15443_b200 import sharded
+        ts, st = _pack_model(dc)
+        q.put((rank, sharded.pack_shard(ts, st, cs, None, rank, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_pack_shard_world2_gpu(cuda):
+    """Two ranks (gloo; both on cuda:0 here) encode disjoint chunk ranges on
+    the GPU; rank 0's assembled file equals single-process container.pack."""
+    from paper_2502_15443_b200 import container
+    ts, st = _pack_model(cuda)
+    cs = 1 << 16
+    want = container.pack(ts, st, cs)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_pack_worker, args=(r, 2, port, q, cs)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert res[1] is None
+    assert res[0] == want
