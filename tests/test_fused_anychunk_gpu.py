@@ -80,3 +80,33 @@ def test_compressed_linears_from_fp_activations(cuda, oracle):
             acc = qx.astype(np.int64) @ qws[i].astype(np.int64).T
             y = acc.astype(np.float64) * np.float64(np.float32(sx * sws[i]))
             assert np.allclose(ys[i].cpu().numpy(), y, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("chunk", [64 << 10, 4 << 20, 50_000])
+def test_fused_fallback_with_stored_chunks(cuda, chunk):
+    """Streamed-fallback layers (decoded by segment range into L2 slots) mixed
+    with native layers, stored chunks (plan-masked and incompressible ones)
+    inside both: exact int32 outputs."""
+    from paper_2502_15443_b200 import container
+    from paper_2502_15443_b200.gemm import FusedRing
+    shapes = [(2560, 2560), (2560, 10240), (1024, 2560), (2560, 10240)]
+    ws = _layer(7, shapes)
+    g = torch.Generator().manual_seed(8)
+    ws[2] = torch.randint(-127, 128, (1024, 2560), generator=g, dtype=torch.int8)  # incompressible: stored
+    xs = [torch.randint(-127, 128, (2, k), generator=g, dtype=torch.int8) for _, k in shapes]
+    want = [(x.long() @ w.long().T) for w, x in zip(ws, xs)]
+    payload = torch.cat([w.reshape(-1).view(torch.uint8) for w in ws]).cuda()
+    t_offs = np.concatenate([[0], np.cumsum([w.numel() for w in ws])[:-1]])
+    n = -(-payload.numel() // chunk)
+    mask = np.array([i % 3 != 1 for i in range(n)])
+    image, enc, entries = container.pack_device(payload, b"\x00" * 8, chunk, mask, seg_shift=8)
+    assert (entries["codec"] == 0).sum() >= (~mask).sum()  # plan-stored (plus incompressible ones)
+    jobs = container.jobs_for(entries, image.device)
+    fr = FusedRing(image, jobs, enc.index, chunk, shapes, t_offs, [x.cuda() for x in xs], 2)
+    assert fr._fb is not None
+    for _ in range(2):
+        fr.run()
+        torch.cuda.synchronize()
+        assert (fr.check() == 0).all()
+        for w, a in zip(want, fr.accs):
+            assert torch.equal(a.cpu().long(), w)
