@@ -307,6 +307,22 @@ class _StreamedDecodeGemm:
             self.ev_free[gi % n].record(main)
 
 
+def _row_slices(li: int, r: int, k: int, t: int, chunk_size: int, rows_per: int) -> list:
+    """Items (layer, m0, 0, k): each row block's whole rows as one K-slice.
+    A chain must never cross a chunk boundary inside its slice, so a row block
+    where some row straddles one is cut there (a multiple of 256 from the row
+    start: the layer offset, K and the chunk size are)."""
+    out = []
+    for m0 in range(0, r, rows_per):
+        rows = np.arange(m0, min(m0 + rows_per, r), dtype=np.int64)
+        st = t + rows * k
+        ca, cb = st // chunk_size, (st + k - 1) // chunk_size
+        bad = np.nonzero(ca != cb)[0]
+        edges = [0] + sorted({int(cb[i] * chunk_size - st[i]) for i in bad}) + [k]
+        out += [(li, m0, a, b - a) for a, b in zip(edges, edges[1:])]
+    return out
+
+
 class FusedRing:
     """Fused decode -> TMEM ring -> tcgen05 W8A8 (csrc/fused_ring.cu): one
     persistent 16-warp CTA per SM, 1024 decode chains feeding the tensor core
@@ -368,7 +384,12 @@ class FusedRing:
             ks = kmax
             while ks > 256 and (k % ks or t % ks or chunk_size % ks):
                 ks //= 2
-            mine = [(li, m0, k0, min(ks, k - k0)) for m0 in range(0, r, rows_per) for k0 in range(0, k, ks)]
+            if native and not epilogue and ks < k <= kmax:
+                # a whole row fits one slice (e.g. a TP shard's K = 768 or 1792):
+                # one K-slice per row block instead of K/ks small ones
+                mine = _row_slices(li, r, k, t, chunk_size, rows_per)
+            else:
+                mine = [(li, m0, k0, min(ks, k - k0)) for m0 in range(0, r, rows_per) for k0 in range(0, k, ks)]
             if native and mine:  # every item's rows must touch at most two chunks (two table slots)
                 it = np.asarray(mine, dtype=np.int64)
                 first = t + it[:, 1] * k + it[:, 2]

@@ -23,7 +23,7 @@ import torch
 from .tensors import MODEL_SHAPES, model_layout
 
 ROW_PARALLEL = ("out_proj", "fc2", "o_proj", "down_proj")
-K_ALIGN = 512
+K_ALIGN = 256
 
 
 def shard_ranges(weights, world: int) -> list[tuple[int, int]]:

@@ -110,3 +110,31 @@ def test_fused_fallback_with_stored_chunks(cuda, chunk):
         assert (fr.check() == 0).all()
         for w, a in zip(want, fr.accs):
             assert torch.equal(a.cpu().long(), w)
+
+
+def test_fused_whole_row_slices_cut_at_chunk_edges(cuda):
+    """K that no power-of-two slice divides well (TP shards: 768, 1792): one
+    K-slice per row block, cut where a row crosses a chunk boundary; exact."""
+    from paper_2502_15443_b200 import container
+    from paper_2502_15443_b200.gemm import FusedRing
+    shapes = [(1500, 768), (2100, 1792), (640, 5120), (12000, 1280)]  # row 6707 of the last crosses 16 MiB
+    ws = _layer(11, shapes)
+    g = torch.Generator().manual_seed(12)
+    xs = [torch.randint(-127, 128, (4, k), generator=g, dtype=torch.int8) for _, k in shapes]
+    want = [(x.long() @ w.long().T) for w, x in zip(ws, xs)]
+    payload = torch.cat([w.reshape(-1).view(torch.uint8) for w in ws]).cuda()
+    t_offs = np.concatenate([[0], np.cumsum([w.numel() for w in ws])[:-1]])
+    chunk = 16 << 20
+    image, enc, entries = container.pack_device(payload, b"\x00" * 8, chunk, None, seg_shift=8)
+    jobs = container.jobs_for(entries, image.device)
+    fr = FusedRing(image, jobs, enc.index, chunk, shapes, t_offs, [x.cuda() for x in xs], 4)
+    assert fr._fb is None
+    klens = set(fr.unit_t[:, 3].tolist())
+    assert 768 in klens and 1792 in klens and 1280 in klens  # whole rows
+    assert any(kl % 256 == 0 and kl not in (768, 1792, 1280, 1024, 2048) for kl in klens)  # a cut slice
+    for _ in range(2):
+        fr.run()
+        torch.cuda.synchronize()
+        assert (fr.check() == 0).all()
+        for w, a in zip(want, fr.accs):
+            assert torch.equal(a.cpu().long(), w)
