@@ -137,3 +137,37 @@ def test_entropy_window_and_distributions(cuda, oracle):
         assert 0.99 * ideal - 16 <= len(blob) <= 1.03 * ideal + 400, name
         assert blob == oracle.compress_blob(data), name
         assert cuda.decompress_blob(blob, n) == data.tobytes(), name
+
+
+@pytest.mark.parametrize("chunk", [16 << 10, 64 << 10, 1 << 20])
+def test_segment_range_tasks_decode_exactly_those_segments(cuda, chunk):
+    """SegmentIndex.tasks(seg_range=...) (the fused fallback's partial-chunk
+    decode): every chunk's [first, end) segment range, including ranges that
+    start and end mid-chunk, is decoded exactly and nothing outside it is
+    written -- for the small, narrow and wide decoders."""
+    import torch
+
+    from paper_2502_15443_b200 import container, engine
+    rng = np.random.default_rng(chunk)
+    n_bytes = 5 * chunk + 4321
+    payload = torch.from_numpy(np.clip(np.round(rng.normal(0, 6, n_bytes)), -127, 127).astype(np.int8)
+                               .view(np.uint8)).cuda()
+    image, enc, entries = container.pack_device(payload, b"\x00" * 8, chunk, None, seg_shift=8)
+    jobs = container.jobs_for(entries, image.device)
+    nseg = (jobs.out_len.astype(np.int64) + 255) // 256
+    lo = np.array([(3 * i) % max(int(s), 1) for i, s in enumerate(nseg)], dtype=np.int64)
+    hi = np.minimum(nseg, lo + 1 + (nseg // 3))
+    tasks = enc.index.tasks(jobs, np.ones(jobs.n, bool), seg_range=(lo, hi))
+    out = torch.full_like(payload, 0xA5)
+    status = torch.zeros(jobs.n, dtype=torch.int32, device=payload.device)
+    engine.decode_segments(image, jobs, enc.index, tasks, out, status)
+    torch.cuda.synchronize()
+    assert int(status.abs().sum()) == 0
+    got, want = out.cpu().numpy(), payload.cpu().numpy()
+    mask = np.zeros(n_bytes, bool)
+    for c in range(jobs.n):
+        a = int(jobs.out_off[c]) + 256 * int(lo[c])
+        b = min(int(jobs.out_off[c]) + 256 * int(hi[c]), int(jobs.out_off[c] + jobs.out_len[c]))
+        mask[a:b] = True
+    assert np.array_equal(got[mask], want[mask])
+    assert (got[~mask] == 0xA5).all()
