@@ -206,7 +206,7 @@ def _pack_impl(tensors, stats, chunk_size, plan, seg_shift):
         return data, None
     payload = _device_payload(tensors)
     image, enc, _ = pack_device(payload, header, chunk_size, plan, seg_shift)
-    return nv.to_host(image).tobytes(), enc.index  # pinned D2H, then the one copy `bytes` needs
+    return nv.to_bytes(image), enc.index  # pinned D2H, then the one (parallel) copy `bytes` needs
 
 
 def pack(tensors, stats, chunk_size: int = DEFAULT_CHUNK_SIZE, plan=None) -> bytes:

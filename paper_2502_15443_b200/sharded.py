@@ -402,9 +402,10 @@ def pack_shard(tensors, stats, chunk_size: int = container.DEFAULT_CHUNK_SIZE, p
     entries["comp_len"] = clen_all
     entries["uncomp_len"] = ulen.astype(np.uint64)
     entries["crc32"] = crc_all
-    out = bytearray(first + sum(sizes))
-    out[:len(prefix)] = prefix
-    out[len(prefix):first] = entries.tobytes()
-    if sizes and sum(sizes):
-        out[first:] = body.cpu().numpy().tobytes() if body.is_cuda else body.numpy().tobytes()
-    return bytes(out)
+    from . import native as nv
+    out = np.empty(first + sum(sizes), np.uint8)
+    out[:len(prefix)] = np.frombuffer(prefix, np.uint8)
+    out[len(prefix):first] = entries.view(np.uint8)
+    if sum(sizes):
+        out[first:] = nv.to_host(body) if body.is_cuda else body.numpy()
+    return nv.host_to_bytes(out)
