@@ -189,27 +189,29 @@ constexpr int kEmitSeg = 256;  // symbols per pass-2 thread (= pass-1 record cad
 
 struct __align__(16) EncEnt {
     uint32_t rcp, xm1, xm2, sh;  // xm1 = f << 16; xm2 = f << 24 or 2^32-1 when f >= 16
-    uint32_t bias, gmul, pad0, pad1;  // gmul = 4096 - f
+    uint32_t bias, gmul, sh8, sh16;  // gmul = 4096 - f; sh8 = sh + 8, sh16 = sh + 16
 };
 
 
-// Shorter chain: q = floor(x / (f << 8n)) = mulhi(x, rcp) >> (sh + 8n) -- the
-// same reciprocal for every renorm count n (nested floor division), so the
-// IMAD.HI starts from x itself in parallel with the renorm test instead of
-// after it; x' = (x >> 8n) + cum + q * (4096 - f).  Critical path: max(IMAD.HI,
-// ISETP -> SEL -> IADD) -> SHF -> IMAD.  f == 1: x >= 2^20 > xm1 = 2^16
-// always renormalizes (8n >= 8), so rcp = 2^31 with sh = -1 gives
-// q = (x >> 1) >> (8n - 1) = x >> 8n exactly.
-__device__ __forceinline__ void enc_step_fast(uint32_t& x, uint32_t& pos, const uint4& a, const uint2& b) {
+// One reverse-encode step.  q = floor(x / (f << 8n)) = mulhi(x, rcp) >> (sh + 8n)
+// -- the same reciprocal for every renorm count n (nested floor division), so
+// the IMAD.HI starts from x itself in parallel with the renorm test -- and
+// x' = (x >> 8n) + cum + q * (4096 - f).  The shift sh + 8n is picked from
+// per-symbol copies (sh, sh + 8, sh + 16) by the renorm predicates (two SELs,
+// no add on the path): critical path max(IMAD.HI, ISETP -> SEL -> SEL) -> SHF
+// -> IMAD (595 -> 538 ms for the OPT-1.3B chains vs forming n8 then sh + n8).
+// f == 1: x >= 2^20 > xm1 = 2^16 always renormalizes (8n >= 8), so rcp = 2^31
+// with sh = -1 gives q = (x >> 1) >> (8n - 1) = x >> 8n exactly.
+__device__ __forceinline__ void enc_step(uint32_t& x, uint32_t& pos, const uint4& a, const uint4& b) {
     asm volatile(
-        "{\n\t.reg .pred p1, p2;\n\t.reg .u32 q, n1, n2, n8, s, xr;\n\t"
+        "{\n\t.reg .pred p1, p2;\n\t.reg .u32 q, n8, s, xr, n1;\n\t"
         "mul.hi.u32 q, %0, %2;\n\t"
         "setp.ge.u32 p1, %0, %3;\n\t"
         "setp.ge.u32 p2, %0, %4;\n\t"
-        "selp.u32 n1, 8, 0, p1;\n\t"
-        "selp.u32 n2, 8, 0, p2;\n\t"
-        "add.u32 n8, n1, n2;\n\t"
-        "add.u32 s, n8, %5;\n\t"
+        "selp.u32 s, %8, %5, p1;\n\t"
+        "selp.u32 s, %9, s, p2;\n\t"
+        "selp.u32 n8, 8, 0, p1;\n\t"
+        "selp.u32 n8, 16, n8, p2;\n\t"
         "shr.u32 q, q, s;\n\t"
         "shr.u32 xr, %0, n8;\n\t"
         "add.u32 xr, xr, %6;\n\t"
@@ -217,7 +219,7 @@ __device__ __forceinline__ void enc_step_fast(uint32_t& x, uint32_t& pos, const 
         "add.u32 %1, %1, n1;\n\t"
         "mad.lo.u32 %0, q, %7, xr;\n\t}"
         : "+r"(x), "+r"(pos)
-        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y));
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w));
 }
 
 // the encoder's per-symbol table for chunk c (called by one warp)
@@ -245,7 +247,7 @@ __device__ __forceinline__ void build_enc_table(const uint32_t* __restrict__ fre
             while (f > (1u << shift)) ++shift;
             e.rcp = (uint32_t)(((1ull << (shift + 31)) + f - 1) / f);
             e.sh = shift - 1;
-        } else {  // f == 1 (see enc_step_fast)
+        } else {  // f == 1 (see enc_step)
             e.rcp = 0x80000000u;
             e.sh = 0xFFFFFFFFu;
         }
@@ -253,7 +255,8 @@ __device__ __forceinline__ void build_enc_table(const uint32_t* __restrict__ fre
         e.xm2 = f < 16 ? f << 24 : 0xFFFFFFFFu;
         e.bias = cum;
         e.gmul = kProbScale - f;
-        e.pad0 = e.pad1 = 0;
+        e.sh8 = e.sh + 8u;  // shift amounts for one / two renorm bytes (enc_step)
+        e.sh16 = e.sh + 16u;
         T[lane * 8 + k] = e;
         cum += f;
     }
@@ -305,9 +308,9 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __rest
         --i;
         const uint32_t sy = src[i];
         const uint4 ea = *reinterpret_cast<const uint4*>(&T[sy].rcp);
-        const uint2 eb = *reinterpret_cast<const uint2*>(&T[sy].bias);
+        const uint4 eb = *reinterpret_cast<const uint4*>(&T[sy].bias);
         if (lead) xsc[i] = x;
-        enc_step_fast(x, pos, ea, eb);
+        enc_step(x, pos, ea, eb);
         record(i);
         if (pos >= limit) stored = true;
     }
@@ -330,18 +333,18 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __rest
         const uint32_t wv[4] = {cur.x, cur.y, cur.z, cur.w};
         // table entries of the whole block first (they do not depend on x), then the chain
         uint4 ea[16];
-        uint2 eb[16];
+        uint4 eb[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             const uint32_t sy = (wv[k >> 2] >> (8 * (k & 3))) & 0xFF;
             ea[k] = *reinterpret_cast<const uint4*>(&T[sy].rcp);
-            eb[k] = *reinterpret_cast<const uint2*>(&T[sy].bias);
+            eb[k] = *reinterpret_cast<const uint4*>(&T[sy].bias);
         }
         uint32_t xin[16];
 #pragma unroll
         for (int k = 15; k >= 0; --k) {
             xin[k] = x;
-            enc_step_fast(x, pos, ea[k], eb[k]);
+            enc_step(x, pos, ea[k], eb[k]);
         }
         if (lead) {
             uint32_t* dst = xsc + 16 * b;
