@@ -404,13 +404,23 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
         const int pc = k * 32 + lane;
         dk[k] = ((uint32_t)(warp * 32 + ((pc >> 1) & 31) + (pc >> 6) * TH) << seg_shift) + (pc & 1) * 16;
     }
+    // groups [0, g_full) are whole 16-symbol groups for every chain of the
+    // warp (one warp-wide min instead of a vote per group)
+    uint32_t my_full = 0xFFFFFFFFu;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) my_full = min(my_full, n[u] == 0 ? 0xFFFFFFFFu : n[u] >> 4);
+    const int g_full = (int)__reduce_min_sync(0xffffffffu, my_full);
+    // staging slots of this lane's segments (shared addresses, loop-invariant)
+    uint32_t stg[NU][2];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        stg[u][0] = smem_u32(ob) + swz(u * 32 + lane, 0);
+        stg[u][1] = smem_u32(ob) + swz(u * 32 + lane, 1);
+    }
     for (int g = 0; g < G; ++g) {
         const uint32_t g0 = (uint32_t)g << 4;
         uint32_t w[NU][4];
-        bool full = true;
-#pragma unroll
-        for (int u = 0; u < NU; ++u) full = full && (n[u] == 0 || g0 + 16 <= n[u]);
-        if (__all_sync(0xffffffffu, full)) {
+        if (g < g_full) {
 #pragma unroll
             for (int v = 0; v < 16; v += 2) {  // step pairs share one window word
                 uint32_t wv[NU], sel[NU];
@@ -462,8 +472,9 @@ __device__ __forceinline__ void decode_warp(uint32_t seg_shift, int s0, int ns, 
         const int slot = g & 1;
 #pragma unroll
         for (int u = 0; u < NU; ++u)
-            *reinterpret_cast<uint4*>(ob + swz(u * 32 + lane, slot)) =
-                make_uint4(w[u][0], w[u][1], w[u][2], w[u][3]);
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg[u][slot]), "r"(w[u][0]),
+                         "r"(w[u][1]), "r"(w[u][2]), "r"(w[u][3])
+                         : "memory");
         if (slot == 1) {  // G is even (K >= 64)
             __syncwarp();
             const uint32_t line0 = (uint32_t)(g >> 1) * kOutLine;
