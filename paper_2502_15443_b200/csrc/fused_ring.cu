@@ -205,22 +205,6 @@ __device__ __forceinline__ void fwin_advance_g(Chain& c, uint32_t s) {
 }
 __device__ __forceinline__ void fwin_rebase(Chain& c) { c.o -= 8u * 0x10820u; }
 
-// fwin_advance with the moves and the offset wrap on the FMA pipe (see
-// win_advance(Win&, s, FmaK) in rans_common.cuh)
-__device__ __forceinline__ void fwin_advance(Chain& c, uint32_t s, const FmaK& k) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t.reg .u32 a;\n\t"
-        "mad.lo.u32 %3, %5, 8, %3;\n\t"
-        "setp.ge.u32 q, %3, 0x10840;\n\t"
-        "@q mad.lo.u32 %0, %1, %6, 0;\n\t"
-        "@q mad.lo.u32 %2, %6, 4, %2;\n\t"
-        "lop3.b32 a, %2, 127, %4, 0xEA;\n\t"
-        "@q ld.shared.u32 %1, [a];\n\t"
-        "@q mad.lo.u32 %3, %6, -32, %3;\n\t"
-        "add.u32 %3, %3, -67616;\n\t}"
-        : "+r"(c.w0), "+r"(c.w1), "+r"(c.pr), "+r"(c.o)
-        : "r"(c.rb), "r"(s), "r"(k.c1));
-}
 
 #ifndef DC_FUSED_CLAMP
 #define DC_FUSED_CLAMP 1  // never request stream bytes past the chain's end (+ the window's 8-byte look-ahead)

@@ -225,46 +225,13 @@ __device__ __forceinline__ void win_advance(Win& w, uint32_t s) {
         : "r"(s));
 }
 
-// win_advance with the window moves and the offset wrap on the FMA pipe
-// (IMAD by the opaque 1 / VIADD) instead of SEL + LOP3 on the ALU pipe, which
-// the decode loop saturates.  o stays in [0, 32): o + 8s - 8*kSelBase, minus
-// 32 when a word was crossed.
-__device__ __forceinline__ void win_advance(Win& w, uint32_t s, const FmaK& k) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t"
-        "mad.lo.u32 %3, %4, 8, %3;\n\t"
-        "setp.ge.u32 q, %3, 0x10840;\n\t"
-        "@q mad.lo.u32 %0, %1, %5, 0;\n\t"
-        "@q mad.lo.u32 %2, %5, 4, %2;\n\t"
-        "@q ld.shared.u32 %1, [%2];\n\t"
-        "@q mad.lo.u32 %3, %5, -32, %3;\n\t"
-        "add.u32 %3, %3, -67616;\n\t}"
-        : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
-        : "r"(s), "r"(k.c1));
-}
-
 // Fast-path advance for pair J (0..7) of a 16-symbol group.  o is not
 // re-biased per pair: it carries the selector bias of the J+1 pairs so far
 // (8 * kSelBase = 0x10820 each, a multiple of 32, so SHF.R.W's shift amount
 // o mod 32 is unaffected), the crossing test compares against a per-pair
 // immediate, and win_rebase() removes the 8 pairs' bias once per group.  The
-// word move is one SEL plus a predicated LDS and two predicated adds (no
-// if-converted IMAD/SEL pairs): 6 instructions per pair instead of 9.
-template <int J>
-__device__ __forceinline__ void win_advance_g(Win& w, uint32_t s) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t"
-        "mad.lo.u32 %3, %4, 8, %3;\n\t"
-        "setp.ge.u32 q, %3, %5;\n\t"
-        "selp.b32 %0, %1, %0, q;\n\t"
-        "@q ld.shared.u32 %1, [%2+4];\n\t"
-        "@q add.u32 %2, %2, 4;\n\t"
-        "@q add.u32 %3, %3, -32;\n\t}"
-        : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
-        : "r"(s), "n"(32u + (J + 1) * 0x10820u));
-}
-// Same with the word move as a predicated IMAD by an opaque 1 (FMA pipe)
-// instead of SEL (ALU pipe).
+// word move is a predicated IMAD by an opaque 1 (FMA pipe; a SEL would load
+// the busy ALU pipe) plus a predicated LDS and two predicated adds.
 template <int J>
 __device__ __forceinline__ void win_advance_gf(Win& w, uint32_t s, uint32_t one) {
     asm volatile(
@@ -280,49 +247,6 @@ __device__ __forceinline__ void win_advance_gf(Win& w, uint32_t s, uint32_t one)
 }
 __device__ __forceinline__ void win_rebase(Win& w) { w.o -= 8u * 0x10820u; }
 
-// Same inside a 128-byte ring (fused kernel): the word address wraps.
-__device__ __forceinline__ void win_advance_ring(Win& w, uint32_t s) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t.reg .u32 n;\n\t"
-        "mad.lo.u32 %3, %4, 8, %3;\n\t"
-        "setp.ge.u32 q, %3, 0x10840;\n\t"
-        "@q mov.b32 %0, %1;\n\t"
-        "@q add.u32 n, %2, 4;\n\t"
-        "@q lop3.b32 %2, n, %2, 127, 0xE4;\n\t"
-        "@q ld.shared.u32 %1, [%2];\n\t"
-        "and.b32 %3, %3, 31;\n\t}"
-        : "+r"(w.w0), "+r"(w.w1), "+r"(w.wa), "+r"(w.o)
-        : "r"(s));
-}
-
-template <bool kConverged>
-__device__ __forceinline__ uint32_t dec_step(uint32_t& x, uint32_t& p, uint32_t& nb, uint32_t tab) {
-    uint32_t e;
-    // 16 SASS instructions: LOP3, LEA.HI, IMAD, LDS, 2x SHF, IMAD, then two
-    // predicated refills (ISETP + IADD + IMAD + LDS.U8 each).  The second
-    // refill is rare (f < 16) and only its predicate differs between lanes.
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t.reg .u32 a, f, b, t;\n\t"
-        "and.b32 a, %0, 4095;\n\t"
-        "mad.lo.u32 a, a, 4, %4;\n\t"
-        "ld.shared.u32 %3, [a];\n\t"
-        "shr.u32 f, %3, 20;\n\t"
-        "shr.u32 b, %3, 8;\n\t"
-        "shr.u32 t, %0, 12;\n\t"
-        "sub.u32 t, t, 4096;\n\t"
-        "mad.lo.u32 %0, f, t, b;\n\t"
-        "setp.lt.u32 q, %0, 0x100000;\n\t"
-        "@q mad.lo.u32 %0, %0, 256, %2;\n\t"
-        "@q add.u32 %1, %1, 1;\n\t"
-        "@q ld.shared.u8 %2, [%1];\n\t"
-        "setp.lt.u32 q, %0, 0x100000;\n\t"
-        "@q mad.lo.u32 %0, %0, 256, %2;\n\t"
-        "@q add.u32 %1, %1, 1;\n\t"
-        "@q ld.shared.u8 %2, [%1];\n\t}"
-        : "+r"(x), "+r"(p), "+r"(nb), "=r"(e)
-        : "r"(tab));
-    return e;
-}
 
 __device__ __forceinline__ uint32_t put_byte(uint32_t w, uint32_t e, int k) {
     // byte k of the result <- byte 0 of e (PRMT)
