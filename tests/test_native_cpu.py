@@ -167,3 +167,18 @@ def test_choose_architecture_reference_cases():
     assert dc.choose_architecture(profile(mem_gpu=10.0), 6.0, 4.0) is A.GPU_BUFFER
     assert dc.choose_architecture(profile(mem_gpu=10.0, mem_cpu=5.0), 6.0, 5.0) is A.GPU_CPU
     assert dc.choose_architecture(profile(mem_gpu=10.0, mem_cpu=5.0), 11.0, 5.0) is A.STORAGE
+
+
+def test_host_to_bytes_parallel_fill():
+    """pack's result: a bytes object filled in place by parallel slice copies
+    (above 64 MiB) equals numpy's tobytes, hashes and compares like any bytes,
+    and small inputs take the plain path."""
+    import numpy as np
+
+    from paper_2502_15443_b200 import native as nv
+    assert nv._BYTES_OFF is not None
+    for n in (0, 1000, (64 << 20) + 12345):
+        a = np.random.default_rng(n).integers(0, 256, n, dtype=np.uint8)
+        b = nv.host_to_bytes(a)
+        assert type(b) is bytes and len(b) == n
+        assert b == a.tobytes() and hash(b) == hash(a.tobytes())
