@@ -11,7 +11,8 @@ import torch  # noqa: E402
 from paper_2502_15443_b200 import engine, synth  # noqa: E402
 
 layers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-m = synth.build_model("opt-1.3b", layers=layers)
+model = sys.argv[2] if len(sys.argv) > 2 else "opt-1.3b"
+m = synth.build_model(model, layers=layers or None)
 pm = synth.pack_model(m, 16 << 20, seg_shift=None)
 for i in range(2):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
