@@ -191,8 +191,11 @@ int dc_assemble_payloads(const uint8_t *data, uint64_t total, uint64_t chunk_siz
  */
 
 /* max |W[r,c] * s[c]| as the bits of a non-negative f64 (exact: max is
- * order-free), plus a non-finite flag.  replaces scaling.py:78-81 (W*s) and
- * :99 (np.abs(v).max()); WeightTensor's isfinite check (tensors.py:33-34). */
+ * order-free), plus a non-finite flag.  f32 / bf16 / f16 inputs with cols % 8
+ * == 0 take a streaming column-max pass: max|W*s| = max_c RN(max_r |W[r,c]| *
+ * s[c]) since IEEE rounding is monotone and s > 0.  replaces scaling.py:78-81
+ * (W*s) and :99 (np.abs(v).max()); WeightTensor's isfinite check
+ * (tensors.py:33-34). */
 int dc_quant_absmax(const void *w, int dtype, const double *s, int64_t rows, int64_t cols,
                     unsigned long long *absmax_bits, int *nonfinite, void *stream);
 

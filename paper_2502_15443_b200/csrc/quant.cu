@@ -238,7 +238,10 @@ __global__ void __launch_bounds__(kQThreads) k_absmax_v(const typename In<T>::ty
     const int64_t cg = t % gpr, rp = t / gpr;
     double sc[8];
     load_s8(s, cg * 8, sc);
-    constexpr int kQR = T == kF64 ? 2 : 4;  // rows in flight per thread (see k_quantize_v)
+#ifndef DC_ABSMAX_ROWS_H
+#define DC_ABSMAX_ROWS_H 4
+#endif
+    constexpr int kQR = T == kF64 ? 2 : (sizeof(typename In<T>::type) == 2 ? DC_ABSMAX_ROWS_H : 4);  // rows in flight per thread
     for (int64_t r0 = rp; r0 < rows && rp < rows_par; r0 += kQR * rows_par) {
         Raw8<T> v[kQR];
 #pragma unroll
@@ -333,7 +336,10 @@ __global__ void __launch_bounds__(kQThreads, DC_QUANT_MINB) k_quantize_v(const t
 #ifndef DC_QUANT_PF
 #define DC_QUANT_PF 1  // rows ahead whose warp span is bulk-prefetched into L2 (0: off)
 #endif
-        constexpr int kQR = DC_QUANT_ROWS;
+#ifndef DC_QUANT_ROWS_H
+#define DC_QUANT_ROWS_H 1  // rows in flight per thread for 2-byte inputs (bf16 / f16)
+#endif
+        constexpr int kQR = sizeof(typename In<T>::type) == 2 ? DC_QUANT_ROWS_H : DC_QUANT_ROWS;
         // the warp's 32 consecutive 8-column groups are one contiguous span of
         // a row (when they do not wrap): lane 0 bulk-prefetches the span
         // DC_QUANT_PF rows ahead into L2, so more bytes are in flight than the
@@ -373,6 +379,102 @@ __global__ void __launch_bounds__(kQThreads, DC_QUANT_MINB) k_quantize_v(const t
                 *reinterpret_cast<uint2*>(q + r * cols + cg * 8) = make_uint2(lo, hi);
             }
         }
+    }
+}
+
+// ---- column-max absmax (f32 / bf16 / f16 inputs) ---------------------------
+// max |W[r,c] * s[c]| over the tensor equals max over columns of
+// RN(max_r |W[r,c]| * s[c]): IEEE rounding is monotone and s > 0.  So the
+// pass over the tensor only keeps per-column maxima of the magnitude bits
+// (integer max on |x|'s bit pattern, monotone for finite values, and inf /
+// NaN patterns sort above every finite one), two 16-bit lanes per instruction
+// for bf16 / f16 (max.u16x2); each CTA then forms the f64 products for the
+// column maxima of its row block only and contributes one atomic max (the max
+// of those over CTAs is the tensor's).  The tensor pass is a pure streaming read.
+constexpr int kCmCols = 256;  // columns per CTA tile: 32 lanes x 8
+constexpr int kCmRows = 4;    // rows in flight per warp iteration
+
+template <int T>
+__global__ void __launch_bounds__(kQThreads) k_absmax_cols(const typename In<T>::type* __restrict__ w,
+                                                            const double* __restrict__ s, int64_t rows, int64_t cols,
+                                                            int64_t rows_per_blk, unsigned long long* __restrict__ out,
+                                                            int* __restrict__ nonfinite) {
+    constexpr bool kHalf = sizeof(typename In<T>::type) == 2;
+    constexpr int kWords = kHalf ? 4 : 8;  // 32-bit words per lane per row (8 columns)
+    __shared__ uint32_t red[kQThreads / 32][kCmCols];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c0 = (int64_t)blockIdx.x * kCmCols + lane * 8;
+    const int64_t r_begin = (int64_t)blockIdx.y * rows_per_blk;
+    const int64_t r_end = min(rows, r_begin + rows_per_blk);
+    uint32_t m[kWords];
+#pragma unroll
+    for (int k = 0; k < kWords; ++k) m[k] = 0;
+    if (c0 < cols) {
+        const uint4* base = reinterpret_cast<const uint4*>(w + c0);
+        const int64_t row_vec = cols * (int64_t)sizeof(typename In<T>::type) / 16;  // uint4 per row
+        for (int64_t r0 = r_begin + warp; r0 < r_end; r0 += kCmRows * (kQThreads / 32)) {
+            uint4 v[kCmRows][kWords / 4];
+#pragma unroll
+            for (int j = 0; j < kCmRows; ++j) {
+                const int64_t r = r0 + j * (kQThreads / 32);
+#pragma unroll
+                for (int h = 0; h < kWords / 4; ++h)
+                    v[j][h] = r < r_end ? __ldg(base + r * row_vec + h) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int j = 0; j < kCmRows; ++j) {
+#pragma unroll
+                for (int h = 0; h < kWords / 4; ++h) {
+                    const uint32_t x[4] = {v[j][h].x, v[j][h].y, v[j][h].z, v[j][h].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if constexpr (kHalf) {
+                            uint32_t a = x[k] & 0x7FFF7FFFu, d;
+                            asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(m[4 * h + k]), "r"(a));
+                            m[4 * h + k] = d;
+                        } else {
+                            m[4 * h + k] = max(m[4 * h + k], x[k] & 0x7FFFFFFFu);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    // column maxima of this warp -> shared, max over the CTA's warps, one atomic per column
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        red[warp][lane * 8 + k] = kHalf ? ((m[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) : m[k];
+    __syncthreads();
+    // this CTA's column maxima (over its row block) -> RN(|x| * s[c]) -> CTA max
+    // -> one atomic: the max over CTAs of these is the tensor's max|W*s|
+    constexpr uint32_t kInf = T == kF32 ? 0x7F800000u : (T == kBF16 ? 0x7F80u : 0x7C00u);
+    const int t = threadIdx.x;
+    uint32_t b = 0;
+#pragma unroll
+    for (int q = 0; q < kQThreads / 32; ++q) b = max(b, red[q][t]);
+    const int64_t c = (int64_t)blockIdx.x * kCmCols + t;
+    double a = 0.0;
+    const bool bad = c < cols && b >= kInf;
+    if (c < cols && b && !bad) {
+        double v;
+        if constexpr (T == kF32) v = (double)__uint_as_float(b);
+        else if constexpr (T == kBF16) v = (double)__uint_as_float(b << 16);
+        else v = (double)__half2float(__ushort_as_half((uint16_t)b));
+        a = s ? __dmul_rn(v, __ldg(s + c)) : v;
+    }
+    __shared__ double dred[kQThreads / 32];
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, a, d);
+        a = o > a ? o : a;
+    }
+    if ((t & 31) == 0) dred[t >> 5] = a;
+    const int anybad = __syncthreads_or(bad);
+    if (t == 0) {
+        double m = 0.0;
+        for (int i = 0; i < kQThreads / 32; ++i) m = dred[i] > m ? dred[i] : m;
+        if (m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+        if (anybad) atomicExch(nonfinite, 1);
     }
 }
 
@@ -560,6 +662,21 @@ extern "C" int dc_quant_absmax(const void* w, int dtype, const double* s, int64_
     cudaMemsetAsync(absmax_bits, 0, sizeof(unsigned long long), st);
     cudaMemsetAsync(nonfinite, 0, sizeof(int), st);
     if (rows == 0 || cols == 0) return DC_OK;
+    if (dtype != kF64 && vec_ok(w, s, cols, nullptr)) {  // f32 / bf16 / f16: column-max streaming pass
+        const int64_t tiles = (cols + kCmCols - 1) / kCmCols;
+        int64_t blocks_y = ((int64_t)sm_count() * 8 + tiles - 1) / tiles;  // ~8 CTAs per SM
+        if (blocks_y > rows) blocks_y = rows;
+        const int64_t rows_per_blk = (rows + blocks_y - 1) / blocks_y;
+        blocks_y = (rows + rows_per_blk - 1) / rows_per_blk;
+        const dim3 grid((unsigned)tiles, (unsigned)blocks_y);
+        switch (dtype) {
+            case kF32: k_absmax_cols<kF32><<<grid, kQThreads, 0, st>>>((const float*)w, s, rows, cols, rows_per_blk, absmax_bits, nonfinite); break;
+            case kBF16: k_absmax_cols<kBF16><<<grid, kQThreads, 0, st>>>((const __nv_bfloat16*)w, s, rows, cols, rows_per_blk, absmax_bits, nonfinite); break;
+            default: k_absmax_cols<kF16><<<grid, kQThreads, 0, st>>>((const __half*)w, s, rows, cols, rows_per_blk, absmax_bits, nonfinite); break;
+        }
+        DC_CHECK_LAUNCH("k_absmax_cols");
+        return DC_OK;
+    }
     if (vec_ok(w, s, cols, nullptr)) {
         int64_t rp;
         unsigned g;

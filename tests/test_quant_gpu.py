@@ -232,3 +232,30 @@ def test_analyze_quantized_gpu_equals_reference(cuda):
         check_report(dataclasses.asdict(cuda.analyze_quantized(qt)), gold[name])
     with pytest.raises(cuda.DcompError):
         cuda.analyze_quantized(np.zeros((0, 3), np.int8))
+
+
+@pytest.mark.parametrize("shape", [(300, 264), (1500, 1000), (64, 4104), (1200, 2048)])
+def test_column_max_absmax_equals_f64(cuda, shape):
+    """f32 / bf16 / f16 absmax through the column-max pass (cols % 8 == 0):
+    max|W*s| bit-equal to the f64 elementwise formula (max over columns of
+    RN(max|W[:,c]| * s[c]) -- rounding is monotone), the max placed in
+    different columns and rows, and the non-finite flag for inf and NaN."""
+    from paper_2502_15443_b200.scaling import _absmax
+    rng = np.random.default_rng(shape[1])
+    rows, cols = shape
+    s = torch.from_numpy(rng.uniform(0.05, 3.0, cols)).cuda()
+    for dt in (torch.float32, torch.bfloat16, torch.float16):
+        for trial in range(3):
+            w = torch.from_numpy(rng.normal(0, 0.2, (rows, cols)).astype(np.float32)).to(dt).cuda()
+            r, c = int(rng.integers(rows)), int(rng.integers(cols))
+            w[r, c] = -1.5 if trial == 1 else w[r, c]
+            wide = w.to(torch.float64).cpu().numpy() * s.cpu().numpy()
+            want = float(np.abs(wide).max())
+            got, bad = _absmax(w, s)
+            assert not bad and got == want, (dt, trial, got, want)
+            got_f64, _ = _absmax(w.to(torch.float64), s)
+            assert got_f64 == got
+        for v in (float("inf"), float("nan"), float("-inf")):
+            w2 = w.clone()
+            w2[rows // 2, cols - 1] = v
+            assert _absmax(w2, s)[1], (dt, v)
